@@ -1,0 +1,218 @@
+/*
+ * nvol.h — C ABI of libnvol.so, the B200 (sm_100a) implementation of the
+ * hash-grid encoder + ReLU MLP training step, full-grid decode and macro-cell
+ * ray marching of the arXiv 2207.11620 CPU reference
+ * (/root/reference/pkg/src/neuralvol).
+ *
+ * Every entry point replaces one numba kernel (or one numpy step) of the
+ * reference; the reference symbol is cited beside each declaration.  The
+ * reference's "FFI" is numba's: caller-allocated arrays, no return value.  Here
+ * every function takes plain device pointers + sizes, returns an int status
+ * and runs asynchronously on the caller's stream:
+ *
+ *   NVOL_OK (0)            enqueued
+ *   NVOL_EINVAL (1)        bad argument        -> ConfigError (errors.py:9-10)
+ *   NVOL_ECUDA (2)         CUDA launch failure -> RuntimeError
+ *
+ * nvol_last_error() returns a static description of the last failure.
+ *
+ * Ownership: the caller owns every buffer (PyTorch allocates them); the
+ * library allocates nothing except transient tensor memory (TMEM) inside
+ * kernels.  Pointers are device pointers unless marked [host].  `stream` is a
+ * cudaStream_t (0 = legacy default stream).  Calls are re-entrant per stream.
+ *
+ * Layouts (all little-endian, row-major, matching the reference):
+ *   coords      f32/f64 [B,3] in [0,1)^3, x fastest              (sampler.py:33-38)
+ *   params      encoder table, level-major / entry-major / feature-minor
+ *               (encoding.py:145-169), followed in the flat training
+ *               buffer by each W_i (out x in) row-major             (trainer.py:114-123)
+ *   level_*     the four per-level arrays of GridEncoder.kernel_tables()
+ *               (encoding.py:174-177) [host]
+ *   volume      normalised f32 [Dz,Dy,Dx], x fastest                (volume.py:99-107)
+ */
+#ifndef NVOL_H
+#define NVOL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NVOL_OK 0
+#define NVOL_EINVAL 1
+#define NVOL_ECUDA 2
+#define NVOL_MAX_LEVELS 32
+
+/* ------------------------------------------------------------------ library */
+
+/* ABI version (bumped on any signature change). */
+int nvol_abi_version(void);
+/* Static string describing the last non-zero status (thread-local). */
+const char *nvol_last_error(void);
+/* 1 when the tcgen05 tensor-core MLP is compiled in and usable on `device`. */
+int nvol_has_tcgen05(int device);
+
+/* ------------------------------------------------------------------ encoder */
+
+/* _kernels.py:31-79 grid_encode_fwd (called from model.py:136-150).
+ * dtype_bytes = 4 (f32 coords/params/out/w_cache) or 8 (f64 path of
+ * encoding.py:203-213, used for gradient checks).  idx_cache (i64 [B,m,8],
+ * flat element offset of each corner row) and w_cache ([B,m,8]) may be NULL.
+ * Float32 results are bit-identical to the reference. */
+int nvol_grid_encode_fwd(const void *coords, int64_t b, const void *params,
+                         const int64_t *level_off, const int64_t *level_res,
+                         const int64_t *level_entries, const uint8_t *level_dense,
+                         int32_t n_levels, int32_t n_feat, int64_t *idx_cache, void *w_cache,
+                         void *out, int32_t dtype_bytes, void *stream);
+
+/* _kernels.py:82-92 grid_encode_bwd: grad_out[idx+f] += w * dl_dfeat[i, l*n+f]
+ * (accumulating).  Float atomics: order-dependent in the last ulp. */
+int nvol_grid_encode_bwd(const void *dl_dfeat, const int64_t *idx_cache, const void *w_cache,
+                         int64_t b, int32_t n_levels, int32_t n_feat, void *grad_out,
+                         int32_t dtype_bytes, void *stream);
+
+/* encoding.py:215-226 encode_backward, recomputing corners from coords
+ * (no caches).  deterministic != 0 reproduces the reference's serial scatter
+ * order exactly (float32 only): bit-identical to _kernels.grid_encode_bwd. */
+int nvol_grid_encode_bwd_coords(const void *coords, const void *dl_dfeat, int64_t b,
+                                const int64_t *level_off, const int64_t *level_res,
+                                const int64_t *level_entries, const uint8_t *level_dense,
+                                int32_t n_levels, int32_t n_feat, void *grad_out,
+                                int32_t dtype_bytes, int32_t deterministic, void *stream);
+
+/* ------------------------------------------------------------------ MLP, loss, optimizer */
+
+/* network.py:61-74 Mlp.forward.  weights[i] -> W_i (widths[i+1] x widths[i]);
+ * acts[i] -> activation buffer i ([B, widths[i]]); acts[0] is the input and
+ * acts[n_layers] the output.  [host] arrays of device pointers. */
+int nvol_mlp_forward(int64_t b, int32_t n_layers, const int32_t *widths, const void *const *weights,
+                     void *const *acts, int32_t relu_out, int32_t dtype_bytes, void *stream);
+
+/* network.py:76-93 Mlp.backward.  dl_dout [B] (output width 1); grads[i] are
+ * accumulated; dl_dinput [B, widths[0]]; scratch: two buffers of
+ * B x max(widths) elements. */
+int nvol_mlp_backward(int64_t b, int32_t n_layers, const int32_t *widths, const void *const *weights,
+                      const void *const *acts, const void *dl_dout, void *const *grads,
+                      void *dl_dinput, void *scratch0, void *scratch1, int32_t relu_out,
+                      int32_t dtype_bytes, void *stream);
+
+/* network.py:96-114 loss_and_grad.  kind 0 = L1, 1 = L2.  Differences in
+ * f64; grad written in the pred dtype; *loss_sum (f64, device) receives the
+ * sum of |d| (L1) or d^2 (L2) — accumulated, caller zeroes. */
+int nvol_loss_and_grad(const void *pred, const void *target, int64_t b, int32_t kind,
+                       void *grad, double *loss_sum, int32_t dtype_bytes, void *stream);
+
+/* Same, with the gradient divided by b_global instead of b (data-parallel
+ * shard of a global batch: network.py:108 grad = sign(d) / B_global). */
+int nvol_loss_and_grad_scaled(const void *pred, const void *target, int64_t b, int64_t b_global,
+                              int32_t kind, void *grad, double *loss_sum, int32_t dtype_bytes,
+                              void *stream);
+
+/* trainer.py:61-77 history bookkeeping on the device: losses[*step_counter - t0]
+ * = *acc * inv_b, then *acc = 0 (CUDA-graph friendly). */
+int nvol_loss_record(double *acc, double *losses, const int64_t *step_counter, int64_t t0,
+                     int64_t cap, double inv_b, void *stream);
+
+/* network.py:160-183 adam_step on one flat group; scalars are the
+ * dtype-cast values the reference computes on the host (lr_at, c1, c2 ...).
+ * Bit-identical to the reference; zeroes g. */
+int nvol_adam_step(void *p, void *g, void *m, void *v, int64_t n, double lr, double beta1,
+                   double one_minus_beta1, double beta2, double one_minus_beta2, double c1,
+                   double c2, double eps, double l2, int32_t dtype_bytes, void *stream);
+
+/* network.py:167-171: index of the first NaN in g (or -1), written to *first. */
+int nvol_find_nan(const void *g, int64_t n, int64_t *first, int32_t dtype_bytes, void *stream);
+
+/* ------------------------------------------------------------------ sampling, volumes, metrics */
+
+/* sampler.py:54-74 sample_incore with the reference's numpy PCG64 stream:
+ * coords are float32 draws u32_offset .. u32_offset+3B of default_rng(seed)
+ * (initial (state, inc) passed as four u64 words); targets are the clamped
+ * cell-centred trilinear reads of volume.py:148-164.  Bit-identical. */
+int nvol_sample_incore(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                       uint64_t u32_offset, int64_t b, const float *volume, int64_t dx,
+                       int64_t dy, int64_t dz, float *coords, float *targets, void *stream);
+
+/* Same stream, step counter read from device memory (CUDA-graph friendly):
+ * u32 offset = u32_base + (*step_counter - counter0) * 3 * b_global + 3 * row0
+ * (rows [row0, row0+b) of a global batch of b_global: the data-parallel shard
+ * of one rank reproduces exactly those rows of the single-process batch). */
+int nvol_sample_incore_dev(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                           uint64_t u32_base, const int64_t *step_counter, int64_t counter0, int64_t b_global,
+                           int64_t row0, int64_t b,
+                           const float *volume, int64_t dx, int64_t dy, int64_t dz, float *coords,
+                           float *targets, void *stream);
+
+/* volume.py:167-171 sample_trilinear_many (no clamp). */
+int nvol_trilinear(const float *volume, int64_t dx, int64_t dy, int64_t dz, const float *pts,
+                   int64_t n, float *out, void *stream);
+
+/* fields.py:67-88 rasterize: field 0 gauss, 1 blobs, 2 waves, 3 mlobb, f64
+ * evaluation at voxel centres, clipped, stored as f32 (out_u8 = 0) or as
+ * round(v*255) u8 (out_u8 = 1); rows [z0, z0+nz). */
+int nvol_rasterize(int32_t field, int64_t dx, int64_t dy, int64_t dz, int64_t z0, int64_t nz,
+                   void *out, int32_t out_u8, void *stream);
+
+/* volume.py:197-207 mse numerator: *sum += sum((a-b)^2) over n normalised
+ * values, f64 accumulation. */
+int nvol_sq_err_sum(const float *a, const float *b, int64_t n, double *sum, void *stream);
+
+/* ------------------------------------------------------------------ fused field evaluation / decode */
+
+/* _kernels.py:154-176 field_eval_model == NeuralModel.eval_fused
+ * (model.py:184-198): per-sample encode + serial float32 matvec chain,
+ * bit-identical to the reference.  weights: flat concatenation of W_i. */
+int nvol_field_eval_exact(const float *coords, int64_t b, const float *params,
+                          const int64_t *level_off, const int64_t *level_res,
+                          const int64_t *level_entries, const uint8_t *level_dense,
+                          int32_t n_levels, int32_t n_feat, const float *weights,
+                          const int32_t *widths, int32_t n_layers, int32_t relu_out,
+                          float *out, void *stream);
+
+/* trainer.py:80-106 decode_slabs over voxel-centre coordinates of the brick
+ * [z0, z0+nz) of a (dx,dy,dz) grid: out[k] = Phi * (hi-lo) + lo (f64 then f32).
+ * mode 0 = exact (serial fp32, == eval_fused), 1 = tensor-core (tcgen05,
+ * fp16 operands / fp32 accumulate). */
+int nvol_decode(const float *params, const int64_t *level_off, const int64_t *level_res,
+                const int64_t *level_entries, const uint8_t *level_dense, int32_t n_levels,
+                int32_t n_feat, const float *weights, const int32_t *widths, int32_t n_layers,
+                int32_t relu_out, int64_t dx, int64_t dy, int64_t dz, int64_t z0, int64_t nz,
+                double lo, double hi, float *out, int32_t mode, void *stream);
+
+/* ------------------------------------------------------------------ fused training step */
+
+/* One NeuralModel.train_step (model.py:154-174) as a device-resident pipeline
+ * over a flat parameter buffer [enc | pad | W_0 | W_1 ... ] (and equally
+ * laid-out grad, m, v buffers), where W_0 starts at the encoder parameter
+ * count rounded up to a multiple of 4 floats (16-byte aligned):  encode -> MLP -> loss -> backprop -> encoder scatter.  The
+ * Adam update is a separate call (nvol_adam_step over the flat buffer) so a
+ * data-parallel caller can all-reduce `grads` in between.
+ * coords/targets: [b] rows of this rank; grad_scale = 1/B_global (L1 sign
+ * gradient, network.py:108).  loss_sum (f64) accumulates sum |pred-target|.
+ * mode 0 = SIMT fp32, 1 = tcgen05 (fp16 operands, fp32 accumulate). */
+int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int64_t b_global,
+                       const float *params, float *grads, const int64_t *level_off,
+                       const int64_t *level_res, const int64_t *level_entries,
+                       const uint8_t *level_dense, int32_t n_levels, int32_t n_feat,
+                       int32_t n_neurons, int32_t n_hidden, int32_t relu_out, int32_t loss_kind,
+                       double *loss_sum, void *workspace, int64_t workspace_bytes, int32_t mode,
+                       void *stream);
+
+/* Workspace bytes nvol_train_fwd_bwd needs for batch b. */
+int64_t nvol_train_workspace_bytes(int64_t b, int32_t n_levels, int32_t n_feat, int32_t n_neurons,
+                                   int32_t n_hidden, int32_t mode);
+
+/* Flat-buffer Adam step reading the step counter from device memory (for
+ * CUDA-graph replay) and a per-step scalar table sched[t] = {lr, c1, c2} as
+ * f32 cast on the host exactly like network.py:163-181; increments
+ * *step_counter.  nan_flag (u32, nullable) is set when any g is NaN. */
+int nvol_adam_flat_dev(float *p, float *g, float *m, float *v, int64_t n, const float *sched,
+                       int64_t sched_len, int64_t *step_counter, float beta1, float one_minus_beta1,
+                       float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
+                       void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NVOL_H */

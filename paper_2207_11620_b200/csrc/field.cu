@@ -1,0 +1,261 @@
+// Exact fused field evaluation (encode + MLP per sample) and full-grid decode.
+//
+// Reference: _kernels.py:95-176 (_mlp_row, _field_one, field_eval_model ==
+// NeuralModel.eval_fused, model.py:184-198) and trainer.py:80-106 (decode).
+// One thread per sample, float32 throughout, each dot product folded in k
+// order without FMA contraction: bit-identical to the reference's numba
+// evaluator.  Weights are staged once per CTA in shared memory, transposed
+// (k-major) so the inner j loop reads a broadcast float4.
+#include "common.cuh"
+
+namespace nvol {
+
+struct MlpShape {
+    int32_t n_layers;
+    int32_t widths[12];
+    int32_t relu_out;
+};
+
+constexpr int FE_THREADS = 128;
+
+// Encode one sample into feat[k * FE_THREADS] (column of this thread).
+__device__ __forceinline__ void encode_exact(float x, float y, float z, const float *__restrict__ params,
+                                             const GridTables &tab, float *feat) {
+    const int m = tab.n_levels, n = tab.n_feat;
+    for (int l = 0; l < m; ++l) {
+        const int32_t res = tab.res[l];
+        Cell<float> c = cell_of<float>(x, y, z, res);
+        float acc[8];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) acc[f] = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int64_t slot = vertex_slot(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), res,
+                                       tab.entries[l], tab.dense[l] != 0);
+            float w = corner_weight<float>(c, k);
+            const float *p = params + tab.offset[l] + slot * n;
+            for (int f = 0; f < n; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(p + f)));
+        }
+        for (int f = 0; f < n; ++f) feat[(l * n + f) * FE_THREADS] = acc[f];
+    }
+}
+
+// Hidden width NN known at compile time: activations live in registers.
+template <int NN>
+__device__ __forceinline__ float mlp_exact_reg(const float *feat, int nin, const float *__restrict__ wt,
+                                               const MlpShape &sh) {
+    float h[NN];
+    // layer 0: nin -> NN, wt holds W0^T (nin x NN)
+    {
+        float acc[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) acc[j] = 0.0f;
+        for (int k = 0; k < nin; ++k) {
+            float hk = feat[k * FE_THREADS];
+            const float4 *wr = reinterpret_cast<const float4 *>(wt + k * NN);
+#pragma unroll
+            for (int j4 = 0; j4 < NN / 4; ++j4) {
+                float4 w = wr[j4];
+                acc[4 * j4 + 0] = xadd(acc[4 * j4 + 0], xmul(w.x, hk));
+                acc[4 * j4 + 1] = xadd(acc[4 * j4 + 1], xmul(w.y, hk));
+                acc[4 * j4 + 2] = xadd(acc[4 * j4 + 2], xmul(w.z, hk));
+                acc[4 * j4 + 3] = xadd(acc[4 * j4 + 3], xmul(w.w, hk));
+            }
+        }
+        const bool relu = sh.n_layers > 1 || sh.relu_out;
+#pragma unroll
+        for (int j = 0; j < NN; ++j) h[j] = relu ? fmaxf(acc[j], 0.0f) : acc[j];
+        wt += nin * NN;
+    }
+    const int nl = sh.n_layers;
+    for (int li = 1; li < nl - 1; ++li) {
+        float acc[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) acc[j] = 0.0f;
+#pragma unroll
+        for (int k = 0; k < NN; ++k) {
+            const float4 *wr = reinterpret_cast<const float4 *>(wt + k * NN);
+#pragma unroll
+            for (int j4 = 0; j4 < NN / 4; ++j4) {
+                float4 w = wr[j4];
+                acc[4 * j4 + 0] = xadd(acc[4 * j4 + 0], xmul(w.x, h[k]));
+                acc[4 * j4 + 1] = xadd(acc[4 * j4 + 1], xmul(w.y, h[k]));
+                acc[4 * j4 + 2] = xadd(acc[4 * j4 + 2], xmul(w.z, h[k]));
+                acc[4 * j4 + 3] = xadd(acc[4 * j4 + 3], xmul(w.w, h[k]));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NN; ++j) h[j] = fmaxf(acc[j], 0.0f);
+        wt += NN * NN;
+    }
+    if (nl == 1) return h[0];
+    // output layer NN -> 1
+    float o = 0.0f;
+#pragma unroll
+    for (int k = 0; k < NN; ++k) o = xadd(o, xmul(wt[k], h[k]));
+    return sh.relu_out ? fmaxf(o, 0.0f) : o;
+}
+
+// Generic widths: activations ping-pong through this thread's smem columns.
+__device__ float mlp_exact_smem(float *h0, float *h1, const float *__restrict__ wt, const MlpShape &sh) {
+    float *cur = h0, *nxt = h1;
+    for (int li = 0; li < sh.n_layers; ++li) {
+        int win = sh.widths[li], wout = sh.widths[li + 1];
+        bool relu = li < sh.n_layers - 1 || sh.relu_out;
+        for (int j = 0; j < wout; ++j) {
+            float acc = 0.0f;
+            for (int k = 0; k < win; ++k) acc = xadd(acc, xmul(wt[k * wout + j], cur[k * FE_THREADS]));
+            nxt[j * FE_THREADS] = relu ? fmaxf(acc, 0.0f) : acc;
+        }
+        wt += win * wout;
+        float *t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    return cur[0];
+}
+
+// mode: 0 = explicit coords, 1 = decode brick (voxel centres of rows [z0, z0+nz)).
+template <int NN>
+__global__ void __launch_bounds__(FE_THREADS) field_exact_kernel(
+    const float *__restrict__ coords, int64_t b, const float *__restrict__ params, const GridTables tab,
+    const float *__restrict__ weights, const MlpShape sh, int decode, int64_t dx, int64_t dy, int64_t dz,
+    int64_t z0, double lo, double scale, float *__restrict__ out, int maxw) {
+    extern __shared__ float4 smem4[];
+    float *smem = reinterpret_cast<float *>(smem4);
+    // transposed weights: layer li occupies widths[li]*widths[li+1] floats, k-major
+    int wtotal = 0;
+    for (int li = 0; li < sh.n_layers; ++li) wtotal += sh.widths[li] * sh.widths[li + 1];
+    float *wt = smem;
+    {
+        const float *src = weights;
+        float *dst = wt;
+        for (int li = 0; li < sh.n_layers; ++li) {
+            int win = sh.widths[li], wout = sh.widths[li + 1];
+            for (int q = threadIdx.x; q < win * wout; q += blockDim.x) {
+                int j = q / win, k = q % win;  // src row-major (j, k)
+                dst[k * wout + j] = src[q];
+            }
+            src += win * wout;
+            dst += win * wout;
+        }
+    }
+    float *h0 = wt + ((wtotal + 3) & ~3);
+    float *h1 = h0 + maxw * FE_THREADS;
+    __syncthreads();
+    for (int64_t base = (int64_t)blockIdx.x * FE_THREADS; base < b; base += (int64_t)gridDim.x * FE_THREADS) {
+        int64_t i = base + threadIdx.x;
+        if (i >= b) continue;
+        float x, y, z;
+        if (decode) {
+            int64_t ix = i % dx, iy = (i / dx) % dy, iz = z0 + i / (dx * dy);
+            x = xdiv(xadd((float)ix, 0.5f), (float)dx);
+            y = xdiv(xadd((float)iy, 0.5f), (float)dy);
+            z = xdiv(xadd((float)iz, 0.5f), (float)dz);
+        } else {
+            x = coords[3 * i];
+            y = coords[3 * i + 1];
+            z = coords[3 * i + 2];
+        }
+        float *col0 = h0 + threadIdx.x, *col1 = h1 + threadIdx.x;
+        encode_exact(x, y, z, params, tab, col0);
+        float v;
+        if constexpr (NN > 0) {
+            v = mlp_exact_reg<NN>(col0, tab.n_levels * tab.n_feat, wt, sh);
+        } else {
+            v = mlp_exact_smem(col0, col1, wt, sh);
+        }
+        if (decode)
+            out[i] = (float)__dadd_rn(__dmul_rn((double)v, scale), lo);
+        else
+            out[i] = v;
+    }
+}
+
+int field_exact_launch(const float *coords, int64_t b, const float *params, const GridTables &tab,
+                       const float *weights, const int32_t *widths, int32_t n_layers, int32_t relu_out,
+                       int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0, double lo, double scale,
+                       float *out, cudaStream_t s) {
+    NVOL_REQUIRE(n_layers >= 1 && n_layers <= 11, "MLP depth out of range");
+    MlpShape sh;
+    sh.n_layers = n_layers;
+    sh.relu_out = relu_out ? 1 : 0;
+    int maxw = 0, wtotal = 0;
+    for (int i = 0; i <= n_layers; ++i) {
+        sh.widths[i] = widths[i];
+        maxw = max(maxw, (int)widths[i]);
+    }
+    for (int i = 0; i < n_layers; ++i) wtotal += widths[i] * widths[i + 1];
+    NVOL_REQUIRE(widths[0] == tab.n_levels * tab.n_feat, "MLP input width != encoder width");
+    NVOL_REQUIRE(widths[n_layers] == 1, "output width must be 1");
+    // register path: uniform hidden width NN in {16,32,64}
+    int nn = n_layers >= 2 ? widths[1] : 0;
+    bool uniform = n_layers >= 2;
+    for (int i = 1; i < n_layers; ++i) uniform &= widths[i] == nn;
+    size_t smem = sizeof(float) * (((wtotal + 3) & ~3) + 2 * (size_t)maxw * FE_THREADS);
+    NVOL_REQUIRE(smem <= 220 * 1024, "MLP too large for the exact evaluator");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t blocks = (b + FE_THREADS - 1) / FE_THREADS;
+    unsigned grid = (unsigned)max((int64_t)1, min(blocks, (int64_t)sms * 16));
+#define LAUNCH_FE(NNV)                                                                                      \
+    do {                                                                                                    \
+        cudaFuncSetAttribute(field_exact_kernel<NNV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        field_exact_kernel<NNV><<<grid, FE_THREADS, smem, s>>>(coords, b, params, tab, weights, sh, decode, dx, \
+                                                               dy, dz, z0, lo, scale, out, maxw);           \
+    } while (0)
+    if (uniform && nn == 16)
+        LAUNCH_FE(16);
+    else if (uniform && nn == 32)
+        LAUNCH_FE(32);
+    else if (uniform && nn == 64)
+        LAUNCH_FE(64);
+    else
+        LAUNCH_FE(0);
+#undef LAUNCH_FE
+    return check_launch("field_eval_exact");
+}
+
+int nvol_decode_tc(const float *params, const GridTables &tab, const float *weights, const int32_t *widths,
+                   int32_t n_layers, int32_t relu_out, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
+                   int64_t nz, double lo, double scale, float *out, cudaStream_t s);
+
+}  // namespace nvol
+
+using namespace nvol;
+
+extern "C" {
+
+int nvol_field_eval_exact(const float *coords, int64_t b, const float *params, const int64_t *level_off,
+                          const int64_t *level_res, const int64_t *level_entries, const uint8_t *level_dense,
+                          int32_t n_levels, int32_t n_feat, const float *weights, const int32_t *widths,
+                          int32_t n_layers, int32_t relu_out, float *out, void *stream) {
+    GridTables tab;
+    int st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
+    if (st) return st;
+    if (b == 0) return NVOL_OK;
+    NVOL_REQUIRE(coords && params && weights && widths && out, "null pointer");
+    return field_exact_launch(coords, b, params, tab, weights, widths, n_layers, relu_out, 0, 0, 0, 0, 0, 0.0,
+                              1.0, out, as_stream(stream));
+}
+
+int nvol_decode(const float *params, const int64_t *level_off, const int64_t *level_res,
+                const int64_t *level_entries, const uint8_t *level_dense, int32_t n_levels, int32_t n_feat,
+                const float *weights, const int32_t *widths, int32_t n_layers, int32_t relu_out, int64_t dx,
+                int64_t dy, int64_t dz, int64_t z0, int64_t nz, double lo, double hi, float *out, int32_t mode,
+                void *stream) {
+    GridTables tab;
+    int st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
+    if (st) return st;
+    NVOL_REQUIRE(dx >= 1 && dy >= 1 && dz >= 1 && z0 >= 0 && nz >= 0 && z0 + nz <= dz, "bad decode brick");
+    NVOL_REQUIRE(params && weights && widths && out, "null pointer");
+    if (nz == 0) return NVOL_OK;
+    double scale = hi - lo;
+    if (mode == 1) return nvol_decode_tc(params, tab, weights, widths, n_layers, relu_out, dx, dy, dz, z0, nz, lo,
+                                         scale, out, as_stream(stream));
+    return field_exact_launch(nullptr, dx * dy * nz, params, tab, weights, widths, n_layers, relu_out, 1, dx, dy,
+                              dz, z0, lo, scale, out, as_stream(stream));
+}
+
+}  // extern "C"

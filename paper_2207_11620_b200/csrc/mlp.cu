@@ -1,0 +1,370 @@
+// Generic (any width / depth / dtype) MLP forward + backward, loss and Adam.
+//
+// Reference: network.py:61-93 (Mlp.forward / backward, numpy sgemm),
+// network.py:96-114 (loss_and_grad), network.py:160-183 (adam_step).
+// These kernels back the reference-shaped API (float32 and the float64
+// gradient-check builds); the training hot path uses the fused kernels in
+// train_fused.cu instead.
+#include "common.cuh"
+
+namespace nvol {
+
+// C[M,N] (=|+=) op(A)[M,K] * op(B)[K,N], optional ReLU.  64x64 tiles,
+// 256 threads, 4x4 outputs per thread, k-tile 16.  gridDim.z > 1 splits K
+// and accumulates with atomics (used for the dW reductions over the batch).
+template <typename T, bool TA, bool TB>
+__global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t K, const T *__restrict__ A,
+                                                   int64_t lda, const T *__restrict__ B, int64_t ldb,
+                                                   T *__restrict__ C, int64_t ldc, int accumulate, int relu) {
+    __shared__ T As[16][64 + 1];
+    __shared__ T Bs[16][64 + 1];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+    const int64_t kchunk = (K + gridDim.z - 1) / gridDim.z;
+    const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+    const int64_t kend = min(K, kbeg + kchunk);
+    T acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = (T)0;
+    for (int64_t k0 = kbeg; k0 < kend; k0 += 16) {
+        for (int q = threadIdx.x; q < 16 * 64; q += 256) {
+            int kk = q / 64, mm = q % 64;
+            int64_t gm = m0 + mm, gk = k0 + kk;
+            T va = (T)0;
+            if (gm < M && gk < kend) va = TA ? A[gk * lda + gm] : A[gm * lda + gk];
+            As[kk][mm] = va;
+            int64_t gn = n0 + mm;
+            T vb = (T)0;
+            if (gn < N && gk < kend) vb = TB ? B[gn * ldb + gk] : B[gk * ldb + gn];
+            Bs[kk][mm] = vb;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            T a[4], b[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a[r] = As[kk][ty * 4 + r];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) b[r] = Bs[kk][tx * 4 + r];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[r][c] += a[r] * b[c];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        int64_t gm = m0 + ty * 4 + r;
+        if (gm >= M) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            int64_t gn = n0 + tx * 4 + c;
+            if (gn >= N) continue;
+            T v = acc[r][c];
+            T *dst = C + gm * ldc + gn;
+            if (gridDim.z > 1) {
+                atomicAdd(dst, v);
+            } else {
+                if (accumulate) v += *dst;
+                if (relu) v = v > (T)0 ? v : (T)0;
+                *dst = v;
+            }
+        }
+    }
+}
+
+template <typename T, bool TA, bool TB>
+static int gemm(int64_t M, int64_t N, int64_t K, const T *A, int64_t lda, const T *B, int64_t ldb, T *C,
+                int64_t ldc, int accumulate, int relu, cudaStream_t s) {
+    dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), 1);
+    int64_t tiles = (int64_t)grid.x * grid.y;
+    if (accumulate && !relu && tiles < 296 && K > 4096) {
+        int64_t split = min((int64_t)1024, max((int64_t)1, (296 * 4) / tiles));
+        split = min(split, (K + 1023) / 1024);
+        grid.z = (unsigned)split;
+    }
+    gemm_kernel<T, TA, TB><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, relu);
+    return check_launch("gemm");
+}
+
+template <typename T>
+__global__ void relu_mask_kernel(T *__restrict__ d, const T *__restrict__ act, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) d[i] = d[i] * (act[i] > (T)0 ? (T)1 : (T)0);
+}
+
+template <typename T>
+static int mlp_forward_t(int64_t b, int nl, const int32_t *widths, const void *const *weights,
+                         void *const *acts, int relu_out, cudaStream_t s) {
+    for (int i = 0; i < nl; ++i) {
+        int64_t win = widths[i], wout = widths[i + 1];
+        bool relu = (i < nl - 1) || relu_out;
+        int st = gemm<T, false, true>(b, wout, win, (const T *)acts[i], win, (const T *)weights[i], win,
+                                      (T *)acts[i + 1], wout, 0, relu ? 1 : 0, s);
+        if (st) return st;
+    }
+    return NVOL_OK;
+}
+
+template <typename T>
+static int mlp_backward_t(int64_t b, int nl, const int32_t *widths, const void *const *weights,
+                          const void *const *acts, const void *dl_dout, void *const *grads, void *dl_din,
+                          void *s0, void *s1, int relu_out, cudaStream_t s) {
+    // d = dl_dout as a (B, 1) matrix, copied so the mask can be applied in place
+    T *d = (T *)s0, *dn = (T *)s1;
+    if (cudaMemcpyAsync(d, dl_dout, sizeof(T) * b * widths[nl], cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return check_launch("mlp_backward copy");
+    for (int i = nl - 1; i >= 0; --i) {
+        int64_t win = widths[i], wout = widths[i + 1];
+        if (i < nl - 1 || relu_out) {
+            relu_mask_kernel<T><<<grid_for(b * wout, 256), 256, 0, s>>>(d, (const T *)acts[i + 1], b * wout);
+        }
+        // grads[i] += d^T @ acts[i]   (wout x win, K = B)
+        int st = gemm<T, true, false>(wout, win, b, d, wout, (const T *)acts[i], win, (T *)grads[i], win, 1, 0, s);
+        if (st) return st;
+        // d = d @ W_i   (B x win)
+        T *dst = (i == 0) ? (T *)dl_din : dn;
+        st = gemm<T, false, false>(b, win, wout, d, wout, (const T *)weights[i], win, dst, win, 0, 0, s);
+        if (st) return st;
+        T *tmp = d;
+        d = dn;
+        dn = tmp;
+    }
+    return check_launch("mlp_backward");
+}
+
+template <typename T>
+__global__ void loss_kernel(const T *__restrict__ pred, const T *__restrict__ target, int64_t b, int kind,
+                            double denom, T *__restrict__ grad, double *__restrict__ loss_sum) {
+    __shared__ double red[32];
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double s = 0.0;
+    if (i < b) {
+        double d = __dsub_rn((double)pred[i], (double)target[i]);
+        double g;
+        if (kind == 0) {
+            s = fabs(d);
+            double sg = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0);
+            g = __ddiv_rn(sg, denom);
+        } else {
+            s = __dmul_rn(d, d);
+            g = __ddiv_rn(__dmul_rn(2.0, d), denom);
+        }
+        if (grad) grad[i] = (T)g;
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) atomicAdd(loss_sum, s);
+    }
+}
+
+// network.py:172-182, operation for operation.
+template <typename T>
+__device__ __forceinline__ void adam_one(T &p, T &g, T &m, T &v, T lr, T b1, T omb1, T b2, T omb2, T c1,
+                                         T c2, T eps, T l2) {
+    T geff = xadd(g, xmul(l2, p));
+    T mj = xadd(xmul(m, b1), xmul(omb1, geff));
+    T vj = xadd(xmul(v, b2), xmul(omb2, xmul(geff, geff)));
+    T mhat = xdiv(mj, c1);
+    T vhat = xdiv(vj, c2);
+    p = xsub(p, xdiv(xmul(lr, mhat), xadd(xsqrt(vhat), eps)));
+    m = mj;
+    v = vj;
+    g = (T)0;
+}
+
+template <typename T>
+__global__ void adam_kernel(T *__restrict__ p, T *__restrict__ g, T *__restrict__ m, T *__restrict__ v,
+                            int64_t n, T lr, T b1, T omb1, T b2, T omb2, T c1, T c2, T eps, T l2) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        T pj = p[j], gj = g[j], mj = m[j], vj = v[j];
+        adam_one<T>(pj, gj, mj, vj, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        p[j] = pj;
+        g[j] = gj;
+        m[j] = mj;
+        v[j] = vj;
+    }
+}
+
+// Flat float32 Adam for the training pipeline: float4-vectorised streaming
+// over (p, g, m, v) — 32 algorithmic bytes per parameter, the dominant HBM
+// term of a cfg2 step.  Scalars come from the device-side schedule so a
+// captured CUDA graph replays correctly step after step.
+__global__ void __launch_bounds__(256) adam_flat_kernel(
+    float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v, int64_t n,
+    const float *__restrict__ sched, int64_t sched_len, const int64_t *__restrict__ step_counter, float b1,
+    float omb1, float b2, float omb2, float eps, float l2, uint32_t *__restrict__ nan_flag) {
+    int64_t t = *step_counter;
+    if (t >= sched_len) t = sched_len - 1;
+    const float lr = sched[3 * t], c1 = sched[3 * t + 1], c2 = sched[3 * t + 2];
+    const int64_t n4 = n >> 2;
+    bool bad = false;
+    float4 *p4 = reinterpret_cast<float4 *>(p), *g4 = reinterpret_cast<float4 *>(g);
+    float4 *m4 = reinterpret_cast<float4 *>(m), *v4 = reinterpret_cast<float4 *>(v);
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
+        float4 P = __ldcs(p4 + j), G = __ldcs(g4 + j), M = __ldcs(m4 + j), V = __ldcs(v4 + j);
+        bad |= isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w);
+        adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        __stcs(p4 + j, P);
+        __stcs(g4 + j, G);
+        __stcs(m4 + j, M);
+        __stcs(v4 + j, V);
+    }
+    for (int64_t j = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        float P = p[j], G = g[j], M = m[j], V = v[j];
+        bad |= isnan(G);
+        adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        p[j] = P;
+        g[j] = G;
+        m[j] = M;
+        v[j] = V;
+    }
+    if (nan_flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan_flag, 1u);
+}
+
+__global__ void step_advance_kernel(int64_t *counter) { *counter += 1; }
+
+__global__ void loss_record_kernel(double *acc, double *losses, const int64_t *counter, int64_t t0, int64_t cap,
+                                   double inv_b) {
+    int64_t k = *counter - t0;
+    if (k >= 0 && k < cap) losses[k] = *acc * inv_b;
+    *acc = 0.0;
+}
+
+template <typename T>
+__global__ void find_nan_kernel(const T *__restrict__ g, int64_t n, unsigned long long *first) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        if (isnan(g[j])) atomicMin(first, (unsigned long long)j);
+}
+
+__global__ void fill_u64_kernel(unsigned long long *p, unsigned long long v) { *p = v; }
+__global__ void finish_nan_kernel(unsigned long long *p) {
+    if (*p == ~0ull) *reinterpret_cast<long long *>(p) = -1;
+}
+
+static unsigned stream_grid(int64_t n) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t want = (n + 255) / 256;
+    int64_t cap = (int64_t)sms * 8;
+    return (unsigned)max((int64_t)1, min(want, cap));
+}
+
+}  // namespace nvol
+
+using namespace nvol;
+
+extern "C" {
+
+int nvol_mlp_forward(int64_t b, int32_t n_layers, const int32_t *widths, const void *const *weights,
+                     void *const *acts, int32_t relu_out, int32_t dtype_bytes, void *stream) {
+    NVOL_REQUIRE(n_layers >= 1 && widths && weights && acts, "bad MLP description");
+    NVOL_REQUIRE(dtype_bytes == 4 || dtype_bytes == 8, "dtype must be float32 or float64");
+    if (b == 0) return NVOL_OK;
+    if (dtype_bytes == 4) return mlp_forward_t<float>(b, n_layers, widths, weights, acts, relu_out, as_stream(stream));
+    return mlp_forward_t<double>(b, n_layers, widths, weights, acts, relu_out, as_stream(stream));
+}
+
+int nvol_mlp_backward(int64_t b, int32_t n_layers, const int32_t *widths, const void *const *weights,
+                      const void *const *acts, const void *dl_dout, void *const *grads, void *dl_dinput,
+                      void *scratch0, void *scratch1, int32_t relu_out, int32_t dtype_bytes, void *stream) {
+    NVOL_REQUIRE(n_layers >= 1 && widths && weights && acts && grads, "bad MLP description");
+    NVOL_REQUIRE(dl_dout && dl_dinput && scratch0 && scratch1, "null pointer");
+    NVOL_REQUIRE(dtype_bytes == 4 || dtype_bytes == 8, "dtype must be float32 or float64");
+    if (b == 0) return NVOL_OK;
+    if (dtype_bytes == 4)
+        return mlp_backward_t<float>(b, n_layers, widths, weights, acts, dl_dout, grads, dl_dinput, scratch0,
+                                     scratch1, relu_out, as_stream(stream));
+    return mlp_backward_t<double>(b, n_layers, widths, weights, acts, dl_dout, grads, dl_dinput, scratch0,
+                                  scratch1, relu_out, as_stream(stream));
+}
+
+int nvol_loss_and_grad_scaled(const void *pred, const void *target, int64_t b, int64_t b_global, int32_t kind,
+                              void *grad, double *loss_sum, int32_t dtype_bytes, void *stream) {
+    NVOL_REQUIRE(kind == 0 || kind == 1, "loss kind must be 0 (L1) or 1 (L2)");
+    NVOL_REQUIRE(b >= 1, "empty batch");
+    NVOL_REQUIRE(pred && target && loss_sum, "null pointer");
+    cudaStream_t s = as_stream(stream);
+    if (dtype_bytes == 4)
+        loss_kernel<float><<<grid_for(b, 256), 256, 0, s>>>((const float *)pred, (const float *)target, b, kind,
+                                                            (double)b_global, (float *)grad, loss_sum);
+    else
+        loss_kernel<double><<<grid_for(b, 256), 256, 0, s>>>((const double *)pred, (const double *)target, b,
+                                                             kind, (double)b_global, (double *)grad, loss_sum);
+    return check_launch("loss_and_grad");
+}
+
+int nvol_loss_and_grad(const void *pred, const void *target, int64_t b, int32_t kind, void *grad,
+                       double *loss_sum, int32_t dtype_bytes, void *stream) {
+    return nvol_loss_and_grad_scaled(pred, target, b, b, kind, grad, loss_sum, dtype_bytes, stream);
+}
+
+int nvol_loss_record(double *acc, double *losses, const int64_t *step_counter, int64_t t0, int64_t cap,
+                     double inv_b, void *stream) {
+    NVOL_REQUIRE(acc && losses && step_counter && cap >= 1, "null pointer");
+    loss_record_kernel<<<1, 1, 0, as_stream(stream)>>>(acc, losses, step_counter, t0, cap, inv_b);
+    return check_launch("loss_record");
+}
+
+int nvol_adam_step(void *p, void *g, void *m, void *v, int64_t n, double lr, double beta1,
+                   double one_minus_beta1, double beta2, double one_minus_beta2, double c1, double c2,
+                   double eps, double l2, int32_t dtype_bytes, void *stream) {
+    NVOL_REQUIRE(dtype_bytes == 4 || dtype_bytes == 8, "dtype must be float32 or float64");
+    if (n == 0) return NVOL_OK;
+    NVOL_REQUIRE(p && g && m && v, "null pointer");
+    cudaStream_t s = as_stream(stream);
+    if (dtype_bytes == 4)
+        adam_kernel<float><<<stream_grid(n), 256, 0, s>>>((float *)p, (float *)g, (float *)m, (float *)v, n,
+                                                          (float)lr, (float)beta1, (float)one_minus_beta1,
+                                                          (float)beta2, (float)one_minus_beta2, (float)c1,
+                                                          (float)c2, (float)eps, (float)l2);
+    else
+        adam_kernel<double><<<stream_grid(n), 256, 0, s>>>((double *)p, (double *)g, (double *)m, (double *)v, n,
+                                                           lr, beta1, one_minus_beta1, beta2, one_minus_beta2,
+                                                           c1, c2, eps, l2);
+    return check_launch("adam_step");
+}
+
+int nvol_adam_flat_dev(float *p, float *g, float *m, float *v, int64_t n, const float *sched, int64_t sched_len,
+                       int64_t *step_counter, float beta1, float one_minus_beta1, float beta2,
+                       float one_minus_beta2, float eps, float l2, uint32_t *nan_flag, void *stream) {
+    NVOL_REQUIRE(p && g && m && v && sched && step_counter && sched_len >= 1, "null pointer");
+    NVOL_REQUIRE((((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) == 0,
+                 "flat Adam buffers must be 16-byte aligned");
+    cudaStream_t s = as_stream(stream);
+    adam_flat_kernel<<<stream_grid((n + 3) / 4), 256, 0, s>>>(p, g, m, v, n, sched, sched_len, step_counter, beta1,
+                                                              one_minus_beta1, beta2, one_minus_beta2, eps, l2,
+                                                              nan_flag);
+    step_advance_kernel<<<1, 1, 0, s>>>(step_counter);
+    return check_launch("adam_flat");
+}
+
+int nvol_find_nan(const void *g, int64_t n, int64_t *first, int32_t dtype_bytes, void *stream) {
+    NVOL_REQUIRE(first, "null pointer");
+    cudaStream_t s = as_stream(stream);
+    unsigned long long *f = reinterpret_cast<unsigned long long *>(first);
+    fill_u64_kernel<<<1, 1, 0, s>>>(f, ~0ull);
+    if (n > 0) {
+        if (dtype_bytes == 4)
+            find_nan_kernel<float><<<stream_grid(n), 256, 0, s>>>((const float *)g, n, f);
+        else
+            find_nan_kernel<double><<<stream_grid(n), 256, 0, s>>>((const double *)g, n, f);
+    }
+    finish_nan_kernel<<<1, 1, 0, s>>>(f);
+    return check_launch("find_nan");
+}
+
+}  // extern "C"

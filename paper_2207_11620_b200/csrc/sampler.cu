@@ -1,0 +1,179 @@
+// Training-sample generation, analytic field rasterisation and metrics.
+//
+// Reference: sampler.py:54-74 (sample_incore: numpy PCG64 float32 coords +
+// volume.py:148-164 trilinear GT, clamped), fields.py:15-88 (rasterize),
+// volume.py:197-207 (mse / psnr).
+#include "common.cuh"
+
+namespace nvol {
+
+constexpr int SAMPLES_PER_THREAD = 4;
+
+// Each thread owns SAMPLES_PER_THREAD consecutive rows = 12 consecutive u32
+// draws of the stream; it jumps there once (O(log n) LCG advance) and then
+// steps sequentially.  The volume read is the bit-exact trilinear of
+// volume.py:148-164, clamped to [0,1] as sampler.py:74.
+__global__ void __launch_bounds__(256) sample_incore_kernel(U128 s0, U128 inc, uint64_t u32_base,
+                                                            const int64_t *__restrict__ step_counter,
+                                                            int64_t counter0, int64_t b_global, int64_t row0,
+                                                            int64_t b,
+                                                            const float *__restrict__ vol, int64_t dx,
+                                                            int64_t dy, int64_t dz, float *__restrict__ coords,
+                                                            float *__restrict__ targets) {
+    int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * SAMPLES_PER_THREAD;
+    if (r0 >= b) return;
+    uint64_t base = u32_base;
+    if (step_counter)
+        base += (uint64_t)(*step_counter - counter0) * 3ull * (uint64_t)b_global + 3ull * (uint64_t)row0;
+    PcgF32Stream rs;
+    rs.init(s0, inc, base + 3ull * (uint64_t)r0);
+#pragma unroll
+    for (int q = 0; q < SAMPLES_PER_THREAD; ++q) {
+        int64_t r = r0 + q;
+        if (r >= b) break;
+        float x = rs.next(), y = rs.next(), z = rs.next();
+        coords[3 * r] = x;
+        coords[3 * r + 1] = y;
+        coords[3 * r + 2] = z;
+        float t = trilinear_at(vol, dx, dy, dz, x, y, z);
+        targets[r] = fminf(fmaxf(t, 0.0f), 1.0f);
+    }
+}
+
+__global__ void trilinear_kernel(const float *__restrict__ vol, int64_t dx, int64_t dy, int64_t dz,
+                                 const float *__restrict__ pts, int64_t n, float *__restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = trilinear_at(vol, dx, dy, dz, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+}
+
+// fields.py:15-57 in float64 (device libm: <= 2 ulp from glibc, so the
+// float32-cast result can differ from the host rasteriser by 1 ulp in rare
+// voxels; tests that need bit-identical inputs upload the host volume).
+__device__ __forceinline__ double gauss3(double x, double y, double z, double cx, double cy, double cz,
+                                         double sigma) {
+    double ax = x - cx, ay = y - cy, az = z - cz;
+    double d2 = ax * ax + ay * ay + az * az;
+    return exp(-d2 / (2.0 * sigma * sigma));
+}
+
+__device__ double field_value(int field, double x, double y, double z) {
+    const double pi = 3.141592653589793;
+    switch (field) {
+        case 0: return gauss3(x, y, z, 0.5, 0.5, 0.5, 0.18);
+        case 1: {
+            double a = gauss3(x, y, z, 0.30, 0.32, 0.28, 0.09);
+            double b = gauss3(x, y, z, 0.68, 0.60, 0.55, 0.07);
+            double c = gauss3(x, y, z, 0.45, 0.75, 0.72, 0.06);
+            return fmax(fmax(a, b), c);
+        }
+        case 2: {
+            double tp = 2.0 * pi;
+            double v = sin(tp * 3 * x) * sin(tp * 2 * y) * sin(tp * 4 * z);
+            return 0.5 + 0.5 * v;
+        }
+        default: {
+            const double fm = 6.0, alpha = 0.25;
+            double qx = 2.0 * x - 1.0, qy = 2.0 * y - 1.0, qz = 2.0 * z - 1.0;
+            double r = sqrt(qx * qx + qy * qy);
+            double rho = cos(2.0 * pi * fm * 0.5 * cos(pi * r / 2.0));
+            double v = (1.0 - sin(pi * qz / 2.0) + alpha * (1.0 + rho)) / (2.0 * (1.0 + alpha));
+            return fmin(fmax(v, 0.0), 1.0);
+        }
+    }
+}
+
+__global__ void rasterize_kernel(int field, int64_t dx, int64_t dy, int64_t dz, int64_t z0, int64_t nz,
+                                 void *__restrict__ out, int out_u8) {
+    int64_t n = dx * dy * nz;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t ix = k % dx, iy = (k / dx) % dy, iz = z0 + k / (dx * dy);
+        double x = ((double)ix + 0.5) / (double)dx;
+        double y = ((double)iy + 0.5) / (double)dy;
+        double z = ((double)iz + 0.5) / (double)dz;
+        double v = fmin(fmax(field_value(field, x, y, z), 0.0), 1.0);
+        if (out_u8)
+            reinterpret_cast<uint8_t *>(out)[k] = (uint8_t)rint(v * 255.0);
+        else
+            reinterpret_cast<float *>(out)[k] = (float)v;
+    }
+}
+
+__global__ void sq_err_kernel(const float *__restrict__ a, const float *__restrict__ b, int64_t n,
+                              double *__restrict__ sum) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double d = (double)a[i] - (double)b[i];
+        s += d * d;
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) atomicAdd(sum, s);
+    }
+}
+
+}  // namespace nvol
+
+using namespace nvol;
+
+extern "C" {
+
+int nvol_sample_incore(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                       uint64_t u32_offset, int64_t b, const float *volume, int64_t dx, int64_t dy, int64_t dz,
+                       float *coords, float *targets, void *stream) {
+    NVOL_REQUIRE(b >= 1, "batch size must be >= 1");
+    NVOL_REQUIRE(volume && coords && targets, "null pointer");
+    NVOL_REQUIRE(dx >= 1 && dy >= 1 && dz >= 1, "bad volume dims");
+    int64_t threads = (b + SAMPLES_PER_THREAD - 1) / SAMPLES_PER_THREAD;
+    sample_incore_kernel<<<grid_for(threads, 256), 256, 0, as_stream(stream)>>>(
+        U128{state_hi, state_lo}, U128{inc_hi, inc_lo}, u32_offset, nullptr, 0, 0, 0, b, volume, dx, dy, dz,
+        coords, targets);
+    return check_launch("sample_incore");
+}
+
+int nvol_sample_incore_dev(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                           uint64_t u32_base, const int64_t *step_counter, int64_t counter0, int64_t b_global,
+                           int64_t row0, int64_t b,
+                           const float *volume, int64_t dx, int64_t dy, int64_t dz, float *coords, float *targets,
+                           void *stream) {
+    NVOL_REQUIRE(b >= 1 && step_counter, "bad arguments");
+    NVOL_REQUIRE(volume && coords && targets, "null pointer");
+    int64_t threads = (b + SAMPLES_PER_THREAD - 1) / SAMPLES_PER_THREAD;
+    sample_incore_kernel<<<grid_for(threads, 256), 256, 0, as_stream(stream)>>>(
+        U128{state_hi, state_lo}, U128{inc_hi, inc_lo}, u32_base, step_counter, counter0, b_global, row0, b, volume,
+        dx, dy, dz, coords, targets);
+    return check_launch("sample_incore_dev");
+}
+
+int nvol_trilinear(const float *volume, int64_t dx, int64_t dy, int64_t dz, const float *pts, int64_t n, float *out,
+                   void *stream) {
+    if (n == 0) return NVOL_OK;
+    NVOL_REQUIRE(volume && pts && out, "null pointer");
+    trilinear_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(volume, dx, dy, dz, pts, n, out);
+    return check_launch("trilinear");
+}
+
+int nvol_rasterize(int32_t field, int64_t dx, int64_t dy, int64_t dz, int64_t z0, int64_t nz, void *out,
+                   int32_t out_u8, void *stream) {
+    NVOL_REQUIRE(field >= 0 && field <= 3, "unknown synthetic field");
+    NVOL_REQUIRE(out && dx >= 1 && dy >= 1 && dz >= 1 && z0 >= 0 && nz >= 0 && z0 + nz <= dz, "bad arguments");
+    if (nz == 0) return NVOL_OK;
+    int64_t n = dx * dy * nz;
+    unsigned grid = (unsigned)min((int64_t)148 * 16, (n + 255) / 256);
+    rasterize_kernel<<<grid, 256, 0, as_stream(stream)>>>(field, dx, dy, dz, z0, nz, out, out_u8);
+    return check_launch("rasterize");
+}
+
+int nvol_sq_err_sum(const float *a, const float *b, int64_t n, double *sum, void *stream) {
+    NVOL_REQUIRE(a && b && sum, "null pointer");
+    if (n == 0) return NVOL_OK;
+    unsigned grid = (unsigned)min((int64_t)148 * 8, (n + 255) / 256);
+    sq_err_kernel<<<grid, 256, 0, as_stream(stream)>>>(a, b, n, sum);
+    return check_launch("sq_err_sum");
+}
+
+}  // extern "C"

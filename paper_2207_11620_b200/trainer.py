@@ -1,0 +1,295 @@
+"""Training orchestration, decoding and model serialisation on the B200.
+
+Mirror of the reference's trainer.py (/root/reference/pkg/src/neuralvol/
+trainer.py): TrainHistory, train, decode_slabs, decode, compression_ratio,
+save_model / load_model with the byte-identical "VNRM" v1 format.
+
+`train` with a device InCoreSampler and a float32 grid model runs the
+device-resident pipeline (StepPipeline): per step one sampling kernel, the
+fused forward/backward, one flat Adam kernel and a device-side loss record,
+captured once into a CUDA graph and replayed — no host round trip per step.
+The per-step losses are read back once at the end.
+"""
+from __future__ import annotations
+
+import csv
+import json
+import logging
+import struct
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError, FormatError
+from .model import NeuralModel, build_model
+from .network import adam_scalars, lr_at
+from .sampler import InCoreSampler
+from .volume import ScalarField, VolumeMeta
+
+log = logging.getLogger(__name__)
+
+MODEL_MAGIC = b"VNRM"
+MODEL_VERSION = 1
+
+
+@dataclass
+class TrainHistory:
+    """trainer.py:30-58."""
+    steps: list = field(default_factory=list)
+    losses: list = field(default_factory=list)
+    lrs: list = field(default_factory=list)
+    wall_ms: list = field(default_factory=list)
+
+    def append(self, step: int, loss: float, lr: float, ms: float) -> None:
+        if self.steps and step <= self.steps[-1]:
+            raise ConfigError(f"history steps must increase: {step} after {self.steps[-1]}")
+        self.steps.append(step)
+        self.losses.append(loss)
+        self.lrs.append(lr)
+        self.wall_ms.append(ms)
+
+    def to_csv(self, path) -> None:
+        with open(path, "w", newline="") as fh:
+            w = csv.writer(fh)
+            w.writerow(["step", "loss", "lr", "ms"])
+            for row in zip(self.steps, self.losses, self.lrs, self.wall_ms):
+                w.writerow([row[0], f"{row[1]:.8g}", f"{row[2]:.8g}", f"{row[3]:.3f}"])
+
+    @staticmethod
+    def from_csv(path) -> "TrainHistory":
+        h = TrainHistory()
+        with open(path, newline="") as fh:
+            for row in csv.DictReader(fh):
+                h.append(int(row["step"]), float(row["loss"]), float(row["lr"]), float(row["ms"]))
+        return h
+
+
+class StepPipeline:
+    """Device-resident training steps (model.py:154-174 + sampler.py:263-270 + network.py:160-183).
+
+    One step = sample (rows [row0, row0+b) of the global batch) -> fused
+    forward/backward -> [all-reduce of the flat gradient + loss, when
+    data-parallel] -> loss record -> flat Adam, all reading the device step
+    counter, so a single captured CUDA graph replays every step."""
+
+    def __init__(self, model: NeuralModel, sampler: InCoreSampler, capacity: int, rank: int = 0, world: int = 1,
+                 group=None, use_graph: bool = True):
+        if not model._use_kernels():
+            raise ConfigError("the device pipeline needs a float32 grid model")
+        B = model.batch_size
+        if B % world:
+            raise ConfigError(f"batch size {B} is not divisible by world size {world}")
+        self.model, self.sampler = model, sampler
+        self.B, self.b, self.row0 = B, B // world, rank * (B // world)
+        self.world, self.group = world, group
+        dev = model.flat_params.device
+        self.coords = torch.empty((self.b, 3), dtype=torch.float32, device=dev)
+        self.targets = torch.empty(self.b, dtype=torch.float32, device=dev)
+        self.t0 = model.opt.t
+        self.counter = torch.full((1,), self.t0, dtype=torch.int64, device=dev)
+        self.u32_base = sampler.rng.u32
+        self.capacity = int(capacity)
+        self.losses = torch.zeros(self.capacity, dtype=torch.float64, device=dev)
+        self.acc = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.nan_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        o = model.opt
+        rows = []
+        for t in range(self.t0 + self.capacity):
+            lr, c1, c2 = adam_scalars(o, t)
+            rows.append((lr, c1, c2))
+        self.sched = torch.tensor(np.asarray(rows, dtype=np.float64).astype(np.float32), device=dev).reshape(-1)
+        f = lambda x: float(np.float32(x))  # noqa: E731  dt(...) of network.py:172-181
+        self.adam_consts = (f(o.beta1), f(1.0 - o.beta1), f(o.beta2), f(1.0 - o.beta2), f(o.epsilon), f(o.l2_reg))
+        self.use_graph = use_graph
+        self.graph = None
+        self.done = 0
+
+    def _body(self) -> None:
+        m, s = self.model, self.sampler
+        vol = s.volume
+        dz, dy, dx = vol.shape
+        _lib.call("nvol_sample_incore_dev", *s.rng.words(), self.u32_base, _lib.ptr(self.counter), self.t0, self.B,
+                  self.row0, self.b, _lib.ptr(vol), dx, dy, dz, _lib.ptr(self.coords), _lib.ptr(self.targets),
+                  _lib.stream())
+        m.fwd_bwd_device(self.coords, self.targets, self.acc, b_global=self.B)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(m.flat_grads, group=self.group)
+            dist.all_reduce(self.acc, group=self.group)
+        _lib.call("nvol_loss_record", _lib.ptr(self.acc), _lib.ptr(self.losses), _lib.ptr(self.counter), self.t0,
+                  self.capacity, 1.0 / self.B, _lib.stream())
+        _lib.call("nvol_adam_flat_dev", _lib.ptr(m.flat_params), _lib.ptr(m.flat_grads), _lib.ptr(m.flat_m),
+                  _lib.ptr(m.flat_v), m.flat_size, _lib.ptr(self.sched), self.sched.numel() // 3,
+                  _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag), _lib.stream())
+
+    def launches_per_step(self) -> int:
+        """Kernels of one step from this library (for the bench's gpu_launches)."""
+        return 1 + (5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 if self.model.train_mode == 0 else 1) + 2
+
+    def step(self, n: int = 1) -> None:
+        """Enqueue n steps (no host synchronisation)."""
+        if self.done + n > self.capacity:
+            raise ConfigError(f"pipeline capacity {self.capacity} exceeded")
+        for _ in range(n):
+            if self.graph is not None:
+                self.graph.replay()
+            elif self.use_graph and self.done >= 1:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._body()
+                self.graph = g
+                g.replay()
+            else:
+                self._body()
+            self.done += 1
+
+    def finish(self) -> np.ndarray:
+        """Synchronise, commit host-side state, return the per-step losses."""
+        losses = self.losses[:self.done].cpu().numpy()
+        self.model.opt.t = self.t0 + self.done
+        self.sampler.rng.u32 = self.u32_base + 3 * self.B * self.done
+        if int(self.nan_flag.item()):
+            raise FloatingPointError("NaN gradient encountered during device-resident training")
+        return losses
+
+
+def _fast_path(model, sampler, tap) -> bool:
+    return (tap is None and model._use_kernels() and isinstance(sampler, InCoreSampler)
+            and sampler.interpolation == "trilinear")
+
+
+def train(model: NeuralModel, sampler, steps: int, tap=None, log_every: int = 0) -> TrainHistory:
+    """Run `steps` optimisation steps, drawing one batch per step (trainer.py:61-77)."""
+    if steps < 1:
+        raise ConfigError(f"steps must be >= 1, got {steps}")
+    history = TrainHistory()
+    if _fast_path(model, sampler, tap):
+        t0 = model.opt.t
+        pipe = StepPipeline(model, sampler, steps)
+        start = time.perf_counter()
+        pipe.step(steps)
+        losses = pipe.finish()
+        ms = (time.perf_counter() - start) * 1e3 / steps
+        for k in range(steps):
+            history.append(t0 + k, float(losses[k]), lr_at(model.opt, t0 + k), ms)
+            if log_every and (t0 + k + 1) % log_every == 0:
+                log.info("step %d  loss %.6f  lr %.5g", t0 + k + 1, losses[k], history.lrs[-1])
+        return history
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        step_index = model.opt.t
+        batch = sampler.sample(model.batch_size)
+        loss = model.train_step(batch)
+        if tap is not None:
+            tap(batch)
+        ms = (time.perf_counter() - t0) * 1e3
+        history.append(step_index, loss, lr_at(model.opt, step_index), ms)
+        if log_every and (step_index + 1) % log_every == 0:
+            log.info("step %d  loss %.6f  lr %.5g  %.1f ms", step_index + 1, loss, history.lrs[-1], ms)
+    return history
+
+
+def decode_brick(model: NeuralModel, dims, z0: int, nz: int, out: torch.Tensor, mode: str | None = None) -> None:
+    """Voxel-centre decode of rows [z0, z0+nz) into out (device, nz*dy*dx f32)."""
+    dx, dy, dz = dims
+    lo, hi = model.value_range
+    c = model.encoder.config
+    off, res, ent, dense = model.encoder.c_tables()
+    widths = model._widths()
+    mode = mode or model.infer_mode
+    _lib.call("nvol_decode", _lib.ptr(model.flat_params), off, res, ent, dense, c.n_levels, c.n_features_per_level,
+              _lib.ptr(model._weights_flat()), _lib.host_i32(widths), len(widths) - 1,
+              int(model.mlp.config.output_activation == "relu"), dx, dy, dz, z0, nz, float(lo), float(hi),
+              _lib.ptr(out), 1 if mode == "tensor" else 0, _lib.stream())
+
+
+def decode_slabs(model: NeuralModel, dims=None, slab_z: int = 16):
+    """Yield (z0, slab) of the decoded volume in ascending z (trainer.py:80-95); slabs are device tensors."""
+    if slab_z < 1:
+        raise ConfigError("slab_z must be >= 1")
+    dims = tuple(dims if dims is not None else model.dims)
+    dx, dy, dz = dims
+    _require_grid_model(model)
+    for z0 in range(0, dz, slab_z):
+        nz = min(slab_z, dz - z0)
+        slab = torch.empty((nz, dy, dx), dtype=torch.float32, device=model.flat_params.device)
+        decode_brick(model, dims, z0, nz, slab)
+        yield z0, slab
+
+
+def _require_grid_model(model) -> None:
+    if not model._use_kernels():
+        raise ConfigError("decode runs on float32 grid models")
+
+
+def decode(model: NeuralModel, dims=None, slab_z: int | None = None, to_host: bool = False) -> ScalarField:
+    """Evaluate Phi at every voxel centre and denormalise by value_range (trainer.py:98-106).
+
+    The whole volume is decoded by one launch (slab boundaries cannot change
+    any value: each voxel is evaluated independently); slab_z only chunks the
+    launches.  The result stays on the device unless to_host."""
+    dims = tuple(dims if dims is not None else model.dims)
+    dx, dy, dz = dims
+    _require_grid_model(model)
+    data = torch.empty((dz, dy, dx), dtype=torch.float32, device=model.flat_params.device)
+    step = dz if slab_z is None else int(slab_z)
+    if step < 1:
+        raise ConfigError("slab_z must be >= 1")
+    for z0 in range(0, dz, step):
+        nz = min(step, dz - z0)
+        decode_brick(model, dims, z0, nz, data[z0:z0 + nz])
+    lo, hi = model.value_range
+    meta = VolumeMeta(dims=dims, dtype="f32", value_range=(lo, hi))
+    return ScalarField(meta=meta, data=data.cpu().numpy() if to_host else data)
+
+
+def compression_ratio(model: NeuralModel, meta: VolumeMeta) -> float:
+    """(source bytes) / (parameter bytes at f32) (trainer.py:109-111)."""
+    return (meta.voxel_count * meta.itemsize) / (model.n_params * 4.0)
+
+
+def save_model(model: NeuralModel, path) -> None:
+    """trainer.py:125-138: magic, version, sorted-key config JSON, f32 blob."""
+    if model.dtype != np.float32:
+        raise ConfigError("only float32 models serialize; rebuild with dtype=float32")
+    cfg = model.config_json()
+    cfg["dims"] = list(model.dims)
+    cfg["value_range"] = [model.value_range[0], model.value_range[1]]
+    cfg["n_params"] = model.n_params
+    blob = model.blob().cpu().numpy().astype("<f4")
+    payload = json.dumps(cfg, sort_keys=True).encode("utf-8")
+    with open(path, "wb") as fh:
+        fh.write(MODEL_MAGIC)
+        fh.write(struct.pack("<II", MODEL_VERSION, len(payload)))
+        fh.write(payload)
+        fh.write(blob.tobytes())
+
+
+def load_model(path) -> NeuralModel:
+    """trainer.py:141-171 (fresh optimizer state, as the reference)."""
+    raw = Path(path).read_bytes()
+    if len(raw) < 12 or raw[:4] != MODEL_MAGIC:
+        raise FormatError(f"{path}: bad magic; not a model file")
+    version, jlen = struct.unpack("<II", raw[4:12])
+    if version != MODEL_VERSION:
+        raise FormatError(f"{path}: unsupported version {version} (expected {MODEL_VERSION})")
+    if len(raw) < 12 + jlen:
+        raise FormatError(f"{path}: truncated config (expected {jlen} bytes, found {len(raw) - 12})")
+    try:
+        cfg = json.loads(raw[12:12 + jlen].decode("utf-8"))
+    except (UnicodeDecodeError, json.JSONDecodeError) as exc:
+        raise FormatError(f"{path}: config block is not valid JSON ({exc})") from exc
+    model = build_model(cfg, dims=tuple(cfg.get("dims", (2, 2, 2))),
+                        value_range=tuple(cfg.get("value_range", (0.0, 1.0))))
+    blob = np.frombuffer(raw[12 + jlen:], dtype="<f4")
+    expected = model.n_params
+    if "n_params" in cfg and cfg["n_params"] != expected:
+        raise FormatError(f"{path}: header n_params {cfg['n_params']} != config-derived {expected}")
+    if blob.size != expected:
+        raise FormatError(f"{path}: parameter blob has {blob.size} floats, expected {expected}")
+    model.load_blob(blob)
+    return model
