@@ -276,3 +276,57 @@ def test_save_load_roundtrip(nv, tmp_path):
     assert p1.read_bytes() == p2.read_bytes()
     c = np.random.default_rng(0).random((64, 3)).astype(np.float32)
     np.testing.assert_array_equal(model.eval_batch(c), m2.eval_batch(c))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_tcgen05_step_matches_oracle(nv, name):
+    """Fused tcgen05 fwd/bwd (fp16 operands, fp32 accumulate) vs the oracle's
+    fp32 step on the same params and batch: loss, MLP and encoder gradients
+    within the north-star half-precision bar (1e-2 relative, floor 1e-3*max)."""
+    import nvol_oracle as orc
+    from paper_2207_11620_b200 import _lib
+    from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
+    if not _lib.load().nvol_has_tcgen05(0):
+        pytest.skip("no tcgen05 device")
+    cfg = dict(golden_config(golden(f"encode_{name}.npz")), batch_size=8192)
+    model = build_model(cfg, dims=(32, 32, 32), seed=0)
+    ref = orc.OracleModel(cfg, seed=0)
+    norm = orc.rasterize("mlobb", (32, 32, 32))
+    c, t = orc.InCoreSampler(norm, seed=1).sample(8192)
+    cap = {}
+    want_loss = ref.train_step(c, t, capture=cap)
+    model.train_mode = MODE_TCGEN05
+    dc, dt = torch.from_numpy(c).cuda(), torch.from_numpy(t).cuda()
+    acc = torch.zeros(1, dtype=torch.float64, device="cuda")
+    model.fwd_bwd_device(dc, dt, acc)
+    loss = float(acc.item()) / 8192
+    assert loss == pytest.approx(want_loss, rel=1e-2)
+    enc_g = model.encoder.param_grads.cpu().numpy()
+    assert rel_err(enc_g, cap["enc_grads"]) < 3e-2
+    for i, g in enumerate(model.mlp.grads):
+        assert rel_err(g.cpu().numpy(), cap["w_grads"][i]) < 3e-2, i
+    # tcgen05 vs the SIMT fp32 engine on the device
+    model.flat_grads.zero_()
+    model.train_mode = 0
+    acc.zero_()
+    model.fwd_bwd_device(dc, dt, acc)
+    assert float(acc.item()) / 8192 == pytest.approx(want_loss, rel=1e-5)
+    assert rel_err(model.encoder.param_grads.cpu().numpy(), cap["enc_grads"]) < 1e-3
+
+
+def test_tcgen05_training_converges(nv):
+    """cfg1-shaped training with the tcgen05 engine tracks the fp32 engine."""
+    from paper_2207_11620_b200 import fields, trainer
+    from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    cfg = dict(golden_config(golden("encode_cfg2.npz")), batch_size=16384)
+    fld = fields.rasterize("mlobb", (48, 48, 48), host=True)
+    res = {}
+    for mode in (0, MODE_TCGEN05):
+        m = build_model(cfg, dims=(48, 48, 48), seed=0)
+        m.train_mode = mode
+        trainer.train(m, InCoreSampler(fld, seed=1), steps=200)
+        from paper_2207_11620_b200.volume import psnr
+        res[mode] = psnr(fld, trainer.decode(m, dims=(48, 48, 48)))
+    assert res[MODE_TCGEN05] > 20.0
+    assert abs(res[MODE_TCGEN05] - res[0]) < 1.5, res
