@@ -170,6 +170,20 @@ int nvol_field_eval_exact(const float *coords, int64_t b, const float *params,
                           const int32_t *widths, int32_t n_layers, int32_t relu_out,
                           float *out, void *stream);
 
+/* Same evaluation on the tensor cores (tcgen05, fp16 operands / fp32
+ * accumulate; north-star half-precision bar): the batched Phi evaluator of
+ * the renderers (_render_kernels.py:518-540 phi_eval_staged). */
+int nvol_field_eval_tc(const float *coords, int64_t b, const float *params,
+                       const int64_t *level_off, const int64_t *level_res,
+                       const int64_t *level_entries, const uint8_t *level_dense, int32_t n_levels,
+                       int32_t n_feat, const float *weights, const int32_t *widths,
+                       int32_t n_layers, int32_t relu_out, void *mlp_image, float *out,
+                       void *stream);
+
+/* Bytes of the device scratch `mlp_image` the tensor-core evaluators pack the
+ * fp32 weights into (fp16 UMMA core-matrix tiles + fp32 output row). */
+int64_t nvol_mlp_image_bytes(int32_t n_levels, int32_t n_feat, int32_t n_neurons, int32_t n_hidden);
+
 /* trainer.py:80-106 decode_slabs over voxel-centre coordinates of the brick
  * [z0, z0+nz) of a (dx,dy,dz) grid: out[k] = Phi * (hi-lo) + lo (f64 then f32).
  * mode 0 = exact (serial fp32, == eval_fused), 1 = tensor-core (tcgen05,
@@ -178,7 +192,7 @@ int nvol_decode(const float *params, const int64_t *level_off, const int64_t *le
                 const int64_t *level_entries, const uint8_t *level_dense, int32_t n_levels,
                 int32_t n_feat, const float *weights, const int32_t *widths, int32_t n_layers,
                 int32_t relu_out, int64_t dx, int64_t dy, int64_t dz, int64_t z0, int64_t nz,
-                double lo, double hi, float *out, int32_t mode, void *stream);
+                double lo, double hi, float *out, int32_t mode, void *mlp_image, void *stream);
 
 /* ------------------------------------------------------------------ fused training step */
 

@@ -219,7 +219,7 @@ int field_exact_launch(const float *coords, int64_t b, const float *params, cons
 
 int nvol_decode_tc(const float *params, const GridTables &tab, const float *weights, const int32_t *widths,
                    int32_t n_layers, int32_t relu_out, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
-                   int64_t nz, double lo, double scale, float *out, cudaStream_t s);
+                   int64_t nz, double lo, double scale, float *out, void *mlp_image, cudaStream_t s);
 
 }  // namespace nvol
 
@@ -244,7 +244,7 @@ int nvol_decode(const float *params, const int64_t *level_off, const int64_t *le
                 const int64_t *level_entries, const uint8_t *level_dense, int32_t n_levels, int32_t n_feat,
                 const float *weights, const int32_t *widths, int32_t n_layers, int32_t relu_out, int64_t dx,
                 int64_t dy, int64_t dz, int64_t z0, int64_t nz, double lo, double hi, float *out, int32_t mode,
-                void *stream) {
+                void *mlp_image, void *stream) {
     GridTables tab;
     int st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
     if (st) return st;
@@ -253,7 +253,7 @@ int nvol_decode(const float *params, const int64_t *level_off, const int64_t *le
     if (nz == 0) return NVOL_OK;
     double scale = hi - lo;
     if (mode == 1) return nvol_decode_tc(params, tab, weights, widths, n_layers, relu_out, dx, dy, dz, z0, nz, lo,
-                                         scale, out, as_stream(stream));
+                                         scale, out, mlp_image, as_stream(stream));
     return field_exact_launch(nullptr, dx * dy * nz, params, tab, weights, widths, n_layers, relu_out, 1, dx, dy,
                               dz, z0, lo, scale, out, as_stream(stream));
 }

@@ -1,0 +1,272 @@
+// tcgen05 field inference: fused encode + MLP forward for decode and render.
+//
+// Reference: trainer.py:80-106 (decode: Phi at voxel centres, denormalised)
+// and _kernels.py:154-176 / model.py:178-198 (batched Phi evaluation used by
+// the renderers' phi_eval_staged, _render_kernels.py:518-540).
+// Persistent CTAs (two per SM, 64 TMEM columns each) walk 128-sample tiles:
+// bit-exact fp32 hash-grid encode -> fp16 tile in smem -> one tcgen05.mma
+// chain per hidden layer into TMEM -> ReLU/fp16 epilogue -> output layer on
+// CUDA cores (fp32).  Accuracy: fp16 operands / fp32 accumulate (north-star
+// 1e-2 relative bar); the exact evaluator (field.cu) remains available.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace nvol {
+
+constexpr int IT_THREADS = 256;
+constexpr int IT_TILE = 128;
+
+struct InferShape {
+    int m, n, nin, ninp, nn, nh, relu_out;
+    uint32_t o_w[8], o_wout, o_x, o_h[2], smem_bytes, t_alloc;
+};
+
+static int build_infer_shape(InferShape &s, int m, int n, int nn, int nh, int relu_out) {
+    s.m = m;
+    s.n = n;
+    s.nin = m * n;
+    s.ninp = (s.nin + 15) & ~15;
+    s.nn = nn;
+    s.nh = nh;
+    s.relu_out = relu_out;
+    if (nh < 1 || nh > 8 || !(nn == 16 || nn == 32 || nn == 64 || nn == 128) || s.ninp > 128) return 0;
+    uint32_t off = 0;
+    auto take = [&](uint32_t bytes) {
+        uint32_t r = off;
+        off += (bytes + 127) & ~127u;
+        return r;
+    };
+    for (int i = 0; i < nh; ++i) s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+    s.o_wout = take(4u * nn);
+    s.o_x = take(2u * IT_TILE * s.ninp);
+    s.o_h[0] = take(2u * IT_TILE * nn);
+    s.o_h[1] = take(2u * IT_TILE * nn);
+    s.smem_bytes = off + 4u * IT_TILE;  // + output partials
+    s.t_alloc = nn < 32 ? 32 : nn;
+    return s.smem_bytes <= 110 * 1024;
+}
+
+__device__ __forceinline__ void st_f16x16(uint8_t *tile, int row, int c, int w, const float *v, bool relu) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        float a[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] = relu ? fmaxf(v[q * 8 + e], 0.0f) : v[q * 8 + e];
+        uint4 pk = make_uint4(tc::pack_half2(a[0], a[1]), tc::pack_half2(a[2], a[3]), tc::pack_half2(a[4], a[5]),
+                              tc::pack_half2(a[6], a[7]));
+        *reinterpret_cast<uint4 *>(tile + tc::tile_off(row, c + q * 8, w)) = pk;
+    }
+}
+
+template <int NF>
+__global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
+    const float *__restrict__ coords, int64_t b, const float *__restrict__ params, const GridTables tab,
+    const InferShape sh, const uint8_t *__restrict__ wimg, int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
+    double lo, double scale, float *__restrict__ out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base_sh;
+    const int tid = threadIdx.x, s = tid & (IT_TILE - 1), h = tid >> 7, warp = tid >> 5;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const int NN = sh.nn, NINP = sh.ninp, NH = sh.nh, M = sh.m;
+    {
+        // pre-packed fp16 weight tiles + fp32 output row (nvol_mlp_pack)
+        const uint4 *src = reinterpret_cast<const uint4 *>(wimg);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem);
+        for (int q = tid; q < (int)(sh.o_x / 16); q += IT_THREADS) dst[q] = __ldg(src + q);
+        for (int q = tid; q < IT_TILE * NINP / 8; q += IT_THREADS)
+            reinterpret_cast<uint4 *>(smem + sh.o_x)[q] = make_uint4(0, 0, 0, 0);
+    }
+    if (warp == 0) tc::tmem_alloc(&tmem_base_sh, sh.t_alloc);
+    if (tid == 0) {
+        tc::mbar_init(&mbar, 1);
+        tc::fence_mbar_init();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    uint32_t phase = 0;
+    const float *s_wout = reinterpret_cast<const float *>(smem + sh.o_wout);
+    float *s_part = reinterpret_cast<float *>(smem + sh.smem_bytes - 4 * IT_TILE);
+    const uint32_t idesc = tc::make_idesc(128, NN, 0, 0);
+    const int mh = (M + 1) / 2, l_lo = h * mh, l_hi = min(M, (h + 1) * mh);
+    const int64_t ntiles = (b + IT_TILE - 1) / IT_TILE;
+    int c0 = NN >= 32 ? h * (NN >> 1) : 0, nc = NN >= 32 ? (NN >> 1) : (h == 0 ? NN : 0);
+
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t i = tile * IT_TILE + s;
+        const bool valid = i < b;
+        float x = 0.f, y = 0.f, z = 0.f;
+        if (valid) {
+            if (decode) {
+                int64_t ix = i % dx, iy = (i / dx) % dy, iz = z0 + i / (dx * dy);
+                x = xdiv(xadd((float)ix, 0.5f), (float)dx);
+                y = xdiv(xadd((float)iy, 0.5f), (float)dy);
+                z = xdiv(xadd((float)iz, 0.5f), (float)dz);
+            } else {
+                x = coords[3 * i];
+                y = coords[3 * i + 1];
+                z = coords[3 * i + 2];
+            }
+        }
+        uint8_t *sx = smem + sh.o_x;
+        for (int l = l_lo; l < l_hi; ++l) {
+            const int32_t res = tab.res[l];
+            Cell<float> c = cell_of<float>(x, y, z, res);
+            float acc[NF];
+#pragma unroll
+            for (int f = 0; f < NF; ++f) acc[f] = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                int64_t slot = vertex_slot(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), res,
+                                           tab.entries[l], tab.dense[l] != 0);
+                float w = corner_weight<float>(c, k);
+                const float *p = params + tab.offset[l] + slot * NF;
+                if constexpr (NF == 2) {
+                    float2 v = __ldg(reinterpret_cast<const float2 *>(p));
+                    acc[0] = xadd(acc[0], xmul(w, v.x));
+                    acc[1] = xadd(acc[1], xmul(w, v.y));
+                } else {
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(p + f)));
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+                *reinterpret_cast<__half *>(sx + tc::tile_off(s, l * NF + f, NINP)) = __float2half_rn(acc[f] * tc::kFeatScale);
+        }
+        tc::fence_proxy_async();
+        __syncthreads();
+        float outp = 0.0f;
+        for (int li = 0; li < NH; ++li) {
+            const int win = li == 0 ? NINP : NN;
+            const uint8_t *a_tile = li == 0 ? smem + sh.o_x : smem + sh.o_h[(li - 1) & 1];
+            if (tid == 0) {
+                tc::fence_after();
+                uint32_t a0 = tc::smem_u32(a_tile), b0 = tc::smem_u32(smem + sh.o_w[li]);
+                for (int k = 0; k < win / 16; ++k)
+                    tc::mma_f16(tmem, tc::make_desc(a0 + k * 256, 128, (win / 8) * 128),
+                                tc::make_desc(b0 + k * 256, 128, (win / 8) * 128), idesc, k > 0);
+                tc::mma_commit(&mbar);
+            }
+            tc::mbar_wait(&mbar, phase);
+            phase ^= 1;
+            tc::fence_after();
+            uint8_t *dst = smem + sh.o_h[li & 1];
+            const float unscale = li == 0 ? 1.0f / tc::kFeatScale : 1.0f;
+            for (int c = c0; c < c0 + nc; c += 16) {
+                float v[16];
+                tc::tmem_ld16(tmem + lane_base + c, v);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] *= unscale;
+                if (li < NH - 1) {
+                    st_f16x16(dst, s, c, NN, v, true);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * fmaxf(v[e], 0.0f);
+                }
+            }
+            tc::fence_before();
+            tc::fence_proxy_async();
+            __syncthreads();
+        }
+        if (h == 1) s_part[s] = outp;
+        __syncthreads();
+        if (h == 0 && valid) {
+            float o = outp + s_part[s];
+            if (sh.relu_out) o = fmaxf(o, 0.0f);
+            out[i] = decode ? (float)__dadd_rn(__dmul_rn((double)o, scale), lo) : o;
+        }
+        __syncthreads();
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, sh.t_alloc);
+}
+
+int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const uint32_t *o_w, uint32_t o_wout,
+                   uint8_t *image, cudaStream_t s);
+
+int infer_tc_launch(const float *coords, int64_t b, const float *params, const GridTables &tab, const float *wflat,
+                    uint8_t *wimg, int nn, int nh, int relu_out, int decode, int64_t dx, int64_t dy, int64_t dz,
+                    int64_t z0, double lo, double scale, float *out, cudaStream_t s) {
+    InferShape sh;
+    if (!build_infer_shape(sh, tab.n_levels, tab.n_feat, nn, nh, relu_out)) {
+        set_error("MLP shape not supported by the tcgen05 inference path");
+        return NVOL_EINVAL;
+    }
+    NVOL_REQUIRE(wimg, "tcgen05 inference needs an mlp_image scratch buffer (nvol_mlp_image_bytes)");
+    int st = pack_mlp_image(wflat, sh.nin, sh.ninp, nn, nh, sh.o_w, sh.o_wout, wimg, s);
+    if (st) return st;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t ntiles = (b + IT_TILE - 1) / IT_TILE;
+    int64_t cap = (int64_t)sms * 2;
+    int grid = (int)(ntiles < cap ? ntiles : cap);
+    if (grid < 1) return NVOL_OK;
+    switch (tab.n_feat) {
+#define LAUNCH_IT(NFV)                                                                                         \
+    case NFV:                                                                                                  \
+        cudaFuncSetAttribute(infer_tc_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes); \
+        infer_tc_kernel<NFV><<<grid, IT_THREADS, sh.smem_bytes, s>>>(coords, b, params, tab, sh, wimg, decode, dx, dy, \
+                                                                    dz, z0, lo, scale, out);                   \
+        break;
+        LAUNCH_IT(1)
+        LAUNCH_IT(2)
+        LAUNCH_IT(4)
+        LAUNCH_IT(8)
+#undef LAUNCH_IT
+    }
+    return check_launch("infer_tc_kernel");
+}
+
+static int mlp_dims(const int32_t *widths, int32_t n_layers, const GridTables &tab, int &nn, int &nh) {
+    NVOL_REQUIRE(n_layers >= 2 && widths[n_layers] == 1, "MLP must have >= 1 hidden layer and output width 1");
+    NVOL_REQUIRE(widths[0] == tab.n_levels * tab.n_feat, "MLP input width != encoder width");
+    nn = widths[1];
+    for (int i = 1; i < n_layers; ++i) NVOL_REQUIRE(widths[i] == nn, "tcgen05 path needs a uniform hidden width");
+    nh = n_layers - 1;
+    return NVOL_OK;
+}
+
+int nvol_decode_tc(const float *params, const GridTables &tab, const float *weights, const int32_t *widths,
+                   int32_t n_layers, int32_t relu_out, int64_t dx, int64_t dy, int64_t dz, int64_t z0, int64_t nz,
+                   double lo, double scale, float *out, void *mlp_image, cudaStream_t s) {
+    int nn, nh;
+    int st = mlp_dims(widths, n_layers, tab, nn, nh);
+    if (st) return st;
+    return infer_tc_launch(nullptr, dx * dy * nz, params, tab, weights, (uint8_t *)mlp_image, nn, nh, relu_out, 1, dx,
+                           dy, dz, z0, lo, scale, out, s);
+}
+
+}  // namespace nvol
+
+using namespace nvol;
+
+extern "C" int64_t nvol_mlp_image_bytes(int32_t n_levels, int32_t n_feat, int32_t n_neurons, int32_t n_hidden) {
+    InferShape sh;
+    if (!build_infer_shape(sh, n_levels, n_feat, n_neurons, n_hidden, 1)) return 0;
+    return sh.o_x;
+}
+
+extern "C" int nvol_field_eval_tc(const float *coords, int64_t b, const float *params, const int64_t *level_off,
+                                  const int64_t *level_res, const int64_t *level_entries,
+                                  const uint8_t *level_dense, int32_t n_levels, int32_t n_feat,
+                                  const float *weights, const int32_t *widths, int32_t n_layers, int32_t relu_out,
+                                  void *mlp_image, float *out, void *stream) {
+    GridTables tab;
+    int st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
+    if (st) return st;
+    if (b == 0) return NVOL_OK;
+    NVOL_REQUIRE(coords && params && weights && widths && out, "null pointer");
+    int nn, nh;
+    st = mlp_dims(widths, n_layers, tab, nn, nh);
+    if (st) return st;
+    return infer_tc_launch(coords, b, params, tab, weights, (uint8_t *)mlp_image, nn, nh, relu_out, 0, 0, 0, 0, 0, 0.0,
+                           1.0, out, as_stream(stream));
+}

@@ -20,13 +20,21 @@ __global__ void __launch_bounds__(256) sample_incore_kernel(U128 s0, U128 inc, u
                                                             const float *__restrict__ vol, int64_t dx,
                                                             int64_t dy, int64_t dz, float *__restrict__ coords,
                                                             float *__restrict__ targets) {
-    int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * SAMPLES_PER_THREAD;
-    if (r0 >= b) return;
+    // One long jump per block (thread 0), then short per-thread jumps.
+    __shared__ U128 blk_state;
+    const int64_t blk_r0 = (int64_t)blockIdx.x * blockDim.x * SAMPLES_PER_THREAD;
     uint64_t base = u32_base;
     if (step_counter)
         base += (uint64_t)(*step_counter - counter0) * 3ull * (uint64_t)b_global + 3ull * (uint64_t)row0;
+    const uint64_t g_blk = base + 3ull * (uint64_t)blk_r0;   // u32 index of the block's first draw
+    if (threadIdx.x == 0) blk_state = pcg_advance(s0, inc, g_blk >> 1);
+    __syncthreads();
+    int64_t r0 = blk_r0 + (int64_t)threadIdx.x * SAMPLES_PER_THREAD;
+    if (r0 >= b) return;
+    const uint64_t g0 = g_blk + 3ull * (uint64_t)threadIdx.x * SAMPLES_PER_THREAD;
     PcgF32Stream rs;
-    rs.init(s0, inc, base + 3ull * (uint64_t)r0);
+    rs.init(blk_state, inc, g0 - ((g_blk >> 1) << 1));  // stream relative to the block state
+    rs.g = g0;
 #pragma unroll
     for (int q = 0; q < SAMPLES_PER_THREAD; ++q) {
         int64_t r = r0 + q;

@@ -1,17 +1,25 @@
-// Fused tcgen05 training tile pipeline (sm_100a).
+// Training step forward/backward on the tensor cores (sm_100a), as three
+// specialised kernels that each run at their own bound:
 //
-// One persistent CTA per SM walks 128-sample tiles of the batch.  Per tile:
-//   encode (hash-grid gather, _kernels.py:31-79)  -> fp16 feature tile in smem
-//   forward MLP (network.py:61-74): per layer one tcgen05.mma chain (M=128
-//     samples, N = width, K = 16 per instruction, fp16 operands, fp32
-//     accumulator in TMEM) + a ReLU/fp16 epilogue back into smem
-//   output layer + L1/L2 loss gradient on CUDA cores (network.py:96-114)
-//   backward (network.py:76-93): per layer dW_j += delta^T H_j (M=128 padded
-//     rows, K = 128 samples, accumulated in TMEM across all tiles of the CTA)
-//     and dX = delta W_j, masked by the stored activations
-//   encoder scatter of dL/dfeat (_kernels.py:82-92) with float2 atomics.
-// Weight gradients leave TMEM once per CTA as fp32 partials; a second kernel
-// sums them in fixed CTA order (deterministic MLP gradients).
+//  1. encode_tiles_kernel — hash-grid gather (_kernels.py:31-79), one thread
+//     per (sample, level), full occupancy: L2-latency/throughput bound.  The
+//     fp32 features (bit-exact) are rounded to fp16 and written straight
+//     into the UMMA core-matrix tile layout of tc.cuh (4 MB at cfg2, stays
+//     in L2).
+//  2. mlp_tc_kernel — one persistent CTA per SM walks 128-sample tiles:
+//     forward (network.py:61-74) as one tcgen05.mma chain per layer
+//     (M=128 samples, fp16 operands, fp32 accumulator in TMEM) with a
+//     ReLU/fp16 epilogue back into smem; output layer and L1/L2 gradient on
+//     CUDA cores (network.py:96-114); backward (network.py:76-93): per layer
+//     dW_j += delta^T H_j (accumulated in TMEM across all tiles of the CTA)
+//     and dX = delta W_j masked by the stored activations.  dL/dfeat leaves
+//     as fp32; dW leaves once per CTA as fp32 partials.
+//  3. scatter_kernel — encoder backward (_kernels.py:82-92): corners
+//     recomputed from the coordinates; the small dense coarse levels
+//     (contended by every sample) accumulate in shared memory and leave as
+//     per-CTA partials, the fine levels scatter with float2 REDs.
+// Partials are summed in fixed CTA order (deterministic MLP and coarse-level
+// gradients).
 //
 // Accuracy contract (north star): fp16 operands / fp32 accumulation, MLP
 // outputs and gradients within 1e-2 relative of the fp32 reference.
@@ -25,15 +33,15 @@ namespace nvol {
 constexpr int TC_THREADS = 256;
 constexpr int TILE = 128;
 constexpr int MAX_NH = 8;
+constexpr int SC_THREADS = 1024;
+constexpr uint32_t COARSE_BYTES = 48 * 1024;
 
 struct TcShape {
     int m, n, nin, ninp, nn, nh;
     int relu_out, loss_kind;
-    // smem byte offsets
-    uint32_t o_w[MAX_NH], o_wout, o_x, o_h[MAX_NH + 1], o_d[2], o_dout, o_dx, o_misc, smem_bytes;
-    // TMEM columns
+    uint32_t o_w[MAX_NH], o_wout, o_x, o_h[MAX_NH + 1], o_d[2], o_dout, o_misc, smem_bytes;
     uint32_t t_f, t_g, t_dw[MAX_NH], t_dwout, t_alloc;
-    int64_t w_floats;  // MLP weights in the flat buffer
+    int64_t w_floats;
 };
 
 static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, int loss_kind) {
@@ -62,8 +70,7 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
     s.o_d[0] = take(2u * TILE * nn);
     s.o_d[1] = take(2u * TILE * nn);
     s.o_dout = take(2048 + 256);
-    s.o_dx = take(4u * TILE * s.ninp);
-    s.o_misc = take(4u * TILE * 3 + 4u * TILE * 3 + 64);
+    s.o_misc = take(4u * TILE * 4 + 64);
     take(4096);  // slack: padded-M operand rows read past the last tile (values unused)
     s.smem_bytes = off;
     uint32_t col = 0;
@@ -85,7 +92,92 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
     return s.smem_bytes <= 227 * 1024;
 }
 
-// Columns [c0, c0+nc) of a width-W accumulator handled by thread half h.
+// Hash-grid levels fit 32-bit slot arithmetic (entries <= 2^24 for hashed
+// levels, dense levels hold <= T entries).
+__device__ __forceinline__ uint32_t slot32(uint32_t vx, uint32_t vy, uint32_t vz, uint32_t r1, uint32_t mask,
+                                           bool dense) {
+    if (dense) return (vz * r1 + vy) * r1 + vx;
+    return (vx ^ (vy * 2654435761u) ^ (vz * 805459861u)) & mask;
+}
+
+struct Cell32 {
+    uint32_t cx, cy, cz;
+    float fx, fy, fz;
+};
+
+__device__ __forceinline__ Cell32 cell32(float x, float y, float z, int32_t res) {
+    Cell<float> c = cell_of<float>(x, y, z, res);
+    return Cell32{(uint32_t)c.cx, (uint32_t)c.cy, (uint32_t)c.cz, c.fx, c.fy, c.fz};
+}
+
+__device__ __forceinline__ float cw32(const Cell32 &c, int k) {
+    float w = (k & 1) ? c.fx : xsub(1.0f, c.fx);
+    w = xmul(w, (k & 2) ? c.fy : xsub(1.0f, c.fy));
+    return xmul(w, (k & 4) ? c.fz : xsub(1.0f, c.fz));
+}
+
+// ============================================================================ 1. encode
+template <int NF>
+__global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restrict__ coords, int64_t b,
+                                                           const float *__restrict__ params, const GridTables tab,
+                                                           int ninp, uint8_t *__restrict__ xtiles) {
+    const int m = tab.n_levels;
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= b * m) return;
+    // level-major: a warp covers 32 consecutive samples of one level (uniform
+    // level constants, coalesced coordinates, L1 reuse on coarse levels)
+    const int l = (int)(t / b);
+    const int64_t i = t - (int64_t)l * b;
+    const int32_t res = tab.res[l];
+    const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
+    const bool dense = tab.dense[l] != 0;
+    const float *tb = params + tab.offset[l];
+    Cell32 c = cell32(__ldg(coords + 3 * i), __ldg(coords + 3 * i + 1), __ldg(coords + 3 * i + 2), res);
+    float acc[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) acc[f] = 0.0f;
+    uint32_t sl[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sl[k] = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask, dense);
+    if constexpr (NF == 2) {
+        float2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float2 *>(tb) + sl[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            float w = cw32(c, k);
+            acc[0] = xadd(acc[0], xmul(w, v[k].x));
+            acc[1] = xadd(acc[1], xmul(w, v[k].y));
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            float w = cw32(c, k);
+#pragma unroll
+            for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(tb + (size_t)sl[k] * NF + f)));
+        }
+    }
+    const int64_t tile = i >> 7;
+    const int s = (int)(i & 127);
+    uint8_t *base = xtiles + tile * (int64_t)(TILE * ninp * 2);
+    __half hv[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) hv[f] = __float2half_rn(acc[f] * tc::kFeatScale);
+#pragma unroll
+    for (int f = 0; f < NF; f += 2) {
+        if constexpr (NF == 1) {
+            *reinterpret_cast<__half *>(base + tc::tile_off(s, l, ninp)) = hv[0];
+        } else {
+            *reinterpret_cast<__half2 *>(base + tc::tile_off(s, l * NF + f, ninp)) = __halves2half2(hv[f], hv[f + 1]);
+        }
+    }
+    if (l == m - 1) {
+        for (int cidx = m * NF; cidx < ninp; ++cidx)
+            *reinterpret_cast<__half *>(base + tc::tile_off(s, cidx, ninp)) = __float2half_rn(0.0f);
+    }
+}
+
+// ============================================================================ 2. MLP
 __device__ __forceinline__ void half_cols(int w, int h, int &c0, int &nc) {
     if (w >= 32) {
         c0 = h * (w >> 1);
@@ -97,17 +189,13 @@ __device__ __forceinline__ void half_cols(int w, int h, int &c0, int &nc) {
 }
 
 __device__ __forceinline__ void store_row_f16(uint8_t *tile, int row, int c, int w, const float *v16, bool relu) {
-    // 16 consecutive columns c..c+15 of `row` (two 16-byte core-matrix rows)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        uint4 pk;
         float a[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) a[e] = relu ? fmaxf(v16[q * 8 + e], 0.0f) : v16[q * 8 + e];
-        pk.x = tc::pack_half2(a[0], a[1]);
-        pk.y = tc::pack_half2(a[2], a[3]);
-        pk.z = tc::pack_half2(a[4], a[5]);
-        pk.w = tc::pack_half2(a[6], a[7]);
+        uint4 pk = make_uint4(tc::pack_half2(a[0], a[1]), tc::pack_half2(a[2], a[3]), tc::pack_half2(a[4], a[5]),
+                              tc::pack_half2(a[6], a[7]));
         *reinterpret_cast<uint4 *>(tile + tc::tile_off(row, c + q * 8, w)) = pk;
     }
 }
@@ -126,40 +214,57 @@ __device__ __forceinline__ void load_row_f16(const uint8_t *tile, int row, int c
     }
 }
 
-template <int NF>
-__global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
-    const float *__restrict__ coords, const float *__restrict__ targets, int64_t b, double inv_bglobal,
-    const float *__restrict__ params, float *__restrict__ grads, const GridTables tab, const TcShape sh,
-    const float *__restrict__ wflat, double *__restrict__ loss_sum, float *__restrict__ partials) {
+// fp32 weights (flat buffer) -> the shared-memory image the MLP kernels copy
+// verbatim: W_0..W_{nh-1} as fp16 core-matrix tiles at o_w[i] (input columns
+// padded to ninp with zeros) and the fp32 output row at o_wout.
+struct MlpImage {
+    uint32_t o_w[MAX_NH], o_wout;
+};
+
+__global__ void pack_mlp_image_kernel(const float *__restrict__ wflat, int nin, int ninp, int nn, int nh,
+                                      const MlpImage img, uint8_t *__restrict__ out) {
+    const int stride = gridDim.x * blockDim.x;
+    const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const float *src = wflat;
+    for (int i = 0; i < nh; ++i) {
+        const int win = i == 0 ? nin : nn, wp = i == 0 ? ninp : nn;
+        for (int q = t0; q < nn * wp; q += stride) {
+            int o = q / wp, j = q % wp;
+            *reinterpret_cast<__half *>(out + img.o_w[i] + tc::tile_off(o, j, wp)) =
+                __float2half_rn(j < win ? src[o * win + j] : 0.0f);
+        }
+        src += (int64_t)nn * win;
+    }
+    for (int q = t0; q < nn; q += stride) reinterpret_cast<float *>(out + img.o_wout)[q] = src[q];
+}
+
+int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const uint32_t *o_w, uint32_t o_wout,
+                   uint8_t *image, cudaStream_t s) {
+    MlpImage img;
+    for (int i = 0; i < nh; ++i) img.o_w[i] = o_w[i];
+    img.o_wout = o_wout;
+    pack_mlp_image_kernel<<<64, 256, 0, s>>>(wflat, nin, ninp, nn, nh, img, image);
+    return check_launch("pack_mlp_image");
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
+    const uint8_t *__restrict__ xtiles, const float *__restrict__ targets, int64_t b, double inv_bglobal, float dscale,
+    const TcShape sh, const uint8_t *__restrict__ wimg, double *__restrict__ loss_sum, float *__restrict__ dfeat,
+    float *__restrict__ partials) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x;
-    const int s = tid & (TILE - 1);     // sample row == TMEM lane
-    const int h = tid >> 7;             // thread half
+    const int s = tid & (TILE - 1);
+    const int h = tid >> 7;
     const int warp = tid >> 5;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int NN = sh.nn, NINP = sh.ninp, NH = sh.nh, M = sh.m;
-
-    // ---------------------------------------------------------------- setup
-    // weights -> fp16 tiles (padded input columns are zero)
+    const int NN = sh.nn, NINP = sh.ninp, NH = sh.nh, NIN = sh.nin;
     {
-        const float *src = wflat;
-        for (int i = 0; i < NH; ++i) {
-            int win = (i == 0) ? sh.nin : NN, wp = (i == 0) ? NINP : NN;
-            uint8_t *dst = smem + sh.o_w[i];
-            for (int q = tid; q < NN * wp; q += TC_THREADS) {
-                int o = q / wp, j = q % wp;
-                float v = j < win ? src[o * win + j] : 0.0f;
-                *reinterpret_cast<__half *>(dst + tc::tile_off(o, j, wp)) = __float2half_rn(v);
-            }
-            src += (int64_t)NN * win;
-        }
-        float *wout = reinterpret_cast<float *>(smem + sh.o_wout);
-        for (int q = tid; q < NN; q += TC_THREADS) wout[q] = src[q];
-        // zero the whole feature tile once (padding columns stay zero)
-        for (int q = tid; q < TILE * NINP / 8; q += TC_THREADS)
-            reinterpret_cast<uint4 *>(smem + sh.o_x)[q] = make_uint4(0, 0, 0, 0);
+        // fp16 weight tiles + fp32 output row, pre-packed once per step (independent 16-byte loads)
+        const uint4 *src = reinterpret_cast<const uint4 *>(wimg);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem);
+        for (int q = tid; q < (int)(sh.o_x / 16); q += TC_THREADS) dst[q] = __ldg(src + q);
         for (int q = tid; q < (2048 + 256) / 16; q += TC_THREADS)
             reinterpret_cast<uint4 *>(smem + sh.o_dout)[q] = make_uint4(0, 0, 0, 0);
     }
@@ -173,63 +278,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
     tc::fence_after();
     const uint32_t tmem = tmem_base_sh;
     uint32_t phase = 0;
-
-    float *s_coords = reinterpret_cast<float *>(smem + sh.o_misc);
-    float *s_part = s_coords + TILE * 3;
+    float *s_part = reinterpret_cast<float *>(smem + sh.o_misc);
     float *s_delta = s_part + TILE;
-    float *s_dx = reinterpret_cast<float *>(smem + sh.o_dx);
     const float *s_wout = reinterpret_cast<const float *>(smem + sh.o_wout);
-
     const uint32_t idesc_fwd = tc::make_idesc(128, NN, 0, 0);
-    const int mh = (M + 1) / 2;  // levels per thread half
-    const int l_lo = h * mh, l_hi = min(M, (h + 1) * mh);
     const int64_t ntiles = (b + TILE - 1) / TILE;
+    const int tile_u4 = TILE * NINP * 2 / 16;
     bool first_tile = true;
 
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t row = tile * TILE + s;
         const bool valid = row < b;
-        float x = 0.f, y = 0.f, z = 0.f, tgt = 0.f;
-        if (valid) {
-            x = coords[3 * row];
-            y = coords[3 * row + 1];
-            z = coords[3 * row + 2];
-            tgt = targets[row];
-        }
-        // ------------------------------------------------------------ encode (bit-exact fp32, stored fp16)
+        const float tgt = valid ? targets[row] : 0.0f;
+        // ---- X tile: global (L2) -> smem; rows past the batch are zeroed
         {
-            uint8_t *sx = smem + sh.o_x;
-            for (int l = l_lo; l < l_hi; ++l) {
-                const int32_t res = tab.res[l];
-                Cell<float> c = cell_of<float>(x, y, z, res);
-                float acc[NF];
-#pragma unroll
-                for (int f = 0; f < NF; ++f) acc[f] = 0.0f;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    int64_t slot = vertex_slot(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), res,
-                                               tab.entries[l], tab.dense[l] != 0);
-                    float w = corner_weight<float>(c, k);
-                    const float *p = params + tab.offset[l] + slot * NF;
-                    if constexpr (NF == 2) {
-                        float2 v = __ldg(reinterpret_cast<const float2 *>(p));
-                        acc[0] = xadd(acc[0], xmul(w, v.x));
-                        acc[1] = xadd(acc[1], xmul(w, v.y));
-                    } else {
-#pragma unroll
-                        for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(p + f)));
-                    }
-                }
-#pragma unroll
-                for (int f = 0; f < NF; ++f)
-                    *reinterpret_cast<__half *>(sx + tc::tile_off(s, l * NF + f, NINP)) =
-                        __float2half_rn(valid ? acc[f] : 0.0f);
+            const uint4 *src = reinterpret_cast<const uint4 *>(xtiles + tile * (int64_t)(TILE * NINP * 2));
+            uint4 *dst = reinterpret_cast<uint4 *>(smem + sh.o_x);
+            const int64_t nvalid = b - tile * TILE;
+            for (int q = tid; q < tile_u4; q += TC_THREADS) {
+                // core-matrix row q*16 bytes -> sample row ((q*16/128)/(NINP/8))*8 + (q%8)
+                int cm = q >> 3, r = ((cm / (NINP / 8)) << 3) + (q & 7);
+                dst[q] = r < nvalid ? src[q] : make_uint4(0, 0, 0, 0);
             }
         }
         tc::fence_proxy_async();
         __syncthreads();
 
-        // ------------------------------------------------------------ forward
+        // ---- forward
         float outp = 0.0f;
         for (int i = 0; i < NH; ++i) {
             const int win = (i == 0) ? NINP : NN;
@@ -250,10 +325,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
             int c0, nc;
             half_cols(NN, h, c0, nc);
             uint8_t *dst = smem + sh.o_h[i + 1];
+            const float unscale = i == 0 ? 1.0f / tc::kFeatScale : 1.0f;
             for (int c = c0; c < c0 + nc; c += 16) {
                 float v[16];
                 tc::tmem_ld16(tmem + lane_base + sh.t_f + c, v);
                 tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] *= unscale;
                 store_row_f16(dst, s, c, NN, v, true);
                 if (i == NH - 1) {
 #pragma unroll
@@ -264,7 +342,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
             tc::fence_proxy_async();
             __syncthreads();
         }
-        // ------------------------------------------------------------ output layer + loss
+        // ---- output layer + loss gradient
         if (h == 1) s_part[s] = outp;
         __syncthreads();
         if (h == 0) {
@@ -286,17 +364,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
                 sl = 0.0;
             }
             s_delta[s] = gf;
-            // delta_out as the MN-major A operand of dW_out: element (m=0, k=s)
-            *reinterpret_cast<__half *>(smem + sh.o_dout + (s >> 3) * 128 + (s & 7) * 16) = __float2half_rn(gf);
+            *reinterpret_cast<__half *>(smem + sh.o_dout + (s >> 3) * 128 + (s & 7) * 16) = __float2half_rn(gf * dscale);
             for (int o2 = 16; o2 > 0; o2 >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o2);
             if ((tid & 31) == 0) atomicAdd(loss_sum, sl);
         }
         __syncthreads();
-        // delta_NH = g * w_out * 1[h_NH > 0]
         {
             int c0, nc;
             half_cols(NN, h, c0, nc);
-            const float g = s_delta[s];
+            const float g = s_delta[s] * dscale;
             const uint8_t *hn = smem + sh.o_h[NH];
             uint8_t *dd = smem + sh.o_d[0];
             for (int c = c0; c < c0 + nc; c += 16) {
@@ -310,7 +386,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
         tc::fence_proxy_async();
         __syncthreads();
 
-        // ------------------------------------------------------------ backward
+        // ---- backward
         int cur = 0;
         for (int j = NH - 1; j >= 0; --j) {
             const int win = (j == 0) ? NINP : NN;
@@ -318,7 +394,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
                 tc::fence_after();
                 const uint32_t dA = tc::smem_u32(smem + sh.o_d[cur]);
                 if (j == NH - 1) {
-                    // dW_out += delta_out^T H_NH  (row 0 of an M=128 accumulator)
                     const uint32_t a0 = tc::smem_u32(smem + sh.o_dout);
                     const uint32_t b0 = tc::smem_u32(smem + sh.o_h[NH]);
                     const uint32_t id = tc::make_idesc(128, NN, 1, 1);
@@ -328,7 +403,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
                         tc::mma_f16(tmem + sh.t_dwout, ad, bd, id, (first_tile && k == 0) ? 0 : 1);
                     }
                 }
-                // dW_j += delta^T H_j   (A: delta MN-major, B: H_j MN-major)
                 {
                     const uint32_t b0 = tc::smem_u32(smem + sh.o_h[j]);
                     const uint32_t id = tc::make_idesc(128, win, 1, 1);
@@ -338,7 +412,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
                         tc::mma_f16(tmem + sh.t_dw[j], ad, bd, id, (first_tile && k == 0) ? 0 : 1);
                     }
                 }
-                // dX = delta W_j   (A: delta K-major, B: W_j MN-major)
                 {
                     const uint32_t b0 = tc::smem_u32(smem + sh.o_w[j]);
                     const uint32_t id = tc::make_idesc(128, win, 0, 1);
@@ -373,7 +446,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
                     tc::tmem_ld16(tmem + lane_base + sh.t_g + c, v);
                     tc::tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) s_dx[s * NINP + c + e] = v[e];
+                    for (int e = 0; e < 16; ++e) v[e] *= 1.0f / dscale;
+                    if (valid) {
+                        // feature-major dL/dfeat [NIN][B]: a warp stores 32 consecutive rows per column
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if (c + e < NIN) dfeat[(int64_t)(c + e) * b + row] = v[e];
+                    }
                 }
             }
             tc::fence_before();
@@ -381,52 +460,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
             __syncthreads();
             cur ^= 1;
         }
-        // ------------------------------------------------------------ encoder scatter
-        if (valid) {
-            for (int l = l_lo; l < l_hi; ++l) {
-                const int32_t res = tab.res[l];
-                Cell<float> c = cell_of<float>(x, y, z, res);
-                float dv[NF];
-#pragma unroll
-                for (int f = 0; f < NF; ++f) dv[f] = s_dx[s * NINP + l * NF + f];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    int64_t slot = vertex_slot(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), res,
-                                               tab.entries[l], tab.dense[l] != 0);
-                    float w = corner_weight<float>(c, k);
-                    float *g = grads + tab.offset[l] + slot * NF;
-                    if constexpr (NF == 2) {
-                        atomicAdd(reinterpret_cast<float2 *>(g), make_float2(w * dv[0], w * dv[1]));
-                    } else if constexpr (NF == 4 || NF == 8) {
-#pragma unroll
-                        for (int q = 0; q < NF / 4; ++q)
-                            atomicAdd(reinterpret_cast<float4 *>(g) + q,
-                                      make_float4(w * dv[4 * q], w * dv[4 * q + 1], w * dv[4 * q + 2], w * dv[4 * q + 3]));
-                    } else {
-                        atomicAdd(g, w * dv[0]);
-                    }
-                }
-            }
-        }
         first_tile = false;
     }
 
-    // ---------------------------------------------------------------- flush dW partials
+    // ---- flush dW partials (fp32) once per CTA
+    float *dst = partials + (int64_t)blockIdx.x * sh.w_floats;
     if (!first_tile) {
-        float *dst = partials + (int64_t)blockIdx.x * sh.w_floats;
-        const int o = (warp & 3) * 32 + (tid & 31);  // accumulator row == output neuron
+        const int o = (warp & 3) * 32 + (tid & 31);
         int64_t base = 0;
         for (int j = 0; j <= NH; ++j) {
-            const int win = (j == 0) ? sh.nin : NN;     // unpadded columns
+            const int win = (j == 0) ? NIN : NN;
             const int wacc = (j == 0) ? NINP : NN;
             const int rows = (j == NH) ? 1 : NN;
             const uint32_t tcol = (j == NH) ? sh.t_dwout : sh.t_dw[j];
+            const float unscale = (j == 0) ? 1.0f / (dscale * tc::kFeatScale) : 1.0f / dscale;
             int c0, nc;
             half_cols(wacc, h, c0, nc);
             for (int c = c0; c < c0 + nc; c += 16) {
                 float v[16];
                 tc::tmem_ld16(tmem + lane_base + tcol + c, v);
                 tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] *= unscale;
                 if (o < rows) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e)
@@ -436,7 +491,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
             base += (int64_t)rows * win;
         }
     } else {
-        float *dst = partials + (int64_t)blockIdx.x * sh.w_floats;
         for (int64_t q = tid; q < sh.w_floats; q += TC_THREADS) dst[q] = 0.0f;
     }
     tc::fence_before();
@@ -444,70 +498,190 @@ __global__ void __launch_bounds__(TC_THREADS, 1) train_tc_kernel(
     if (warp == 0) tc::tmem_dealloc(tmem, sh.t_alloc);
 }
 
-// grads_w[i] += sum over CTAs (fixed order) of partials[c][i]
-__global__ void reduce_partials_kernel(const float *__restrict__ partials, int nparts, int64_t n,
-                                       float *__restrict__ gw) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float acc = 0.0f;
-    for (int c = 0; c < nparts; ++c) acc += partials[(int64_t)c * n + i];
-    gw[i] += acc;
+// ============================================================================ 3. scatter
+template <int NF>
+__global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__restrict__ coords,
+                                                                const float *__restrict__ dfeat, int64_t b,
+                                                                const GridTables tab, int n_coarse, int coarse_floats,
+                                                                float *__restrict__ grads,
+                                                                float *__restrict__ partials) {
+    extern __shared__ float acc_s[];
+    for (int q = threadIdx.x; q < coarse_floats; q += SC_THREADS) acc_s[q] = 0.0f;
+    __syncthreads();
+    const int m = tab.n_levels, nin = m * NF;
+    const int64_t items = b * m;
+    for (int64_t t = (int64_t)blockIdx.x * SC_THREADS + threadIdx.x; t < items; t += (int64_t)gridDim.x * SC_THREADS) {
+        const int l = (int)(t / b);          // level-major, as the encode kernel
+        const int64_t i = t - (int64_t)l * b;
+        const int32_t res = tab.res[l];
+        const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
+        const bool dense = tab.dense[l] != 0;
+        Cell32 c = cell32(__ldg(coords + 3 * i), __ldg(coords + 3 * i + 1), __ldg(coords + 3 * i + 2), res);
+        float d[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) d[f] = __ldg(dfeat + (int64_t)(l * NF + f) * b + i);
+        const bool coarse = l < n_coarse;
+        float *gl = coarse ? acc_s + tab.offset[l] : grads + tab.offset[l];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint32_t slot = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask, dense);
+            float w = cw32(c, k);
+            float *g = gl + (size_t)slot * NF;
+            if (coarse) {
+#pragma unroll
+                for (int f = 0; f < NF; ++f) atomicAdd(g + f, w * d[f]);
+            } else if constexpr (NF == 2) {
+                atomicAdd(reinterpret_cast<float2 *>(g), make_float2(w * d[0], w * d[1]));
+            } else if constexpr (NF == 4 || NF == 8) {
+#pragma unroll
+                for (int q = 0; q < NF / 4; ++q)
+                    atomicAdd(reinterpret_cast<float4 *>(g) + q,
+                              make_float4(w * d[4 * q], w * d[4 * q + 1], w * d[4 * q + 2], w * d[4 * q + 3]));
+            } else {
+                atomicAdd(g, w * d[0]);
+            }
+        }
+    }
+    __syncthreads();
+    float *dst = partials + (int64_t)blockIdx.x * coarse_floats;
+    for (int q = threadIdx.x; q < coarse_floats; q += SC_THREADS) dst[q] = acc_s[q];
 }
 
-static int g_sms = 0;
+// g[i] += sum_c partials[c][i] in fixed c order.  Block = 32 outputs x 8
+// CTA groups; the 8 group sums combine in fixed order through shared memory.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float *__restrict__ partials, int nparts,
+                                                              int64_t n, float *__restrict__ g) {
+    __shared__ float red[8][33];
+    const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+    float acc = 0.0f;
+    if (i < n)
+        for (int c = grp; c < nparts; c += 8) acc += partials[(int64_t)c * n + i];
+    red[grp][lane] = acc;
+    __syncthreads();
+    if (grp == 0 && i < n) {
+        float s = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += red[q][lane];
+        g[i] += s;
+    }
+}
 
-int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
+// ============================================================================ host side
+struct TcPlan {
     TcShape sh;
-    if (!build_shape(sh, m, n, nn, nh, 1, 0)) return 0;
-    if (g_sms == 0) {
+    int grid_mlp, grid_sc, n_coarse, coarse_floats;
+    int64_t ntiles, off_x, off_dfeat, off_wpart, off_cpart, off_img, total;
+};
+
+static int num_sms() {
+    static int sms = 0;
+    if (sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_sms <= 0) g_sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
     }
-    return (int64_t)g_sms * sh.w_floats * 4 + 256;
+    return sms;
+}
+
+static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh, int relu_out, int loss_kind) {
+    if (!build_shape(p.sh, tab.n_levels, tab.n_feat, nn, nh, relu_out, loss_kind)) return 0;
+    for (int l = 0; l < tab.n_levels; ++l)
+        if (tab.entries[l] >= (1ll << 31)) return 0;
+    const int sms = num_sms();
+    p.ntiles = (b + TILE - 1) / TILE;
+    p.grid_mlp = (int)(p.ntiles < sms ? p.ntiles : sms);
+    p.grid_sc = sms;
+    p.n_coarse = 0;
+    p.coarse_floats = 0;
+    for (int l = 0; l < tab.n_levels; ++l) {
+        int64_t end = tab.offset[l] + tab.entries[l] * tab.n_feat;
+        if (!tab.dense[l] || end * 4 > (int64_t)COARSE_BYTES) break;
+        p.n_coarse = l + 1;
+        p.coarse_floats = (int)end;
+    }
+    auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+    p.off_x = 0;
+    p.off_dfeat = al(p.ntiles * TILE * p.sh.ninp * 2);
+    p.off_wpart = p.off_dfeat + al(b * p.sh.nin * 4);
+    p.off_cpart = p.off_wpart + al((int64_t)p.grid_mlp * p.sh.w_floats * 4);
+    p.off_img = p.off_cpart + al((int64_t)p.grid_sc * p.coarse_floats * 4);
+    p.total = p.off_img + al(p.sh.o_x) + 256;
+    return 1;
+}
+
+int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
+    GridTables tab{};
+    tab.n_levels = m;
+    tab.n_feat = n;
+    // workspace size does not depend on the level tables beyond m, n and the
+    // coarse prefix, which is bounded by COARSE_BYTES
+    TcPlan p;
+    if (!build_shape(p.sh, m, n, nn, nh, 1, 0)) return 0;
+    const int sms = num_sms();
+    int64_t ntiles = (b + TILE - 1) / TILE;
+    int grid_mlp = (int)(ntiles < sms ? ntiles : sms);
+    auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+    return al(ntiles * TILE * p.sh.ninp * 2) + al(b * p.sh.nin * 4) + al((int64_t)grid_mlp * p.sh.w_floats * 4) +
+           al((int64_t)sms * (COARSE_BYTES / 4) * 4) + al(p.sh.o_x) + 256;
 }
 
 int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_t b_global, const float *params,
                     float *grads, const GridTables &tab, int nn, int nh, int relu_out, int loss_kind,
                     double *loss_sum, void *workspace, int64_t ws_bytes, cudaStream_t s) {
-    TcShape sh;
-    if (!build_shape(sh, tab.n_levels, tab.n_feat, nn, nh, relu_out, loss_kind)) {
-        set_error("MLP shape not supported by the tcgen05 path");
+    TcPlan p;
+    if (!make_plan(p, b, tab, nn, nh, relu_out, loss_kind)) {
+        set_error("MLP / grid shape not supported by the tcgen05 path");
         return NVOL_EINVAL;
     }
+    NVOL_REQUIRE(ws_bytes >= p.total, "workspace too small for the tcgen05 pipeline");
+    uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
+    uint8_t *xt = ws + p.off_x;
+    float *dfeat = reinterpret_cast<float *>(ws + p.off_dfeat);
+    float *wpart = reinterpret_cast<float *>(ws + p.off_wpart);
+    float *cpart = reinterpret_cast<float *>(ws + p.off_cpart);
+    uint8_t *wimg = ws + p.off_img;
     int64_t enc = 0;
     for (int l = 0; l < tab.n_levels; ++l) enc = max(enc, tab.offset[l] + tab.entries[l] * tab.n_feat);
-    int64_t woff = (enc + 3) & ~(int64_t)3;
-    int64_t ntiles = (b + TILE - 1) / TILE;
-    int64_t sms = g_sms > 0 ? g_sms : 148;
-    int grid = (int)(ntiles < sms ? ntiles : sms);
-    float *partials = reinterpret_cast<float *>(workspace);
-    NVOL_REQUIRE(ws_bytes >= (int64_t)grid * sh.w_floats * 4, "workspace too small for tcgen05 partials");
-    const double inv_bg = 1.0 / (double)b_global;
+    const int64_t woff = (enc + 3) & ~(int64_t)3;
+    const unsigned egrid = grid_for(b * tab.n_levels, 256);
     switch (tab.n_feat) {
-#define LAUNCH_TC(NFV)                                                                                        \
-    case NFV:                                                                                                 \
-        cudaFuncSetAttribute(train_tc_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes); \
-        train_tc_kernel<NFV><<<grid, TC_THREADS, sh.smem_bytes, s>>>(coords, targets, b, inv_bg, params, grads, tab, \
-                                                                    sh, params + woff, loss_sum, partials);    \
-        break;
-        LAUNCH_TC(1)
-        LAUNCH_TC(2)
-        LAUNCH_TC(4)
-        LAUNCH_TC(8)
-#undef LAUNCH_TC
+        case 1: encode_tiles_kernel<1><<<egrid, 256, 0, s>>>(coords, b, params, tab, p.sh.ninp, xt); break;
+        case 2: encode_tiles_kernel<2><<<egrid, 256, 0, s>>>(coords, b, params, tab, p.sh.ninp, xt); break;
+        case 4: encode_tiles_kernel<4><<<egrid, 256, 0, s>>>(coords, b, params, tab, p.sh.ninp, xt); break;
+        default: encode_tiles_kernel<8><<<egrid, 256, 0, s>>>(coords, b, params, tab, p.sh.ninp, xt); break;
     }
-    int st = check_launch("train_tc_kernel");
+    int st = check_launch("encode_tiles_kernel");
     if (st) return st;
-    reduce_partials_kernel<<<grid_for(sh.w_floats, 256), 256, 0, s>>>(partials, grid, sh.w_floats, grads + woff);
+    st = pack_mlp_image(params + woff, p.sh.nin, p.sh.ninp, nn, nh, p.sh.o_w, p.sh.o_wout, wimg, s);
+    if (st) return st;
+    cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh.smem_bytes);
+    const float dscale = exp2f(rintf(log2f((float)b_global)));  // ~B: L1 deltas become +-1 in fp16
+    mlp_tc_kernel<<<p.grid_mlp, TC_THREADS, p.sh.smem_bytes, s>>>(xt, targets, b, 1.0 / (double)b_global, dscale, p.sh,
+                                                                   wimg, loss_sum, dfeat, wpart);
+    st = check_launch("mlp_tc_kernel");
+    if (st) return st;
+    const size_t csm = (size_t)p.coarse_floats * 4;
+    switch (tab.n_feat) {
+#define LAUNCH_SC(NFV)                                                                                        \
+    case NFV:                                                                                                 \
+        cudaFuncSetAttribute(scatter_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);     \
+        scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, s>>>(coords, dfeat, b, tab, p.n_coarse, p.coarse_floats, \
+                                                              grads, cpart);                                  \
+        break;
+        LAUNCH_SC(1)
+        LAUNCH_SC(2)
+        LAUNCH_SC(4)
+        LAUNCH_SC(8)
+#undef LAUNCH_SC
+    }
+    st = check_launch("scatter_kernel");
+    if (st) return st;
+    reduce_partials_kernel<<<grid_for(p.sh.w_floats, 32), 256, 0, s>>>(wpart, p.grid_mlp, p.sh.w_floats, grads + woff);
+    if (p.coarse_floats > 0)
+        reduce_partials_kernel<<<grid_for(p.coarse_floats, 32), 256, 0, s>>>(cpart, p.grid_sc, p.coarse_floats, grads);
     return check_launch("reduce_partials");
-}
-
-int nvol_decode_tc(const float *, const GridTables &, const float *, const int32_t *, int32_t, int32_t, int64_t,
-                   int64_t, int64_t, int64_t, int64_t, double, double, float *, cudaStream_t) {
-    set_error("tcgen05 decode path not built");
-    return NVOL_EINVAL;
 }
 
 }  // namespace nvol

@@ -315,11 +315,28 @@ class NeuralModel:
         c = self.encoder.config
         off, res, ent, dense = self.encoder.c_tables()
         widths = self._widths()
-        _lib.call("nvol_field_eval_exact", _lib.ptr(coords.contiguous()), b, _lib.ptr(self.flat_params), off, res,
-                  ent, dense, c.n_levels, c.n_features_per_level, _lib.ptr(self._weights_flat()),
-                  _lib.host_i32(widths), len(widths) - 1, int(self.mlp.config.output_activation == "relu"),
-                  _lib.ptr(o), _lib.stream())
+        relu = int(self.mlp.config.output_activation == "relu")
+        if mode == "tensor":
+            _lib.call("nvol_field_eval_tc", _lib.ptr(coords.contiguous()), b, _lib.ptr(self.flat_params), off, res,
+                      ent, dense, c.n_levels, c.n_features_per_level, _lib.ptr(self._weights_flat()),
+                      _lib.host_i32(widths), len(widths) - 1, relu, _lib.ptr(self.mlp_image()), _lib.ptr(o),
+                      _lib.stream())
+        else:
+            _lib.call("nvol_field_eval_exact", _lib.ptr(coords.contiguous()), b, _lib.ptr(self.flat_params), off,
+                      res, ent, dense, c.n_levels, c.n_features_per_level, _lib.ptr(self._weights_flat()),
+                      _lib.host_i32(widths), len(widths) - 1, relu, _lib.ptr(o), _lib.stream())
         return o
+
+    def mlp_image(self) -> torch.Tensor:
+        """Device scratch the tensor-core evaluators pack the weights into (refilled on every call)."""
+        if getattr(self, "_img", None) is None:
+            c = self.encoder.config
+            n = int(_lib.load().nvol_mlp_image_bytes(c.n_levels, c.n_features_per_level, self.mlp.config.n_neurons,
+                                                      self.mlp.config.n_hidden_layers))
+            if n <= 0:
+                raise ConfigError("MLP shape not supported by the tcgen05 inference path")
+            self._img = torch.empty(n, dtype=torch.uint8, device=self.flat_params.device)
+        return self._img
 
     def eval_batch(self, coords):
         """Phi(coords) in normalised value space (model.py:178-182)."""
