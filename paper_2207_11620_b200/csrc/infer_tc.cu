@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
             }
 #pragma unroll
             for (int f = 0; f < NF; ++f)
-                *reinterpret_cast<__half *>(sx + tc::tile_off(s, l * NF + f, NINP)) = __float2half_rn(acc[f] * tc::kFeatScale);
+                *reinterpret_cast<__half *>(sx + tc::tile_off(s, l * NF + f, NINP)) = __float2half_rn(acc[f] * tc::kActScale);
         }
         tc::fence_proxy_async();
         __syncthreads();
@@ -156,13 +156,10 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
             phase ^= 1;
             tc::fence_after();
             uint8_t *dst = smem + sh.o_h[li & 1];
-            const float unscale = li == 0 ? 1.0f / tc::kFeatScale : 1.0f;
-            for (int c = c0; c < c0 + nc; c += 16) {
+            for (int c = c0; c < c0 + nc; c += 16) {   // values carry kActScale (see tc.cuh)
                 float v[16];
                 tc::tmem_ld16(tmem + lane_base + c, v);
                 tc::tmem_wait_ld();
-#pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] *= unscale;
                 if (li < NH - 1) {
                     st_f16x16(dst, s, c, NN, v, true);
                 } else {
@@ -177,7 +174,7 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
         if (h == 1) s_part[s] = outp;
         __syncthreads();
         if (h == 0 && valid) {
-            float o = outp + s_part[s];
+            float o = (outp + s_part[s]) * (1.0f / tc::kActScale);
             if (sh.relu_out) o = fmaxf(o, 0.0f);
             out[i] = decode ? (float)__dadd_rn(__dmul_rn((double)o, scale), lo) : o;
         }

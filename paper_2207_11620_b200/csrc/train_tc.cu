@@ -140,9 +140,21 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
 #pragma unroll
     for (int k = 0; k < 8; ++k) sl[k] = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask, dense);
     if constexpr (NF == 2) {
+        // x-adjacent corners (k, k+1) whose slots differ only in bit 0 share
+        // one aligned 16-byte entry pair: fetch it with a single float4 load
         float2 v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float2 *>(tb) + sl[k]);
+        for (int k = 0; k < 8; k += 2) {
+            if ((sl[k] ^ sl[k + 1]) == 1u) {
+                float4 q = __ldg(reinterpret_cast<const float4 *>(tb) + (sl[k] >> 1));
+                const bool lo_first = (sl[k] & 1u) == 0u;
+                v[k] = lo_first ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
+                v[k + 1] = lo_first ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
+            } else {
+                v[k] = __ldg(reinterpret_cast<const float2 *>(tb) + sl[k]);
+                v[k + 1] = __ldg(reinterpret_cast<const float2 *>(tb) + sl[k + 1]);
+            }
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             float w = cw32(c, k);
@@ -162,7 +174,7 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
     uint8_t *base = xtiles + tile * (int64_t)(TILE * ninp * 2);
     __half hv[NF];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) hv[f] = __float2half_rn(acc[f] * tc::kFeatScale);
+    for (int f = 0; f < NF; ++f) hv[f] = __float2half_rn(acc[f] * tc::kActScale);
 #pragma unroll
     for (int f = 0; f < NF; f += 2) {
         if constexpr (NF == 1) {
@@ -325,13 +337,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
             int c0, nc;
             half_cols(NN, h, c0, nc);
             uint8_t *dst = smem + sh.o_h[i + 1];
-            const float unscale = i == 0 ? 1.0f / tc::kFeatScale : 1.0f;
+            // accumulator = kActScale * pre-activation: ReLU commutes with the
+            // positive scale, so the stored activations stay scaled too
             for (int c = c0; c < c0 + nc; c += 16) {
                 float v[16];
                 tc::tmem_ld16(tmem + lane_base + sh.t_f + c, v);
                 tc::tmem_wait_ld();
-#pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] *= unscale;
                 store_row_f16(dst, s, c, NN, v, true);
                 if (i == NH - 1) {
 #pragma unroll
@@ -346,7 +357,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
         if (h == 1) s_part[s] = outp;
         __syncthreads();
         if (h == 0) {
-            float o = outp + s_part[s];
+            float o = (outp + s_part[s]) * (1.0f / tc::kActScale);
             float pred = sh.relu_out ? fmaxf(o, 0.0f) : o;
             double d = (double)pred - (double)tgt;
             double g, sl;
@@ -473,7 +484,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
             const int wacc = (j == 0) ? NINP : NN;
             const int rows = (j == NH) ? 1 : NN;
             const uint32_t tcol = (j == NH) ? sh.t_dwout : sh.t_dw[j];
-            const float unscale = (j == 0) ? 1.0f / (dscale * tc::kFeatScale) : 1.0f / dscale;
+            const float unscale = 1.0f / (dscale * tc::kActScale);  // dW = (dscale*delta)^T (kActScale*H)
             int c0, nc;
             half_cols(wacc, h, c0, nc);
             for (int c = c0; c < c0 + nc; c += 16) {
@@ -522,6 +533,28 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
         for (int f = 0; f < NF; ++f) d[f] = __ldg(dfeat + (int64_t)(l * NF + f) * b + i);
         const bool coarse = l < n_coarse;
         float *gl = coarse ? acc_s + tab.offset[l] : grads + tab.offset[l];
+        if constexpr (NF == 2) {
+            if (!coarse) {
+                // fine levels: x-adjacent corner pairs in one aligned 16-byte
+                // entry pair go out as a single float4 RED
+#pragma unroll
+                for (int k = 0; k < 8; k += 2) {
+                    const uint32_t yo = (k >> 1) & 1, zo = (k >> 2) & 1;
+                    uint32_t s0 = slot32(c.cx, c.cy + yo, c.cz + zo, r1, mask, dense);
+                    uint32_t s1 = slot32(c.cx + 1, c.cy + yo, c.cz + zo, r1, mask, dense);
+                    float w0 = cw32(c, k), w1 = cw32(c, k + 1);
+                    if ((s0 ^ s1) == 1u) {
+                        float4 q = (s0 & 1u) == 0u ? make_float4(w0 * d[0], w0 * d[1], w1 * d[0], w1 * d[1])
+                                                   : make_float4(w1 * d[0], w1 * d[1], w0 * d[0], w0 * d[1]);
+                        atomicAdd(reinterpret_cast<float4 *>(gl) + (s0 >> 1), q);
+                    } else {
+                        atomicAdd(reinterpret_cast<float2 *>(gl) + s0, make_float2(w0 * d[0], w0 * d[1]));
+                        atomicAdd(reinterpret_cast<float2 *>(gl) + s1, make_float2(w1 * d[0], w1 * d[1]));
+                    }
+                }
+                continue;
+            }
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             uint32_t slot = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask, dense);
