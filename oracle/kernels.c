@@ -116,7 +116,7 @@ void orc_grid_encode_bwd(const float *dl_dfeat, const int64_t *idx_cache, const 
  * _kernels.py:154-176 field_eval_model: fused per-sample encode + serial
  * float32 matvec chain, bias-free, ReLU on hidden layers (and output if
  * relu_out).  weights: concatenated row-major W_i (out x in); widths[0..nl]. */
-static float field_one(float x, float y, float z, const float *params, const int64_t *level_off,
+float orc_field_one(float x, float y, float z, const float *params, const int64_t *level_off,
                        const int64_t *level_res, const int64_t *level_entries,
                        const uint8_t *level_dense, int m, int n_feat, const float *weights,
                        const int *widths, int nl, int relu_out, float *h0, float *h1) {
@@ -169,7 +169,7 @@ void orc_field_eval_model(const float *coords, int64_t b, const float *params,
         (void)maxw;
         #pragma omp for schedule(static)
         for (int64_t i = 0; i < b; ++i)
-            out[i] = field_one(coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], params,
+            out[i] = orc_field_one(coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], params,
                                level_off, level_res, level_entries, level_dense, m, n_feat,
                                weights, widths, nl, relu_out, h0, h1);
     }
