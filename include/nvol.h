@@ -226,6 +226,50 @@ int nvol_adam_flat_dev(float *p, float *g, float *m, float *v, int64_t n, const 
                        float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
                        void *stream);
 
+/* ------------------------------------------------------------------ rendering */
+
+/* Workspace bytes nvol_render needs for an image of n_pixels and batch K. */
+int64_t nvol_render_workspace_bytes(int64_t n_pixels, int32_t k_batch);
+
+/* One frame of the ray marcher: camera.py:117-143 pixel rays, render.py:225-243
+ * slab test + compaction, then either the sample-streaming wavefront loop
+ * (architecture 0 = render_wavefront, render.py:383-454: rm_coord ->
+ * batched Phi (eval_mode 0 exact / 1 tcgen05) -> rm_shade -> compaction) or
+ * the in-shader mega-kernel (architecture 1 = render_reference,
+ * render.py:347-380).  [host] cam_params[16] = eye[3], fwd[3], right[3],
+ * up[3] (camera.py:44-56 basis, float64), tan_half, aspect, width, height;
+ * [host] render_params[20] = mode_shadow, use_mc, skip_empty, k_batch, s1,
+ * s2, pexp, termination, ambient, density_scale, n_g, -light[3],
+ * background[3], Dx, Dy, Dz.  TF tables as TransferFunction.tables
+ * (transfer.py:43-47) [host].  mu: device macro-cell majorants (gz,gy,gx)
+ * (a 1x1x1 dummy without macro-cells).  Field: a dense normalised grid
+ * (use_grid) or the hash-grid model (tables [host], params/weights device).
+ * img: device (H*W*3) float32.  stats_out [host]: {field evaluations,
+ * iterations}; alive_hist [host]: rays alive per iteration (up to max_hist). */
+int nvol_render(const double *cam_params, const double *render_params, const float *tf_cv,
+                const float *tf_crgb, int32_t ncv, const float *tf_ov, const float *tf_oa,
+                int32_t nov, const float *mu, int64_t gx, int64_t gy, int64_t gz, int32_t use_grid,
+                const float *norm, int64_t ndx, int64_t ndy, int64_t ndz, const float *params,
+                const int64_t *level_off, const int64_t *level_res, const int64_t *level_entries,
+                const uint8_t *level_dense, int32_t n_levels, int32_t n_feat, const float *weights,
+                const int32_t *widths, int32_t n_layers, int32_t relu_out, int32_t architecture,
+                int32_t eval_mode, void *mlp_image, float *img, void *workspace,
+                int64_t workspace_bytes, int64_t *stats_out, int32_t *alive_hist, int32_t max_hist,
+                void *stream);
+
+/* macrocell.py:63-76 _ranges_from_array: bordered per-cell min/max of a
+ * (dz,dy,dx) float32 array (clip != 0: values clipped to [0,1] first, as
+ * macrocell_from_model does). */
+int nvol_macrocell_ranges(const float *vals, int64_t dx, int64_t dy, int64_t dz, int64_t ng,
+                          int32_t clip, float *lo, float *hi, void *stream);
+
+/* macrocell.py:136-156 macrocell_set_tf: mu = max TF opacity over [lo,hi]
+ * (np.interp semantics, float64) * density_scale; untouched cells -> 0.
+ * op_v / op_a [host]: opacity control points. */
+int nvol_macrocell_set_tf(const float *lo, const float *hi, int64_t ncell, const double *op_v,
+                          const double *op_a, int32_t nop, double density_scale, float *mu,
+                          void *stream);
+
 #ifdef __cplusplus
 }
 #endif

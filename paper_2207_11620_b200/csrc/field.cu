@@ -7,113 +7,10 @@
 // evaluator.  Weights are staged once per CTA in shared memory, transposed
 // (k-major) so the inner j loop reads a broadcast float4.
 #include "common.cuh"
+#include "field_exact.cuh"
 
 namespace nvol {
 
-struct MlpShape {
-    int32_t n_layers;
-    int32_t widths[12];
-    int32_t relu_out;
-};
-
-constexpr int FE_THREADS = 128;
-
-// Encode one sample into feat[k * FE_THREADS] (column of this thread).
-__device__ __forceinline__ void encode_exact(float x, float y, float z, const float *__restrict__ params,
-                                             const GridTables &tab, float *feat) {
-    const int m = tab.n_levels, n = tab.n_feat;
-    for (int l = 0; l < m; ++l) {
-        const int32_t res = tab.res[l];
-        Cell<float> c = cell_of<float>(x, y, z, res);
-        float acc[8];
-#pragma unroll
-        for (int f = 0; f < 8; ++f) acc[f] = 0.0f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            int64_t slot = vertex_slot(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), res,
-                                       tab.entries[l], tab.dense[l] != 0);
-            float w = corner_weight<float>(c, k);
-            const float *p = params + tab.offset[l] + slot * n;
-            for (int f = 0; f < n; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(p + f)));
-        }
-        for (int f = 0; f < n; ++f) feat[(l * n + f) * FE_THREADS] = acc[f];
-    }
-}
-
-// Hidden width NN known at compile time: activations live in registers.
-template <int NN>
-__device__ __forceinline__ float mlp_exact_reg(const float *feat, int nin, const float *__restrict__ wt,
-                                               const MlpShape &sh) {
-    float h[NN];
-    // layer 0: nin -> NN, wt holds W0^T (nin x NN)
-    {
-        float acc[NN];
-#pragma unroll
-        for (int j = 0; j < NN; ++j) acc[j] = 0.0f;
-        for (int k = 0; k < nin; ++k) {
-            float hk = feat[k * FE_THREADS];
-            const float4 *wr = reinterpret_cast<const float4 *>(wt + k * NN);
-#pragma unroll
-            for (int j4 = 0; j4 < NN / 4; ++j4) {
-                float4 w = wr[j4];
-                acc[4 * j4 + 0] = xadd(acc[4 * j4 + 0], xmul(w.x, hk));
-                acc[4 * j4 + 1] = xadd(acc[4 * j4 + 1], xmul(w.y, hk));
-                acc[4 * j4 + 2] = xadd(acc[4 * j4 + 2], xmul(w.z, hk));
-                acc[4 * j4 + 3] = xadd(acc[4 * j4 + 3], xmul(w.w, hk));
-            }
-        }
-        const bool relu = sh.n_layers > 1 || sh.relu_out;
-#pragma unroll
-        for (int j = 0; j < NN; ++j) h[j] = relu ? fmaxf(acc[j], 0.0f) : acc[j];
-        wt += nin * NN;
-    }
-    const int nl = sh.n_layers;
-    for (int li = 1; li < nl - 1; ++li) {
-        float acc[NN];
-#pragma unroll
-        for (int j = 0; j < NN; ++j) acc[j] = 0.0f;
-#pragma unroll
-        for (int k = 0; k < NN; ++k) {
-            const float4 *wr = reinterpret_cast<const float4 *>(wt + k * NN);
-#pragma unroll
-            for (int j4 = 0; j4 < NN / 4; ++j4) {
-                float4 w = wr[j4];
-                acc[4 * j4 + 0] = xadd(acc[4 * j4 + 0], xmul(w.x, h[k]));
-                acc[4 * j4 + 1] = xadd(acc[4 * j4 + 1], xmul(w.y, h[k]));
-                acc[4 * j4 + 2] = xadd(acc[4 * j4 + 2], xmul(w.z, h[k]));
-                acc[4 * j4 + 3] = xadd(acc[4 * j4 + 3], xmul(w.w, h[k]));
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < NN; ++j) h[j] = fmaxf(acc[j], 0.0f);
-        wt += NN * NN;
-    }
-    if (nl == 1) return h[0];
-    // output layer NN -> 1
-    float o = 0.0f;
-#pragma unroll
-    for (int k = 0; k < NN; ++k) o = xadd(o, xmul(wt[k], h[k]));
-    return sh.relu_out ? fmaxf(o, 0.0f) : o;
-}
-
-// Generic widths: activations ping-pong through this thread's smem columns.
-__device__ float mlp_exact_smem(float *h0, float *h1, const float *__restrict__ wt, const MlpShape &sh) {
-    float *cur = h0, *nxt = h1;
-    for (int li = 0; li < sh.n_layers; ++li) {
-        int win = sh.widths[li], wout = sh.widths[li + 1];
-        bool relu = li < sh.n_layers - 1 || sh.relu_out;
-        for (int j = 0; j < wout; ++j) {
-            float acc = 0.0f;
-            for (int k = 0; k < win; ++k) acc = xadd(acc, xmul(wt[k * wout + j], cur[k * FE_THREADS]));
-            nxt[j * FE_THREADS] = relu ? fmaxf(acc, 0.0f) : acc;
-        }
-        wt += win * wout;
-        float *t = cur;
-        cur = nxt;
-        nxt = t;
-    }
-    return cur[0];
-}
 
 // mode: 0 = explicit coords, 1 = decode brick (voxel centres of rows [z0, z0+nz)).
 template <int NN>
@@ -149,9 +46,15 @@ __global__ void __launch_bounds__(FE_THREADS) field_exact_kernel(
         float x, y, z;
         if (decode) {
             int64_t ix = i % dx, iy = (i / dx) % dy, iz = z0 + i / (dx * dy);
-            x = xdiv(xadd((float)ix, 0.5f), (float)dx);
-            y = xdiv(xadd((float)iy, 0.5f), (float)dy);
-            z = xdiv(xadd((float)iz, 0.5f), (float)dz);
+            if (decode == 2) {  // macrocell.py:90-94: centres in float64, then cast
+                x = (float)(((double)ix + 0.5) / (double)dx);
+                y = (float)(((double)iy + 0.5) / (double)dy);
+                z = (float)(((double)iz + 0.5) / (double)dz);
+            } else {            // trainer.py:86-92: float32 arithmetic
+                x = xdiv(xadd((float)ix, 0.5f), (float)dx);
+                y = xdiv(xadd((float)iy, 0.5f), (float)dy);
+                z = xdiv(xadd((float)iz, 0.5f), (float)dz);
+            }
         } else {
             x = coords[3 * i];
             y = coords[3 * i + 1];
@@ -165,7 +68,7 @@ __global__ void __launch_bounds__(FE_THREADS) field_exact_kernel(
         } else {
             v = mlp_exact_smem(col0, col1, wt, sh);
         }
-        if (decode)
+        if (decode == 1)
             out[i] = (float)__dadd_rn(__dmul_rn((double)v, scale), lo);
         else
             out[i] = v;
@@ -254,8 +157,10 @@ int nvol_decode(const float *params, const int64_t *level_off, const int64_t *le
     double scale = hi - lo;
     if (mode == 1) return nvol_decode_tc(params, tab, weights, widths, n_layers, relu_out, dx, dy, dz, z0, nz, lo,
                                          scale, out, mlp_image, as_stream(stream));
-    return field_exact_launch(nullptr, dx * dy * nz, params, tab, weights, widths, n_layers, relu_out, 1, dx, dy,
-                              dz, z0, lo, scale, out, as_stream(stream));
+    // mode 0: trainer.decode semantics (float32 centres, denormalised);
+    // mode 2: macrocell_from_model semantics (float64 centres, raw Phi)
+    return field_exact_launch(nullptr, dx * dy * nz, params, tab, weights, widths, n_layers, relu_out,
+                              mode == 2 ? 2 : 1, dx, dy, dz, z0, lo, scale, out, as_stream(stream));
 }
 
 }  // extern "C"

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
 }
 
 int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const uint32_t *o_w, uint32_t o_wout,
-                   uint8_t *image, cudaStream_t s);
+                   uint8_t *image, cudaStream_t s, const uint32_t *o_wlo);
 
 int infer_tc_launch(const float *coords, int64_t b, const float *params, const GridTables &tab, const float *wflat,
                     uint8_t *wimg, int nn, int nh, int relu_out, int decode, int64_t dx, int64_t dy, int64_t dz,
@@ -197,7 +197,7 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
         return NVOL_EINVAL;
     }
     NVOL_REQUIRE(wimg, "tcgen05 inference needs an mlp_image scratch buffer (nvol_mlp_image_bytes)");
-    int st = pack_mlp_image(wflat, sh.nin, sh.ninp, nn, nh, sh.o_w, sh.o_wout, wimg, s);
+    int st = pack_mlp_image(wflat, sh.nin, sh.ninp, nn, nh, sh.o_w, sh.o_wout, wimg, s, nullptr);
     if (st) return st;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -1,0 +1,814 @@
+// Ray-marched volume rendering with macro-cell empty-space skipping (sm_100a).
+//
+// Reference: render.py:201-454 (scene setup, render_reference,
+// render_wavefront), _render_kernels.py:52-563 (slab test, macro-cell DDA,
+// adaptive step, the ray-march state machine, TF lookup, opacity
+// correction, compositing, shadow phase), camera.py:117-143 (pixel rays),
+// macrocell.py:63-156 (bordered ranges, exact majorants).
+//
+// Two schedules, as in the reference:
+//  * in-shader (render_reference / rm_reference): one thread per ray runs its
+//    state machine to completion and evaluates Phi inline (exact evaluator);
+//  * sample streaming (render_wavefront): per iteration, rm_coord stages up to
+//    K samples per alive ray, one batched Phi evaluation runs over all staged
+//    samples (exact or tcgen05), rm_shade composites and retires rays, and a
+//    stable CUB compaction keeps the alive rays contiguous.
+// Geometry (DDA, clocks, coordinates) is float64/float32 with the reference's
+// operation order and no FMA contraction (file compiled with -fmad=false).
+// pow is evaluated in float64 and rounded, which matches the reference's
+// glibc powf in all but ~0.1% of inputs (1 ulp); images agree to float
+// rounding, not bitwise.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "field_exact.cuh"
+
+namespace nvol {
+
+constexpr int MAX_TF = 16;
+
+struct TfTables {
+    int ncv, nov;
+    float cv[MAX_TF], crgb[3 * MAX_TF], ov[MAX_TF], oa[MAX_TF];
+};
+
+struct RmScene {
+    int mode_shadow, use_mc, skip_empty, k_batch;
+    float s1, s2, pexp, term, ka, ds;
+    int64_t gx, gy, gz;
+    double ng;
+    float sd[3], bg[3];
+    double hx, hy, hz;
+    TfTables tf;
+};
+
+struct RayState {
+    float T, r, g, b, clock, sbar, best_w, best_t, Tsh, o[3], d[3], muc;
+    double cell_exit, march_end, tm[3], td[3];
+    int32_t pixel, phase, in_cell, pad0;
+    int64_t c[3], st[3];
+};
+
+__device__ __forceinline__ float powd(float x, float y) { return (float)pow((double)x, (double)y); }
+
+__device__ __forceinline__ int64_t clampl(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// _render_kernels.py:244-253
+__device__ __forceinline__ float adaptive(float muc, float s1, float s2, float pexp) {
+    float m = muc > 1.0f ? 1.0f : muc;
+    float gap = 1.0f - m;
+    float s = s1 + (s2 - s1) * powd(gap, pexp);
+    return s < s1 ? s1 : s;
+}
+
+__device__ __forceinline__ float mu_read(const RmScene &S, const float *__restrict__ mu, int64_t cx, int64_t cy,
+                                         int64_t cz) {
+    int64_t ix = clampl(cx, 0, S.gx - 1), iy = clampl(cy, 0, S.gy - 1), iz = clampl(cz, 0, S.gz - 1);
+    return __ldg(mu + (iz * S.gy + iy) * S.gx + ix);
+}
+
+// _render_kernels.py:92-138 _dda_enter + 268-305 _rm_cell_entry
+__device__ void cell_entry(const RmScene &S, const float *__restrict__ mu, RayState &R) {
+    const double t1 = R.march_end;
+    if (!S.use_mc) {
+        R.cell_exit = t1;
+        R.sbar = S.s1;
+        R.muc = 1.0f;
+        R.in_cell = 1;
+        return;
+    }
+    const double t0 = (double)R.clock, ng = S.ng;
+    const int64_t gd[3] = {S.gx, S.gy, S.gz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double o = (double)R.o[a], d = (double)R.d[a];
+        double p = o + t0 * d;
+        int64_t c = clampl((int64_t)floor(p / ng), 0, gd[a] - 1);
+        R.c[a] = c;
+        if (d > 0.0) {
+            R.st[a] = 1;
+            R.tm[a] = t0 + ((double)(c + 1) * ng - p) / d;
+            R.td[a] = ng / d;
+        } else if (d < 0.0) {
+            R.st[a] = -1;
+            R.tm[a] = t0 + ((double)c * ng - p) / d;
+            R.td[a] = -ng / d;
+        } else {
+            R.st[a] = 0;
+            R.tm[a] = INFINITY;
+            R.td[a] = INFINITY;
+        }
+    }
+    double se = R.tm[0];
+    if (R.tm[1] < se) se = R.tm[1];
+    if (R.tm[2] < se) se = R.tm[2];
+    if (se > t1) se = t1;
+    R.cell_exit = se;
+    R.muc = mu_read(S, mu, R.c[0], R.c[1], R.c[2]);
+    R.sbar = adaptive(R.muc, S.s1, S.s2, S.pexp);
+    R.in_cell = 1;
+}
+
+// _render_kernels.py:308-333
+__device__ void cell_advance(const RmScene &S, const float *__restrict__ mu, RayState &R) {
+    const double t1 = R.march_end;
+    if (R.tm[0] <= R.tm[1] && R.tm[0] <= R.tm[2]) {
+        R.c[0] += R.st[0];
+        R.tm[0] = R.tm[0] + R.td[0];
+    } else if (R.tm[1] <= R.tm[2]) {
+        R.c[1] += R.st[1];
+        R.tm[1] = R.tm[1] + R.td[1];
+    } else {
+        R.c[2] += R.st[2];
+        R.tm[2] = R.tm[2] + R.td[2];
+    }
+    double se = R.tm[0];
+    if (R.tm[1] < se) se = R.tm[1];
+    if (R.tm[2] < se) se = R.tm[2];
+    if (se > t1) se = t1;
+    R.cell_exit = se;
+    R.muc = mu_read(S, mu, R.c[0], R.c[1], R.c[2]);
+    R.sbar = adaptive(R.muc, S.s1, S.s2, S.pexp);
+}
+
+// _render_kernels.py:336-361 _rm_next (returns the sample t or -1 at march end)
+__device__ float rm_next(const RmScene &S, const float *__restrict__ mu, RayState &R) {
+    const double t1 = R.march_end;
+    if (R.in_cell == 0) cell_entry(S, mu, R);
+    for (;;) {
+        const float sbar = R.sbar;
+        const double se = R.cell_exit;
+        if (S.use_mc && S.skip_empty && R.muc <= 0.0f) {
+            float t = R.clock;
+            while ((double)(t + 0.5f * sbar) < se) t = t + sbar;
+            R.clock = t;
+        } else {
+            float ts = R.clock + 0.5f * sbar;
+            if ((double)ts < se) {
+                R.clock = R.clock + sbar;
+                return ts;
+            }
+        }
+        if (se >= t1) return -1.0f;
+        cell_advance(S, mu, R);
+    }
+}
+
+__device__ float tf_alpha(const TfTables &T, float v) {
+    float x = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
+    int n = T.nov;
+    if (x <= T.ov[0]) return T.oa[0];
+    if (x >= T.ov[n - 1]) return T.oa[n - 1];
+    int i = 1;
+    while (T.ov[i] < x) ++i;
+    float w = (x - T.ov[i - 1]) / (T.ov[i] - T.ov[i - 1]);
+    return T.oa[i - 1] + w * (T.oa[i] - T.oa[i - 1]);
+}
+
+__device__ void tf_rgb(const TfTables &T, float v, float &r, float &g, float &b) {
+    float x = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
+    int n = T.ncv;
+    const float *c = T.crgb;
+    if (x <= T.cv[0]) {
+        r = c[0], g = c[1], b = c[2];
+        return;
+    }
+    if (x >= T.cv[n - 1]) {
+        r = c[3 * (n - 1)], g = c[3 * (n - 1) + 1], b = c[3 * (n - 1) + 2];
+        return;
+    }
+    int i = 1;
+    while (T.cv[i] < x) ++i;
+    float w = (x - T.cv[i - 1]) / (T.cv[i] - T.cv[i - 1]);
+    r = c[3 * (i - 1)] + w * (c[3 * i] - c[3 * (i - 1)]);
+    g = c[3 * (i - 1) + 1] + w * (c[3 * i + 1] - c[3 * (i - 1) + 1]);
+    b = c[3 * (i - 1) + 2] + w * (c[3 * i + 2] - c[3 * (i - 1) + 2]);
+}
+
+// _render_kernels.py:364-392 (true when the current march just ended)
+__device__ bool rm_consume(const RmScene &S, RayState &R, float v, float ts, float sbar) {
+    float a = tf_alpha(S.tf, v) * S.ds;
+    if (a < 0.0f) a = 0.0f;
+    if (a > 1.0f) a = 1.0f;
+    float abar = 1.0f - powd(1.0f - a, sbar / S.s1);
+    if (R.phase == 0) {
+        float T = R.T;
+        float w = T * abar;
+        if (S.mode_shadow && w > R.best_w) {
+            R.best_w = w;
+            R.best_t = ts;
+        }
+        float cr, cg, cb;
+        tf_rgb(S.tf, v, cr, cg, cb);
+        R.r += w * cr;
+        R.g += w * cg;
+        R.b += w * cb;
+        T = T * (1.0f - abar);
+        R.T = T;
+        return T < S.term;
+    }
+    float Tsh = R.Tsh * (1.0f - abar);
+    R.Tsh = Tsh;
+    return Tsh < S.term;
+}
+
+// _render_kernels.py:54-89
+__device__ bool isect(double ox, double oy, double oz, double dx, double dy, double dz, double hx, double hy,
+                      double hz, double &t0o, double &t1o) {
+    double t0 = -INFINITY, t1 = INFINITY;
+    const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz}, h[3] = {hx, hy, hz};
+    for (int a = 0; a < 3; ++a) {
+        if (d[a] != 0.0) {
+            double ta = (0.0 - o[a]) / d[a], tb = (h[a] - o[a]) / d[a];
+            if (ta > tb) {
+                double t = ta;
+                ta = tb;
+                tb = t;
+            }
+            t0 = t0 > ta ? t0 : ta;
+            t1 = t1 < tb ? t1 : tb;
+        } else if (o[a] < 0.0 || o[a] > h[a]) {
+            return false;
+        }
+    }
+    t0 = t0 > 0.0 ? t0 : 0.0;
+    if (t1 <= t0) return false;
+    t0o = t0;
+    t1o = t1;
+    return true;
+}
+
+// _render_kernels.py:395-420 (true = ray done)
+__device__ bool rm_phase_end(const RmScene &S, RayState &R) {
+    if (!S.mode_shadow || R.phase != 0) return true;
+    R.phase = 1;
+    if (R.r == 0.0f && R.g == 0.0f && R.b == 0.0f) return true;
+    double bt = (double)R.best_t;
+    double bx = (double)R.o[0] + bt * (double)R.d[0];
+    double by = (double)R.o[1] + bt * (double)R.d[1];
+    double bz = (double)R.o[2] + bt * (double)R.d[2];
+    double t0s, t1s;
+    if (!isect(bx, by, bz, (double)S.sd[0], (double)S.sd[1], (double)S.sd[2], S.hx, S.hy, S.hz, t0s, t1s)) return true;
+    R.o[0] = (float)bx;
+    R.o[1] = (float)by;
+    R.o[2] = (float)bz;
+    R.d[0] = S.sd[0];
+    R.d[1] = S.sd[1];
+    R.d[2] = S.sd[2];
+    R.clock = (float)t0s;
+    R.march_end = t1s;
+    R.in_cell = 0;
+    return false;
+}
+
+// _render_kernels.py:423-432
+__device__ void rm_final(const RmScene &S, const RayState &R, float *__restrict__ img) {
+    float scale = 1.0f;
+    if (S.mode_shadow) scale = S.ka + (1.0f - S.ka) * R.Tsh;
+    float T = R.T;
+    int64_t p = R.pixel;
+    img[3 * p] = R.r * scale + T * S.bg[0];
+    img[3 * p + 1] = R.g * scale + T * S.bg[1];
+    img[3 * p + 2] = R.b * scale + T * S.bg[2];
+}
+
+// _render_kernels.py:435-452
+__device__ void coord_at(const RmScene &S, const RayState &R, float ts, float &x, float &y, float &z) {
+    const float one_below = 0.99999994f;
+    const double h[3] = {S.hx, S.hy, S.hz};
+    float c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float v = (float)(((double)R.o[a] + (double)ts * (double)R.d[a]) / h[a]);
+        if (v < 0.0f) v = 0.0f;
+        if (v >= 1.0f) v = one_below;
+        c[a] = v;
+    }
+    x = c[0];
+    y = c[1];
+    z = c[2];
+}
+
+// ----------------------------------------------------------------------------- ray generation
+struct CamParams {
+    float eye[3];
+    double fwd[3], right[3], up[3];
+    double tan_half, aspect;
+    int64_t width, height;
+};
+
+// camera.py:117-143 (float64, cast to float32) + render.py:225-243 slab test
+__global__ void raygen_kernel(const CamParams cam, const RmScene S, RayState *__restrict__ rays,
+                              uint8_t *__restrict__ hit, float *__restrict__ img) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = cam.width * cam.height;
+    if (p >= n) return;
+    img[3 * p] = S.bg[0];
+    img[3 * p + 1] = S.bg[1];
+    img[3 * p + 2] = S.bg[2];
+    double ii = (double)(p % cam.width), jj = floor((double)p / (double)cam.width);
+    double nx = ((ii + 0.5) / (double)cam.width * 2.0 - 1.0) * (cam.tan_half * cam.aspect);
+    double ny = (1.0 - (jj + 0.5) / (double)cam.height * 2.0) * cam.tan_half;
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) d[a] = cam.fwd[a] + nx * cam.right[a] + ny * cam.up[a];
+    double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    RayState R;
+    memset(&R, 0, sizeof(R));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        R.d[a] = (float)(d[a] / nrm);
+        R.o[a] = cam.eye[a];
+    }
+    // vectorised slab test of render.py:225-243 on the float32 ray, in float64
+    const double h[3] = {S.hx, S.hy, S.hz};
+    double lo = -INFINITY, up = INFINITY;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double o = (double)R.o[a], dd = (double)R.d[a];
+        double l, u;
+        if (dd == 0.0) {
+            bool inside = (o >= 0.0) && (o <= h[a]);
+            l = inside ? -INFINITY : INFINITY;
+            u = inside ? INFINITY : -INFINITY;
+        } else {
+            double ta = (0.0 - o) / dd, tb = (h[a] - o) / dd;
+            l = fmin(ta, tb);
+            u = fmax(ta, tb);
+        }
+        lo = fmax(lo, l);
+        up = fmin(up, u);
+    }
+    double t0 = fmax(lo, 0.0), t1 = up;
+    bool h_ = t1 > t0;
+    hit[p] = h_ ? 1 : 0;
+    R.T = 1.0f;
+    R.clock = (float)t0;
+    R.Tsh = 1.0f;
+    R.march_end = t1;
+    R.pixel = (int32_t)p;
+    rays[p] = R;
+}
+
+// ----------------------------------------------------------------------------- field for the in-shader marcher
+struct FieldDesc {
+    int use_grid;
+    const float *norm;
+    int64_t ndx, ndy, ndz;
+    const float *params;
+    const float *weights;
+};
+
+// render_reference / rm_reference (_render_kernels.py:455-488): one thread per
+// ray to completion, Phi inline (exact evaluator, shared-memory feature column).
+template <int NN>
+__global__ void __launch_bounds__(FE_THREADS) rm_mega_kernel(RayState *__restrict__ rays, int64_t n, const RmScene S,
+                                                             const float *__restrict__ mu, const FieldDesc F,
+                                                             const GridTables tab, const MlpShape sh, int maxw,
+                                                             float *__restrict__ img,
+                                                             unsigned long long *__restrict__ evals) {
+    extern __shared__ float4 smem4[];
+    float *smem = reinterpret_cast<float *>(smem4);
+    float *wt = smem;
+    int wsz = F.use_grid ? 0 : stage_weights_t(F.weights, sh, wt);
+    float *h0 = wt + wsz, *h1 = h0 + maxw * FE_THREADS;
+    __syncthreads();
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    RayState R = rays[r];
+    unsigned long long ev = 0;
+    float *col0 = h0 + threadIdx.x, *col1 = h1 + threadIdx.x;
+    for (;;) {
+        float ts = rm_next(S, mu, R);
+        if (ts < 0.0f) {
+            if (rm_phase_end(S, R)) {
+                rm_final(S, R, img);
+                break;
+            }
+            continue;
+        }
+        float x, y, z;
+        coord_at(S, R, ts, x, y, z);
+        float v;
+        if (F.use_grid) {
+            v = trilinear_at(F.norm, F.ndx, F.ndy, F.ndz, x, y, z);
+        } else {
+            encode_exact(x, y, z, F.params, tab, col0);
+            if constexpr (NN > 0)
+                v = mlp_exact_reg<NN>(col0, tab.n_levels * tab.n_feat, wt, sh);
+            else
+                v = mlp_exact_smem(col0, col1, wt, sh);
+        }
+        ++ev;
+        if (rm_consume(S, R, v, ts, R.sbar)) {
+            if (rm_phase_end(S, R)) {
+                rm_final(S, R, img);
+                break;
+            }
+        }
+    }
+    atomicAdd(evals, ev);
+}
+
+// ----------------------------------------------------------------------------- wavefront stages
+// _render_kernels.py:491-515 rm_coord
+__global__ void rm_coord_kernel(RayState *__restrict__ rays, int64_t n, const RmScene S, const float *__restrict__ mu,
+                                float *__restrict__ sxyz, float *__restrict__ sts, float *__restrict__ ssbar,
+                                int32_t *__restrict__ counts, uint8_t *__restrict__ mdone,
+                                unsigned long long *__restrict__ evals) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    RayState R = rays[r];
+    const int K = S.k_batch;
+    int c = 0;
+    uint8_t done = 0;
+    while (c < K) {
+        float ts = rm_next(S, mu, R);
+        if (ts < 0.0f) {
+            done = 1;
+            break;
+        }
+        float x, y, z;
+        coord_at(S, R, ts, x, y, z);
+        int64_t i = r * K + c;
+        sxyz[3 * i] = x;
+        sxyz[3 * i + 1] = y;
+        sxyz[3 * i + 2] = z;
+        sts[i] = ts;
+        ssbar[i] = R.sbar;
+        ++c;
+    }
+    for (int q = c; q < K; ++q) {  // holes: a valid coordinate the batched evaluator may read
+        int64_t i = r * K + q;
+        sxyz[3 * i] = sxyz[3 * i + 1] = sxyz[3 * i + 2] = 0.0f;
+    }
+    counts[r] = c;
+    mdone[r] = done;
+    rays[r] = R;
+    // phi_eval_staged evaluates exactly the staged samples (_render_kernels.py:518-540)
+    unsigned long long tot = (unsigned long long)c;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(__activemask(), tot, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(evals, tot);
+}
+
+// _render_kernels.py:543-563 rm_shade
+__global__ void rm_shade_kernel(RayState *__restrict__ rays, int64_t n, const RmScene S,
+                                const float *__restrict__ values, const float *__restrict__ sts,
+                                const float *__restrict__ ssbar, const int32_t *__restrict__ counts,
+                                const uint8_t *__restrict__ mdone, float *__restrict__ img,
+                                uint8_t *__restrict__ alive) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    RayState R = rays[r];
+    const int K = S.k_batch;
+    bool ended = false;
+    for (int c = 0; c < counts[r]; ++c) {
+        int64_t i = r * K + c;
+        if (rm_consume(S, R, values[i], sts[i], ssbar[i])) {
+            ended = true;
+            break;
+        }
+    }
+    if (!ended && mdone[r]) ended = true;
+    bool al = true;
+    if (ended && rm_phase_end(S, R)) {
+        rm_final(S, R, img);
+        al = false;
+    }
+    alive[r] = al ? 1 : 0;
+    rays[r] = R;
+}
+
+// ----------------------------------------------------------------------------- macro-cells
+// macrocell.py:63-76: per cell min/max over its voxels plus a one-voxel border
+// (optionally clipping the values to [0,1] first, macrocell.py:97).
+__global__ void mc_ranges_kernel(const float *__restrict__ vals, int64_t dx, int64_t dy, int64_t dz, int64_t ng,
+                                 int64_t gx, int64_t gy, int64_t gz, int clip, float *__restrict__ lo,
+                                 float *__restrict__ hi) {
+    int64_t cell = blockIdx.x;
+    if (cell >= gx * gy * gz) return;
+    int64_t cx = cell % gx, cy = (cell / gx) % gy, cz = cell / (gx * gy);
+    int64_t x0 = max(cx * ng - 1, (int64_t)0), x1 = min((cx + 1) * ng + 1, dx);
+    int64_t y0 = max(cy * ng - 1, (int64_t)0), y1 = min((cy + 1) * ng + 1, dy);
+    int64_t z0 = max(cz * ng - 1, (int64_t)0), z1 = min((cz + 1) * ng + 1, dz);
+    int64_t nxv = x1 - x0, nyv = y1 - y0, nzv = z1 - z0, tot = nxv * nyv * nzv;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int64_t q = threadIdx.x; q < tot; q += blockDim.x) {
+        int64_t x = x0 + q % nxv, y = y0 + (q / nxv) % nyv, z = z0 + q / (nxv * nyv);
+        float v = vals[(z * dy + y) * dx + x];
+        if (clip) v = fminf(fmaxf(v, 0.0f), 1.0f);
+        mn = fminf(mn, v);
+        mx = fmaxf(mx, v);
+    }
+    __shared__ float smn[32], smx[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        smn[threadIdx.x >> 5] = mn;
+        smx[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            mn = fminf(mn, smn[w]);
+            mx = fmaxf(mx, smx[w]);
+        }
+        if (tot > 0) {
+            lo[cell] = mn;
+            hi[cell] = mx;
+        }
+    }
+}
+
+// numpy.interp (the reference's np.interp in macrocell.py:148-149), float64
+__device__ double interp_np(double x, const double *xp, const double *fp, int n) {
+    if (x < xp[0]) return fp[0];
+    if (x > xp[n - 1]) return fp[n - 1];
+    if (x == xp[n - 1]) return fp[n - 1];
+    int j = 0;
+    while (j < n - 2 && xp[j + 1] <= x) ++j;
+    if (x == xp[j]) return fp[j];
+    double slope = (fp[j + 1] - fp[j]) / (xp[j + 1] - xp[j]);
+    double r = slope * (x - xp[j]) + fp[j];
+    if (isnan(r)) r = slope * (x - xp[j + 1]) + fp[j + 1];
+    return r;
+}
+
+struct OpacityPts {
+    int n;
+    double v[MAX_TF], a[MAX_TF];
+};
+
+// macrocell.py:136-156 macrocell_set_tf: exact max opacity over [lo, hi]
+__global__ void mc_set_tf_kernel(const float *__restrict__ lo_a, const float *__restrict__ hi_a, int64_t ncell,
+                                 const OpacityPts P, double density_scale, float *__restrict__ mu) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ncell) return;
+    float lf = lo_a[i], hf = hi_a[i];
+    bool touched = lf <= hf;
+    double lo = fmin(fmax((double)lf, 0.0), 1.0), hi = fmin(fmax((double)hf, 0.0), 1.0);
+    double best = fmax(interp_np(lo, P.v, P.a, P.n), interp_np(hi, P.v, P.a, P.n));
+    for (int q = 0; q < P.n; ++q)
+        if (P.v[q] > lo && P.v[q] < hi) best = fmax(best, P.a[q]);
+    mu[i] = touched ? (float)(best * density_scale) : 0.0f;
+}
+
+// ----------------------------------------------------------------------------- host helpers
+static int fill_scene(RmScene &S, const double *rp, const float *tf_cv, const float *tf_crgb, int ncv,
+                      const float *tf_ov, const float *tf_oa, int nov, int64_t gx, int64_t gy, int64_t gz) {
+    NVOL_REQUIRE(ncv >= 1 && ncv <= MAX_TF && nov >= 1 && nov <= MAX_TF, "transfer function has too many points");
+    // rp: mode_shadow, use_mc, skip_empty, k_batch, s1, s2, pexp, term, ka, ds, ng,
+    //     sd[3], bg[3], hx, hy, hz
+    S.mode_shadow = (int)rp[0];
+    S.use_mc = (int)rp[1];
+    S.skip_empty = (int)rp[2];
+    S.k_batch = (int)rp[3];
+    S.s1 = (float)rp[4];
+    S.s2 = (float)rp[5];
+    S.pexp = (float)rp[6];
+    S.term = (float)rp[7];
+    S.ka = (float)rp[8];
+    S.ds = (float)rp[9];
+    S.ng = rp[10];
+    for (int a = 0; a < 3; ++a) {
+        S.sd[a] = (float)rp[11 + a];
+        S.bg[a] = (float)rp[14 + a];
+    }
+    S.hx = rp[17];
+    S.hy = rp[18];
+    S.hz = rp[19];
+    S.gx = gx;
+    S.gy = gy;
+    S.gz = gz;
+    S.tf.ncv = ncv;
+    S.tf.nov = nov;
+    for (int i = 0; i < ncv; ++i) {
+        S.tf.cv[i] = tf_cv[i];
+        for (int c = 0; c < 3; ++c) S.tf.crgb[3 * i + c] = tf_crgb[3 * i + c];
+    }
+    for (int i = 0; i < nov; ++i) {
+        S.tf.ov[i] = tf_ov[i];
+        S.tf.oa[i] = tf_oa[i];
+    }
+    return NVOL_OK;
+}
+
+static void fill_cam(CamParams &C, const double *cp) {
+    // cp: eye[3], fwd[3], right[3], up[3], tan_half, aspect, width, height
+    for (int a = 0; a < 3; ++a) {
+        C.eye[a] = (float)cp[a];
+        C.fwd[a] = cp[3 + a];
+        C.right[a] = cp[6 + a];
+        C.up[a] = cp[9 + a];
+    }
+    C.tan_half = cp[12];
+    C.aspect = cp[13];
+    C.width = (int64_t)cp[14];
+    C.height = (int64_t)cp[15];
+}
+
+struct RenderWs {
+    RayState *rays[2];
+    uint8_t *flags;
+    float *sxyz, *sts, *ssbar, *values;
+    int32_t *counts;
+    uint8_t *mdone;
+    unsigned long long *evals;
+    int64_t *nsel;
+    void *cub_tmp;
+    size_t cub_bytes;
+    int64_t total;
+};
+
+static int64_t al256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+static RenderWs carve(void *base, int64_t npix, int k) {
+    RenderWs w{};
+    char *p = (char *)base;
+    int64_t off = 0;
+    auto take = [&](int64_t bytes) {
+        char *r = p ? p + off : nullptr;
+        off += al256(bytes);
+        return r;
+    };
+    w.rays[0] = (RayState *)take(npix * (int64_t)sizeof(RayState));
+    w.rays[1] = (RayState *)take(npix * (int64_t)sizeof(RayState));
+    w.flags = (uint8_t *)take(npix);
+    w.sxyz = (float *)take(npix * k * 12);
+    w.sts = (float *)take(npix * k * 4);
+    w.ssbar = (float *)take(npix * k * 4);
+    w.values = (float *)take(npix * k * 4);
+    w.counts = (int32_t *)take(npix * 4);
+    w.mdone = (uint8_t *)take(npix);
+    w.evals = (unsigned long long *)take(8);
+    w.nsel = (int64_t *)take(8);
+    size_t cb = 0;
+    cub::DeviceSelect::Flagged(nullptr, cb, (RayState *)nullptr, (uint8_t *)nullptr, (RayState *)nullptr,
+                               (int64_t *)nullptr, (int64_t)npix);
+    w.cub_bytes = cb;
+    w.cub_tmp = take((int64_t)cb);
+    w.total = off;
+    return w;
+}
+
+int field_exact_launch(const float *coords, int64_t b, const float *params, const GridTables &tab,
+                       const float *weights, const int32_t *widths, int32_t n_layers, int32_t relu_out, int decode,
+                       int64_t dx, int64_t dy, int64_t dz, int64_t z0, double lo, double scale, float *out,
+                       cudaStream_t s);
+int infer_tc_launch(const float *coords, int64_t b, const float *params, const GridTables &tab, const float *wflat,
+                    uint8_t *wimg, int nn, int nh, int relu_out, int decode, int64_t dx, int64_t dy, int64_t dz,
+                    int64_t z0, double lo, double scale, float *out, cudaStream_t s);
+
+}  // namespace nvol
+
+using namespace nvol;
+
+extern "C" {
+
+int64_t nvol_render_workspace_bytes(int64_t n_pixels, int32_t k_batch) {
+    return carve(nullptr, n_pixels, k_batch < 1 ? 1 : k_batch).total;
+}
+
+// render.py:383-454 render_wavefront (architecture 0) or render.py:347-380
+// render_reference (architecture 1, in-shader).  See nvol.h.
+int nvol_render(const double *cam_params, const double *render_params, const float *tf_cv, const float *tf_crgb,
+                int32_t ncv, const float *tf_ov, const float *tf_oa, int32_t nov, const float *mu, int64_t gx,
+                int64_t gy, int64_t gz, int32_t use_grid, const float *norm, int64_t ndx, int64_t ndy, int64_t ndz,
+                const float *params, const int64_t *level_off, const int64_t *level_res, const int64_t *level_entries,
+                const uint8_t *level_dense, int32_t n_levels, int32_t n_feat, const float *weights,
+                const int32_t *widths, int32_t n_layers, int32_t relu_out, int32_t architecture, int32_t eval_mode,
+                void *mlp_image, float *img, void *workspace, int64_t workspace_bytes, int64_t *stats_out,
+                int32_t *alive_hist, int32_t max_hist, void *stream) {
+    cudaStream_t s = as_stream(stream);
+    RmScene S;
+    int st = fill_scene(S, render_params, tf_cv, tf_crgb, ncv, tf_ov, tf_oa, nov, gx, gy, gz);
+    if (st) return st;
+    NVOL_REQUIRE(mu && img && workspace && stats_out, "null pointer");
+    CamParams C;
+    fill_cam(C, cam_params);
+    const int64_t npix = C.width * C.height;
+    const int K = S.k_batch < 1 ? 1 : S.k_batch;
+    RenderWs w = carve(workspace, npix, K);
+    NVOL_REQUIRE(workspace_bytes >= w.total, "render workspace too small");
+    GridTables tab{};
+    MlpShape sh{};
+    int maxw = 1;
+    FieldDesc F{use_grid, norm, ndx, ndy, ndz, params, weights};
+    if (!use_grid) {
+        st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
+        if (st) return st;
+        NVOL_REQUIRE(n_layers >= 1 && n_layers <= 11, "MLP depth out of range");
+        sh.n_layers = n_layers;
+        sh.relu_out = relu_out;
+        for (int i = 0; i <= n_layers; ++i) {
+            sh.widths[i] = widths[i];
+            maxw = max(maxw, (int)widths[i]);
+        }
+    } else {
+        NVOL_REQUIRE(norm, "grid field without data");
+    }
+    cudaMemsetAsync(w.evals, 0, 8, s);
+    raygen_kernel<<<grid_for(npix, 256), 256, 0, s>>>(C, S, w.rays[0], w.flags, img);
+    st = check_launch("raygen");
+    if (st) return st;
+    cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, w.rays[0], w.flags, w.rays[1], w.nsel, npix, s);
+    int64_t n = 0;
+    cudaMemcpyAsync(&n, w.nsel, 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    int cur = 1, iters = 0;
+    if (architecture == 1) {
+        // in-shader: one thread per ray to completion
+        if (n > 0) {
+            int wtot = 0;
+            for (int i = 0; i < (use_grid ? 0 : n_layers); ++i) wtot += widths[i] * widths[i + 1];
+            size_t smem = sizeof(float) * (((wtot + 3) & ~3) + 2 * (size_t)maxw * FE_THREADS);
+            int nn = (!use_grid && n_layers >= 2) ? widths[1] : 0;
+            bool uniform = !use_grid && n_layers >= 2;
+            for (int i = 1; i < n_layers && uniform; ++i) uniform &= widths[i] == nn;
+            unsigned grid = grid_for(n, FE_THREADS);
+#define LAUNCH_MK(NNV)                                                                                            \
+    do {                                                                                                          \
+        cudaFuncSetAttribute(rm_mega_kernel<NNV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+        rm_mega_kernel<NNV><<<grid, FE_THREADS, smem, s>>>(w.rays[cur], n, S, mu, F, tab, sh, maxw, img, w.evals); \
+    } while (0)
+            if (uniform && nn == 16)
+                LAUNCH_MK(16);
+            else if (uniform && nn == 32)
+                LAUNCH_MK(32);
+            else if (uniform && nn == 64)
+                LAUNCH_MK(64);
+            else
+                LAUNCH_MK(0);
+#undef LAUNCH_MK
+            st = check_launch("rm_mega_kernel");
+            if (st) return st;
+        }
+        if (max_hist > 0) alive_hist[0] = (int32_t)n;
+        iters = 1;
+    } else {
+        while (n > 0) {
+            if (iters < max_hist) alive_hist[iters] = (int32_t)n;
+            ++iters;
+            RayState *rs = w.rays[cur];
+            rm_coord_kernel<<<grid_for(n, 128), 128, 0, s>>>(rs, n, S, mu, w.sxyz, w.sts, w.ssbar, w.counts, w.mdone,
+                                                              w.evals);
+            st = check_launch("rm_coord");
+            if (st) return st;
+            const int64_t ns = n * K;
+            if (use_grid) {
+                extern int nvol_trilinear(const float *, int64_t, int64_t, int64_t, const float *, int64_t, float *,
+                                          void *);
+                st = nvol_trilinear(norm, ndx, ndy, ndz, w.sxyz, ns, w.values, stream);
+            } else if (eval_mode == 1) {
+                int nnv = widths[1];
+                st = infer_tc_launch(w.sxyz, ns, params, tab, weights, (uint8_t *)mlp_image, nnv, n_layers - 1,
+                                     relu_out, 0, 0, 0, 0, 0, 0.0, 1.0, w.values, s);
+            } else {
+                st = field_exact_launch(w.sxyz, ns, params, tab, weights, widths, n_layers, relu_out, 0, 0, 0, 0, 0,
+                                        0.0, 1.0, w.values, s);
+            }
+            if (st) return st;
+            rm_shade_kernel<<<grid_for(n, 128), 128, 0, s>>>(rs, n, S, w.values, w.sts, w.ssbar, w.counts, w.mdone,
+                                                              img, w.flags);
+            st = check_launch("rm_shade");
+            if (st) return st;
+            cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, rs, w.flags, w.rays[cur ^ 1], w.nsel, n, s);
+            cudaMemcpyAsync(&n, w.nsel, 8, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            cur ^= 1;
+        }
+    }
+    unsigned long long ev = 0;
+    cudaMemcpyAsync(&ev, w.evals, 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    stats_out[0] = (int64_t)ev;
+    stats_out[1] = iters;
+    return check_launch("render");
+}
+
+int nvol_macrocell_ranges(const float *vals, int64_t dx, int64_t dy, int64_t dz, int64_t ng, int32_t clip,
+                          float *lo, float *hi, void *stream) {
+    NVOL_REQUIRE(vals && lo && hi && ng >= 1, "bad arguments");
+    int64_t gx = (dx + ng - 1) / ng, gy = (dy + ng - 1) / ng, gz = (dz + ng - 1) / ng;
+    mc_ranges_kernel<<<(unsigned)(gx * gy * gz), 256, 0, as_stream(stream)>>>(vals, dx, dy, dz, ng, gx, gy, gz, clip,
+                                                                               lo, hi);
+    return check_launch("macrocell_ranges");
+}
+
+int nvol_macrocell_set_tf(const float *lo, const float *hi, int64_t ncell, const double *op_v, const double *op_a,
+                          int32_t nop, double density_scale, float *mu, void *stream) {
+    NVOL_REQUIRE(lo && hi && mu && nop >= 1 && nop <= MAX_TF, "bad arguments");
+    OpacityPts P;
+    P.n = nop;
+    for (int i = 0; i < nop; ++i) {
+        P.v[i] = op_v[i];
+        P.a[i] = op_a[i];
+    }
+    if (ncell == 0) return NVOL_OK;
+    mc_set_tf_kernel<<<grid_for(ncell, 256), 256, 0, as_stream(stream)>>>(lo, hi, ncell, P, density_scale, mu);
+    return check_launch("macrocell_set_tf");
+}
+
+}  // extern "C"

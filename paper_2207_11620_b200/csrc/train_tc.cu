@@ -39,8 +39,9 @@ constexpr uint32_t COARSE_BYTES = 48 * 1024;
 struct TcShape {
     int m, n, nin, ninp, nn, nh;
     int relu_out, loss_kind;
-    uint32_t o_w[MAX_NH], o_wout, o_x, o_h[MAX_NH + 1], o_d[2], o_dout, o_misc, smem_bytes;
-    uint32_t t_f, t_g, t_dw[MAX_NH], t_dwout, t_alloc;
+    uint32_t o_w[MAX_NH], o_wout, o_wlo[MAX_NH], o_x, o_xlo, o_h[MAX_NH + 1], o_hlo[2], o_d[2], o_dout, o_misc,
+        smem_bytes;
+    uint32_t t_f, t_flo, t_g, t_dw[MAX_NH], t_dwout, t_alloc;
     int64_t w_floats;
 };
 
@@ -64,9 +65,13 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
     };
     for (int i = 0; i < nh; ++i) s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
     s.o_wout = take(4u * nn);
-    s.o_x = take(2u * TILE * s.ninp);
+    for (int i = 0; i < nh; ++i) s.o_wlo[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+    s.o_x = take(2u * TILE * s.ninp);      // [o_x, o_x + 2 tiles): hi then lo feature tile
+    s.o_xlo = take(2u * TILE * s.ninp);
     s.o_h[0] = s.o_x;
     for (int i = 1; i <= nh; ++i) s.o_h[i] = take(2u * TILE * nn);
+    s.o_hlo[0] = take(2u * TILE * nn);
+    s.o_hlo[1] = take(2u * TILE * nn);
     s.o_d[0] = take(2u * TILE * nn);
     s.o_d[1] = take(2u * TILE * nn);
     s.o_dout = take(2048 + 256);
@@ -75,6 +80,8 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
     s.smem_bytes = off;
     uint32_t col = 0;
     s.t_f = col;
+    col += nn;
+    s.t_flo = col;  // forward lo-product accumulator (split-fp16 forward, see tc.cuh)
     col += nn;
     s.t_g = col;
     col += (uint32_t)max(s.ninp, nn);
@@ -142,12 +149,16 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
     if constexpr (NF == 2) {
         // x-adjacent corners (k, k+1) whose slots differ only in bit 0 share
         // one aligned 16-byte entry pair: fetch it with a single float4 load
+        // (a pair {e, e+1} is 16-byte aligned iff the level offset + 2e is a
+        // multiple of 4 floats; odd-sized dense levels shift later offsets)
         float2 v[8];
+        const uint32_t par = (uint32_t)(tab.offset[l] >> 1) & 1u;
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
-            if ((sl[k] ^ sl[k + 1]) == 1u) {
-                float4 q = __ldg(reinterpret_cast<const float4 *>(tb) + (sl[k] >> 1));
-                const bool lo_first = (sl[k] & 1u) == 0u;
+            const uint32_t lo = min(sl[k], sl[k + 1]);
+            if (max(sl[k], sl[k + 1]) == lo + 1 && ((lo + par) & 1u) == 0u) {
+                const float4 q = __ldg(reinterpret_cast<const float4 *>(tb + 2 * (size_t)lo));
+                const bool lo_first = sl[k] == lo;
                 v[k] = lo_first ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
                 v[k + 1] = lo_first ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
             } else {
@@ -171,21 +182,28 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
     }
     const int64_t tile = i >> 7;
     const int s = (int)(i & 127);
-    uint8_t *base = xtiles + tile * (int64_t)(TILE * ninp * 2);
-    __half hv[NF];
+    // per tile: fp16 hi tile followed by the fp16 lo tile (split-fp16 forward)
+    uint8_t *base = xtiles + tile * (int64_t)(2 * TILE * ninp * 2);
+    uint8_t *base_lo = base + TILE * ninp * 2;
+    __half hv[NF], lv[NF];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) hv[f] = __float2half_rn(acc[f] * tc::kActScale);
+    for (int f = 0; f < NF; ++f) tc::split_f16(acc[f] * tc::kActScale, hv[f], lv[f]);
 #pragma unroll
     for (int f = 0; f < NF; f += 2) {
         if constexpr (NF == 1) {
             *reinterpret_cast<__half *>(base + tc::tile_off(s, l, ninp)) = hv[0];
+            *reinterpret_cast<__half *>(base_lo + tc::tile_off(s, l, ninp)) = lv[0];
         } else {
-            *reinterpret_cast<__half2 *>(base + tc::tile_off(s, l * NF + f, ninp)) = __halves2half2(hv[f], hv[f + 1]);
+            const uint32_t o = tc::tile_off(s, l * NF + f, ninp);
+            *reinterpret_cast<__half2 *>(base + o) = __halves2half2(hv[f], hv[f + 1]);
+            *reinterpret_cast<__half2 *>(base_lo + o) = __halves2half2(lv[f], lv[f + 1]);
         }
     }
     if (l == m - 1) {
-        for (int cidx = m * NF; cidx < ninp; ++cidx)
+        for (int cidx = m * NF; cidx < ninp; ++cidx) {
             *reinterpret_cast<__half *>(base + tc::tile_off(s, cidx, ninp)) = __float2half_rn(0.0f);
+            *reinterpret_cast<__half *>(base_lo + tc::tile_off(s, cidx, ninp)) = __float2half_rn(0.0f);
+        }
     }
 }
 
@@ -230,7 +248,8 @@ __device__ __forceinline__ void load_row_f16(const uint8_t *tile, int row, int c
 // verbatim: W_0..W_{nh-1} as fp16 core-matrix tiles at o_w[i] (input columns
 // padded to ninp with zeros) and the fp32 output row at o_wout.
 struct MlpImage {
-    uint32_t o_w[MAX_NH], o_wout;
+    uint32_t o_w[MAX_NH], o_wout, o_wlo[MAX_NH];
+    int with_lo;
 };
 
 __global__ void pack_mlp_image_kernel(const float *__restrict__ wflat, int nin, int ninp, int nn, int nh,
@@ -242,19 +261,27 @@ __global__ void pack_mlp_image_kernel(const float *__restrict__ wflat, int nin, 
         const int win = i == 0 ? nin : nn, wp = i == 0 ? ninp : nn;
         for (int q = t0; q < nn * wp; q += stride) {
             int o = q / wp, j = q % wp;
-            *reinterpret_cast<__half *>(out + img.o_w[i] + tc::tile_off(o, j, wp)) =
-                __float2half_rn(j < win ? src[o * win + j] : 0.0f);
+            const uint32_t off = tc::tile_off(o, j, wp);
+            __half hi, lo;
+            tc::split_f16(j < win ? src[o * win + j] : 0.0f, hi, lo);
+            *reinterpret_cast<__half *>(out + img.o_w[i] + off) = hi;
+            if (img.with_lo) *reinterpret_cast<__half *>(out + img.o_wlo[i] + off) = lo;
         }
         src += (int64_t)nn * win;
     }
     for (int q = t0; q < nn; q += stride) reinterpret_cast<float *>(out + img.o_wout)[q] = src[q];
 }
 
+// o_wlo == nullptr: hi tiles only (the inference kernels' image)
 int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const uint32_t *o_w, uint32_t o_wout,
-                   uint8_t *image, cudaStream_t s) {
+                   uint8_t *image, cudaStream_t s, const uint32_t *o_wlo) {
     MlpImage img;
-    for (int i = 0; i < nh; ++i) img.o_w[i] = o_w[i];
+    for (int i = 0; i < nh; ++i) {
+        img.o_w[i] = o_w[i];
+        img.o_wlo[i] = o_wlo ? o_wlo[i] : 0;
+    }
     img.o_wout = o_wout;
+    img.with_lo = o_wlo != nullptr;
     pack_mlp_image_kernel<<<64, 256, 0, s>>>(wflat, nin, ninp, nn, nh, img, image);
     return check_launch("pack_mlp_image");
 }
@@ -304,12 +331,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
         const float tgt = valid ? targets[row] : 0.0f;
         // ---- X tile: global (L2) -> smem; rows past the batch are zeroed
         {
-            const uint4 *src = reinterpret_cast<const uint4 *>(xtiles + tile * (int64_t)(TILE * NINP * 2));
+            // hi tile then lo tile (contiguous both in global and in smem: o_xlo = o_x + tile bytes)
+            const uint4 *src = reinterpret_cast<const uint4 *>(xtiles + tile * (int64_t)(2 * TILE * NINP * 2));
             uint4 *dst = reinterpret_cast<uint4 *>(smem + sh.o_x);
             const int64_t nvalid = b - tile * TILE;
-            for (int q = tid; q < tile_u4; q += TC_THREADS) {
-                // core-matrix row q*16 bytes -> sample row ((q*16/128)/(NINP/8))*8 + (q%8)
-                int cm = q >> 3, r = ((cm / (NINP / 8)) << 3) + (q & 7);
+            for (int q = tid; q < 2 * tile_u4; q += TC_THREADS) {
+                // core-matrix row (q % tile_u4)*16 bytes -> sample row ((..)/(NINP/8))*8 + (q%8)
+                const int qq = q % tile_u4;
+                int cm = qq >> 3, r = ((cm / (NINP / 8)) << 3) + (qq & 7);
                 dst[q] = r < nvalid ? src[q] : make_uint4(0, 0, 0, 0);
             }
         }
@@ -321,13 +350,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
         for (int i = 0; i < NH; ++i) {
             const int win = (i == 0) ? NINP : NN;
             if (tid == 0) {
+                // split-fp16 forward: hi*hi -> t_f; lo*hi + hi*lo -> t_flo (x kLoScale)
                 tc::fence_after();
-                uint32_t a0 = tc::smem_u32(smem + sh.o_h[i]);
-                uint32_t b0 = tc::smem_u32(smem + sh.o_w[i]);
+                const uint32_t ah = tc::smem_u32(smem + sh.o_h[i]);
+                const uint32_t al = tc::smem_u32(smem + (i == 0 ? sh.o_xlo : sh.o_hlo[(i - 1) & 1]));
+                const uint32_t bh = tc::smem_u32(smem + sh.o_w[i]);
+                const uint32_t bl = tc::smem_u32(smem + sh.o_wlo[i]);
+                const uint32_t sbo = (win / 8) * 128;
                 for (int k = 0; k < win / 16; ++k) {
-                    uint64_t ad = tc::make_desc(a0 + k * 256, 128, (win / 8) * 128);
-                    uint64_t bd = tc::make_desc(b0 + k * 256, 128, (win / 8) * 128);
-                    tc::mma_f16(tmem + sh.t_f, ad, bd, idesc_fwd, k > 0);
+                    const uint64_t adh = tc::make_desc(ah + k * 256, 128, sbo), adl = tc::make_desc(al + k * 256, 128, sbo);
+                    const uint64_t bdh = tc::make_desc(bh + k * 256, 128, sbo), bdl = tc::make_desc(bl + k * 256, 128, sbo);
+                    tc::mma_f16(tmem + sh.t_f, adh, bdh, idesc_fwd, k > 0);
+                    tc::mma_f16(tmem + sh.t_flo, adl, bdh, idesc_fwd, k > 0);
+                    tc::mma_f16(tmem + sh.t_flo, adh, bdl, idesc_fwd, 1);
                 }
                 tc::mma_commit(&mbar);
             }
@@ -337,13 +372,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
             int c0, nc;
             half_cols(NN, h, c0, nc);
             uint8_t *dst = smem + sh.o_h[i + 1];
+            uint8_t *dst_lo = smem + sh.o_hlo[i & 1];
             // accumulator = kActScale * pre-activation: ReLU commutes with the
             // positive scale, so the stored activations stay scaled too
             for (int c = c0; c < c0 + nc; c += 16) {
-                float v[16];
+                float v[16], vl[16];
                 tc::tmem_ld16(tmem + lane_base + sh.t_f + c, v);
+                tc::tmem_ld16(tmem + lane_base + sh.t_flo + c, vl);
                 tc::tmem_wait_ld();
-                store_row_f16(dst, s, c, NN, v, true);
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
+                store_row_f16(dst, s, c, NN, v, false);
+                if (i < NH - 1) {
+                    // lo part of the activation for the next layer's split product
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) vl[e] = (v[e] - __half2float(__float2half_rn(v[e]))) * tc::kLoScale;
+                    store_row_f16(dst_lo, s, c, NN, vl, false);
+                }
                 if (i == NH - 1) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * fmaxf(v[e], 0.0f);
@@ -534,6 +579,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
         const bool coarse = l < n_coarse;
         float *gl = coarse ? acc_s + tab.offset[l] : grads + tab.offset[l];
         if constexpr (NF == 2) {
+            const uint32_t par = (uint32_t)(tab.offset[l] >> 1) & 1u;
             if (!coarse) {
                 // fine levels: x-adjacent corner pairs in one aligned 16-byte
                 // entry pair go out as a single float4 RED
@@ -543,10 +589,11 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
                     uint32_t s0 = slot32(c.cx, c.cy + yo, c.cz + zo, r1, mask, dense);
                     uint32_t s1 = slot32(c.cx + 1, c.cy + yo, c.cz + zo, r1, mask, dense);
                     float w0 = cw32(c, k), w1 = cw32(c, k + 1);
-                    if ((s0 ^ s1) == 1u) {
-                        float4 q = (s0 & 1u) == 0u ? make_float4(w0 * d[0], w0 * d[1], w1 * d[0], w1 * d[1])
-                                                   : make_float4(w1 * d[0], w1 * d[1], w0 * d[0], w0 * d[1]);
-                        atomicAdd(reinterpret_cast<float4 *>(gl) + (s0 >> 1), q);
+                    const uint32_t lo = min(s0, s1);
+                    if (max(s0, s1) == lo + 1 && ((lo + par) & 1u) == 0u) {   // adjacent and 16-byte aligned
+                        float4 q = s0 == lo ? make_float4(w0 * d[0], w0 * d[1], w1 * d[0], w1 * d[1])
+                                            : make_float4(w1 * d[0], w1 * d[1], w0 * d[0], w0 * d[1]);
+                        atomicAdd(reinterpret_cast<float4 *>(gl + 2 * (size_t)lo), q);
                     } else {
                         atomicAdd(reinterpret_cast<float2 *>(gl) + s0, make_float2(w0 * d[0], w0 * d[1]));
                         atomicAdd(reinterpret_cast<float2 *>(gl) + s1, make_float2(w1 * d[0], w1 * d[1]));
@@ -636,7 +683,7 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
     }
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
     p.off_x = 0;
-    p.off_dfeat = al(p.ntiles * TILE * p.sh.ninp * 2);
+    p.off_dfeat = al(p.ntiles * TILE * p.sh.ninp * 4);  // hi + lo fp16 tiles
     p.off_wpart = p.off_dfeat + al(b * p.sh.nin * 4);
     p.off_cpart = p.off_wpart + al((int64_t)p.grid_mlp * p.sh.w_floats * 4);
     p.off_img = p.off_cpart + al((int64_t)p.grid_sc * p.coarse_floats * 4);
@@ -656,7 +703,7 @@ int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
     int64_t ntiles = (b + TILE - 1) / TILE;
     int grid_mlp = (int)(ntiles < sms ? ntiles : sms);
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
-    return al(ntiles * TILE * p.sh.ninp * 2) + al(b * p.sh.nin * 4) + al((int64_t)grid_mlp * p.sh.w_floats * 4) +
+    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) + al((int64_t)grid_mlp * p.sh.w_floats * 4) +
            al((int64_t)sms * (COARSE_BYTES / 4) * 4) + al(p.sh.o_x) + 256;
 }
 
@@ -687,7 +734,7 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
     }
     int st = check_launch("encode_tiles_kernel");
     if (st) return st;
-    st = pack_mlp_image(params + woff, p.sh.nin, p.sh.ninp, nn, nh, p.sh.o_w, p.sh.o_wout, wimg, s);
+    st = pack_mlp_image(params + woff, p.sh.nin, p.sh.ninp, nn, nh, p.sh.o_w, p.sh.o_wout, wimg, s, p.sh.o_wlo);
     if (st) return st;
     cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh.smem_bytes);
     const float dscale = exp2f(rintf(log2f((float)b_global)));  // ~B: L1 deltas become +-1 in fp16

@@ -1,0 +1,123 @@
+"""Macro-cell acceleration grid (macrocell.py of the reference) on the device.
+
+Per-cell value ranges (bordered min/max, macrocell.py:63-76) and exact
+opacity majorants (macrocell.py:136-156) are computed by csrc/render.cu
+kernels; `macrocell_from_model` decodes Phi at every voxel centre with the
+exact evaluator (float64 centre coordinates, as macrocell.py:87-94) and
+reduces on the device.  Arrays (`value_lo`, `value_hi`, `mu_max`) are device
+tensors shaped (gz, gy, gx).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError
+from .transfer import TransferFunction
+
+DEFAULT_CELL_SIZE = 64
+
+
+@dataclass
+class MacroCellGrid:
+    """macrocell.py:27-55."""
+    vol_dims: tuple
+    n_g: int = DEFAULT_CELL_SIZE
+    value_lo: object = field(default=None, repr=False)
+    value_hi: object = field(default=None, repr=False)
+    mu_max: object = field(default=None, repr=False)
+
+    def __post_init__(self) -> None:
+        if self.n_g < 1:
+            raise ConfigError(f"macro-cell size must be >= 1, got {self.n_g}")
+        dx, dy, dz = (int(d) for d in self.vol_dims)
+        if min(dx, dy, dz) < 1:
+            raise ConfigError(f"bad volume dims {self.vol_dims}")
+        self.vol_dims = (dx, dy, dz)
+        gx, gy, gz = self.grid_dims
+        shape = (gz, gy, gx)
+        dev = _lib.device()
+        if self.value_lo is None:
+            self.value_lo = torch.full(shape, float("inf"), dtype=torch.float32, device=dev)
+            self.value_hi = torch.full(shape, float("-inf"), dtype=torch.float32, device=dev)
+        if self.mu_max is None:
+            self.mu_max = torch.zeros(shape, dtype=torch.float32, device=dev)
+        for name in ("value_lo", "value_hi", "mu_max"):
+            arr = getattr(self, name)
+            if not isinstance(arr, torch.Tensor):
+                setattr(self, name, torch.as_tensor(np.asarray(arr, dtype=np.float32), device=dev))
+            if tuple(getattr(self, name).shape) != shape:
+                raise ConfigError(f"cell array shape {tuple(getattr(self, name).shape)} != grid {shape}")
+
+    @property
+    def grid_dims(self):
+        return tuple(-(-d // self.n_g) for d in self.vol_dims)
+
+
+def macrocell_empty(dims, n_g: int = DEFAULT_CELL_SIZE) -> MacroCellGrid:
+    return MacroCellGrid(vol_dims=tuple(dims), n_g=n_g)
+
+
+def _ranges(vals: torch.Tensor, dims, n_g: int, clip: bool) -> MacroCellGrid:
+    grid = macrocell_empty(dims, n_g)
+    dx, dy, dz = grid.vol_dims
+    _lib.call("nvol_macrocell_ranges", _lib.ptr(vals.contiguous()), dx, dy, dz, n_g, int(clip),
+              _lib.ptr(grid.value_lo), _lib.ptr(grid.value_hi), _lib.stream())
+    return grid
+
+
+def macrocell_build(fld, n_g: int = DEFAULT_CELL_SIZE) -> MacroCellGrid:
+    """Per-cell min/max (with border) of a dense volume (macrocell.py:79-81)."""
+    return _ranges(fld.normalized, fld.meta.dims, n_g, clip=False)
+
+
+def macrocell_from_model(model, n_g: int = DEFAULT_CELL_SIZE, chunk: int = 0) -> MacroCellGrid:
+    """Ranges from the model decoded at voxel centres (macrocell.py:84-98)."""
+    from .trainer import decode_brick
+    dx, dy, dz = model.dims
+    vals = torch.empty((dz, dy, dx), dtype=torch.float32, device=model.flat_params.device)
+    decode_brick(model, (dx, dy, dz), 0, dz, vals, mode="centres64")
+    return _ranges(vals, (dx, dy, dz), n_g, clip=True)
+
+
+def macrocell_update_online(grid: MacroCellGrid, batch) -> None:
+    """Widen cell ranges with a training batch (macrocell.py:101-133), on the device."""
+    c = batch.coords if isinstance(batch.coords, torch.Tensor) else torch.as_tensor(batch.coords)
+    t = batch.targets if isinstance(batch.targets, torch.Tensor) else torch.as_tensor(batch.targets)
+    if c.shape[0] == 0:
+        return
+    dev = grid.value_lo.device
+    c = c.to(dev, torch.float32)
+    t = t.to(dev, torch.float32)
+    gx, gy, gz = grid.grid_dims
+    n = grid.n_g
+    dims = torch.tensor(grid.vol_dims, dtype=torch.float32, device=dev)
+    s = c * dims - 0.5
+    i0 = torch.floor(s).to(torch.int64)
+    vmax = torch.tensor(grid.vol_dims, dtype=torch.int64, device=dev) - 1
+    zero = torch.zeros_like(vmax)
+    v_lo = torch.minimum(torch.maximum(i0, zero), vmax)
+    v_hi = torch.minimum(torch.maximum(i0 + (s > i0.to(torch.float32)).to(torch.int64), zero), vmax)
+    bound = torch.tensor((gx, gy, gz), dtype=torch.int64, device=dev) - 1
+    c_lo = torch.minimum(torch.maximum(torch.div(v_hi + n - 1, n, rounding_mode="floor") - 1, zero), bound)
+    c_hi = torch.minimum(torch.maximum(torch.div(v_lo + 1, n, rounding_mode="floor"), zero), bound)
+    flat = torch.cat([(iz * gy + iy) * gx + ix
+                      for iz in (c_lo[:, 2], c_hi[:, 2]) for iy in (c_lo[:, 1], c_hi[:, 1])
+                      for ix in (c_lo[:, 0], c_hi[:, 0])])
+    tt = t.repeat(8)
+    lo = grid.value_lo.view(-1)
+    hi = grid.value_hi.view(-1)
+    lo.scatter_reduce_(0, flat, tt, reduce="amin")
+    hi.scatter_reduce_(0, flat, tt, reduce="amax")
+
+
+def macrocell_set_tf(grid: MacroCellGrid, tf: TransferFunction) -> None:
+    """Exact per-cell majorant for the current TF (macrocell.py:136-156)."""
+    pv = np.ascontiguousarray(tf.opacity_points[:, 0], dtype=np.float64)
+    pa = np.ascontiguousarray(tf.opacity_points[:, 1], dtype=np.float64)
+    cv = (np.ctypeslib.as_ctypes(pv), np.ctypeslib.as_ctypes(pa))
+    _lib.call("nvol_macrocell_set_tf", _lib.ptr(grid.value_lo), _lib.ptr(grid.value_hi), grid.value_lo.numel(),
+              cv[0], cv[1], len(pv), float(tf.density_scale), _lib.ptr(grid.mu_max), _lib.stream())

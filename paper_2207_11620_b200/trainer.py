@@ -204,7 +204,7 @@ def decode_brick(model: NeuralModel, dims, z0: int, nz: int, out: torch.Tensor, 
     _lib.call("nvol_decode", _lib.ptr(model.flat_params), off, res, ent, dense, c.n_levels, c.n_features_per_level,
               _lib.ptr(model._weights_flat()), _lib.host_i32(widths), len(widths) - 1,
               int(model.mlp.config.output_activation == "relu"), dx, dy, dz, z0, nz, float(lo), float(hi),
-              _lib.ptr(out), 1 if mode == "tensor" else 0,
+              _lib.ptr(out), {"exact": 0, "tensor": 1, "centres64": 2}[mode],
               _lib.ptr(model.mlp_image()) if mode == "tensor" else None, _lib.stream())
 
 

@@ -1,0 +1,153 @@
+"""GPU renderer / macro-cell parity against the reference's golden renders.
+
+Bars: macro-cell ranges and majorants bit-exact (exact evaluator, float64
+centres as macrocell.py:87-94); images: the reference composites with glibc
+powf while the device evaluates pow in float64 and rounds (identical in all
+but ~0.1% of inputs, 1 ulp), so images are compared at float tolerance
+(max |diff| <= 2e-3, PSNR >= 50 dB) and field-evaluation counts within 1%;
+schedule invariants (K batching, in-shader == wavefront) are bitwise.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden, golden_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def scene(nv):
+    from paper_2207_11620_b200 import macrocell
+    from paper_2207_11620_b200.camera import default_camera
+    from paper_2207_11620_b200.model import build_model
+    from paper_2207_11620_b200.transfer import default_tf
+    z = golden("render_small.npz")
+    dims = tuple(int(x) for x in z["dims"])
+    model = build_model(golden_config(z), dims=dims, seed=0)
+    model.load_blob(z["blob"])
+    grid = macrocell.macrocell_from_model(model, n_g=8)
+    tf = default_tf()
+    macrocell.macrocell_set_tf(grid, tf)
+    return z, dims, model, grid, tf, default_camera(dims, 48, 27)
+
+
+def img_psnr(a, b):
+    e = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
+    return 99.0 if e == 0 else -10 * math.log10(e)
+
+
+def test_macrocells_from_model_bit_exact(scene):
+    z, dims, model, grid, tf, cam = scene
+    np.testing.assert_array_equal(grid.value_lo.cpu().numpy(), z["mc_lo"])
+    np.testing.assert_array_equal(grid.value_hi.cpu().numpy(), z["mc_hi"])
+    np.testing.assert_array_equal(grid.mu_max.cpu().numpy(), z["mc_mu"])
+
+
+def test_macrocells_from_volume_bit_exact(scene):
+    from paper_2207_11620_b200 import macrocell
+    from paper_2207_11620_b200.volume import ScalarField, VolumeMeta
+    z, dims, model, grid, tf, cam = scene
+    fld = ScalarField(VolumeMeta(dims, "f32", (0.0, 1.0)), z["norm"])
+    g = macrocell.macrocell_build(fld, n_g=8)
+    macrocell.macrocell_set_tf(g, tf)
+    np.testing.assert_array_equal(g.value_lo.cpu().numpy(), z["mcf_lo"])
+    np.testing.assert_array_equal(g.value_hi.cpu().numpy(), z["mcf_hi"])
+    np.testing.assert_array_equal(g.mu_max.cpu().numpy(), z["mcf_mu"])
+
+
+CASES = {
+    "rm_mc": dict(mode="raymarch", use_macrocells=True),
+    "rm_nomc": dict(mode="raymarch", use_macrocells=False),
+    "rms_mc": dict(mode="raymarch_shadow", use_macrocells=True, k_batch=4),
+    "rm_mc_step": dict(mode="raymarch", use_macrocells=True, step_size=0.5, max_step=16.0),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_wavefront_matches_reference(scene, name):
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    cfg = RenderConfig(**CASES[name])
+    stats = []
+    img = render(model, tf, cam, cfg, "wavefront", grid=grid if cfg.use_macrocells else None, stats_out=stats)
+    want = z[f"img_{name}"]
+    assert np.abs(img - want).max() <= 2e-3
+    assert img_psnr(img, want) >= 50.0
+    ev = int(z[f"evals_{name}"])
+    assert abs(stats[0].evals - ev) <= max(2, 0.01 * ev)
+
+
+def test_in_shader_equals_wavefront_and_reference(scene):
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    cfg = RenderConfig(mode="raymarch", use_macrocells=True)
+    a = render(model, tf, cam, cfg, "reference", grid=grid)
+    b = render(model, tf, cam, cfg, "wavefront", grid=grid)
+    np.testing.assert_array_equal(a, b)                 # same device state machine, bitwise
+    assert img_psnr(a, z["img_megakernel"]) >= 50.0
+
+
+def test_k_batching_is_scheduling_only(scene):
+    # test_render.py:116-128
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    imgs = [render(model, tf, cam, RenderConfig(mode="raymarch", use_macrocells=True, k_batch=k), grid=grid)
+            for k in (1, 3, 8, 16)]
+    for im in imgs[1:]:
+        np.testing.assert_array_equal(im, imgs[0])
+
+
+def test_macrocells_never_increase_evals(scene):
+    # test_render.py:234-255
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    s_on, s_off = [], []
+    render(model, tf, cam, RenderConfig(mode="raymarch", use_macrocells=True), "reference", grid=grid, stats_out=s_on)
+    render(model, tf, cam, RenderConfig(mode="raymarch", use_macrocells=False), "reference", stats_out=s_off)
+    assert s_on[0].evals <= s_off[0].evals
+
+
+def test_grid_field_render(scene):
+    from paper_2207_11620_b200 import macrocell
+    from paper_2207_11620_b200.render import RenderConfig, render
+    from paper_2207_11620_b200.volume import ScalarField, VolumeMeta
+    z, dims, model, grid, tf, cam = scene
+    fld = ScalarField(VolumeMeta(dims, "f32", (0.0, 1.0)), z["norm"])
+    g = macrocell.macrocell_build(fld, n_g=8)
+    stats = []
+    img = render(fld, tf, cam, RenderConfig(mode="raymarch", use_macrocells=True), grid=g, stats_out=stats)
+    assert np.abs(img - z["img_grid_mc"]).max() <= 2e-3
+    assert abs(stats[0].evals - int(z["evals_grid_mc"])) <= max(2, 0.01 * int(z["evals_grid_mc"]))
+
+
+def test_tensor_core_batched_inference_render(scene):
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    model.infer_mode = "tensor"
+    try:
+        img = render(model, tf, cam, RenderConfig(mode="raymarch", use_macrocells=True), "wavefront", grid=grid)
+    finally:
+        model.infer_mode = "exact"
+    assert img_psnr(img, z["img_rm_mc"]) >= 35.0
+
+
+def test_online_macrocells_inside_precomputed(nv):
+    # test_macrocell.py:116-139: streamed ranges never exceed the bordered precomputed ones
+    from paper_2207_11620_b200 import fields, macrocell
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    fld = fields.rasterize("blobs", (24, 20, 16), host=True)
+    pre = macrocell.macrocell_build(fld, n_g=4)
+    onl = macrocell.macrocell_empty((24, 20, 16), n_g=4)
+    s = InCoreSampler(fld, seed=3)
+    for _ in range(20):
+        macrocell.macrocell_update_online(onl, s.sample(4096))
+    lo, hi = onl.value_lo.cpu().numpy(), onl.value_hi.cpu().numpy()
+    plo, phi = pre.value_lo.cpu().numpy(), pre.value_hi.cpu().numpy()
+    touched = lo <= hi
+    assert touched.mean() > 0.9
+    assert np.all(lo[touched] >= plo[touched] - 1e-7) and np.all(hi[touched] <= phi[touched] + 1e-7)
