@@ -2,25 +2,25 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Own arm: K device-resident training steps (sample -> fused fwd/bwd ->
-[NCCL all-reduce] -> flat Adam, one CUDA graph per step) of the cfg2 model
-(16 levels x 2^19 x 2 features, 4x64 ReLU MLP, B = 65,536 samples/step, L1 +
-Adam) on a synthetic 256^3 mlobb volume, timed with CUDA events, max over
-ranks.  Data parallel runs shard the fixed global batch (strong scaling,
-bit-identical sample stream to the single-GPU run).  Prints ONE JSON line.
+Own arm: K device-resident training steps (sample -> encode / tcgen05 MLP /
+scatter (three streams) -> [NCCL all-reduce] -> flat Adam; one CUDA graph per
+step) of the cfg2 model (16 levels x 2^19 x 2 features, 4x64 ReLU MLP,
+B = 65,536 samples/step, L1 + Adam) on a synthetic 256^3 mlobb volume, timed
+with CUDA events, max over ranks.  Data-parallel runs shard the fixed global
+batch (strong scaling; the union of the shards is the single-process batch).
+Prints ONE JSON line; decode (cfg3) and render (cfg4) rates ride along in
+sub-objects.
 
 Reference arm: the CPU oracle (the reference's algorithm restated in C +
-numpy/OpenBLAS, oracle/) on all host cores, same config / metric.
+numpy/OpenBLAS, oracle/) on all host threads, same config / metric.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -38,6 +38,7 @@ DIMS = (256, 256, 256)
 FIELD = "mlobb"
 METRIC = "train samples/s (hash-grid+fused-MLP step)"
 PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
+N_PARAMS_CFG2 = 12_181_394
 
 
 def peaks():
@@ -58,18 +59,19 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the sampler start before the timed region
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.lines = []
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -82,7 +84,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             try:
                 sm.append(float(f[0]))
@@ -119,8 +121,21 @@ def cpu_train_rate(steps: int, budget_s: float = 30.0):
     dt = time.perf_counter() - t0
     threads = max(orc.num_threads(), int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1)))
     return {"value": B * n / dt, "unit": "samples/s", "cores": int(threads), "kind": "port",
-            "sample": f"{n} full cfg2 training steps (B=65536, sampling + encode + MLP + loss + scatter + dense Adam "
-                      f"over 12,181,394 params) of the C/numpy oracle, {dt:.2f} s"}
+            "sample": f"{n} full cfg2 training steps (B=65536: sampling + encode + MLP + loss + scatter + dense Adam "
+                      f"over 12,181,394 params) of the C/numpy oracle in {dt:.2f} s on {threads} threads"}
+
+
+def cpu_decode_rate(model_blob, n: int = 48):
+    """Oracle eval_batch (the reference decode path) on an n^3 brick of the cfg2 model."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import nvol_oracle as orc
+    m = orc.OracleModel(CFG2, seed=0)
+    m.load_flat(model_blob)
+    t0 = time.perf_counter()
+    orc.decode(m, (n, n, n), slab_z=8)
+    dt = time.perf_counter() - t0
+    return {"value": n ** 3 / dt, "unit": "samples/s", "sample": f"{n}^3 voxel decode (eval_batch path)",
+            "cores": orc.num_threads(), "kind": "port"}
 
 
 # ---------------------------------------------------------------------------- reference arm
@@ -142,26 +157,39 @@ def run_reference(args):
 
 # ---------------------------------------------------------------------------- own arm
 
+def _event_ms(torch, fn, reps=5, nev=2):
+    """Device time of fn() with CUDA events on the current stream; a spin
+    kernel in front keeps the host ahead of the GPU so launch latency is
+    excluded."""
+    out = []
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+        for e in ev:          # torch creates the CUDA event lazily on first record
+            e.record()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
+        fn(ev)
+        torch.cuda.synchronize()
+        out.append([ev[0].elapsed_time(e) for e in ev[1:]])
+    return np.median(np.array(out), axis=0)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2207_11620_b200 import _lib, fields
+    from paper_2207_11620_b200.distributed import init_from_env
     from paper_2207_11620_b200.model import build_model
     from paper_2207_11620_b200.sampler import InCoreSampler, SampleBatch
     from paper_2207_11620_b200.trainer import StepPipeline, decode
 
-    L = _lib.load()
+    rank, world, local = init_from_env("nccl")
+    torch.cuda.set_device(local)
+    _lib.load()
     hbm, tc_sus, tc_burst, peak_kind = peaks()
-    mode = args.mode
     model = build_model(CFG2, dims=DIMS, seed=0)
-    model.train_mode = mode
+    model.train_mode = args.mode
     field = fields.rasterize(FIELD, DIMS)
     sampler = InCoreSampler(field, seed=1)
     B = model.batch_size
@@ -169,11 +197,8 @@ def run_ours(args):
     pipe = StepPipeline(model, sampler, capacity=K + W + 2, rank=rank, world=world)
     stream = torch.cuda.current_stream()
 
-    # ---- warm-up (includes graph capture)
-    pipe.step(W)
+    pipe.step(W)                      # warm-up (the second step captures the graph)
     torch.cuda.synchronize()
-
-    # ---- timed region: K graph replays
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -193,55 +218,67 @@ def run_ours(args):
     ms_per_step = ms / K
     value = B * K / (ms / 1e3)
 
-    # ---- per-phase device times (instrumented eager steps, same kernels as the graph)
-    phases = {"sample": [], "fwd_bwd": [], "adam": []}
+    # ---- per-kernel device times: CUDA events on the launching stream
     vol = sampler.volume
     dz, dy, dx = vol.shape
-    for _ in range(5):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        e[0].record(stream)
+    b = pipe.b
+
+    def sample_fn(ev):
+        ev[0].record(stream)
         _lib.call("nvol_sample_incore_dev", *sampler.rng.words(), pipe.u32_base, _lib.ptr(pipe.counter), pipe.t0, B,
-                  pipe.row0, pipe.b, _lib.ptr(vol), dx, dy, dz, _lib.ptr(pipe.coords), _lib.ptr(pipe.targets),
+                  pipe.row0, b, _lib.ptr(vol), dx, dy, dz, _lib.ptr(pipe.coords), _lib.ptr(pipe.targets),
                   _lib.stream())
-        e[1].record(stream)
+        ev[1].record(stream)
+
+    def stages_fn(ev):
+        arr = (__import__("ctypes").c_void_p * 4)(*[e.cuda_event for e in ev[:4]])
+        _lib.call("nvol_set_stage_events", arr, 4)
         model.fwd_bwd_device(pipe.coords, pipe.targets, pipe.acc, b_global=B)
-        e[2].record(stream)
+        ev[4].record(stream)
+        _lib.call("nvol_set_stage_events", None, 0)
+
+    def adam_fn(ev):
+        ev[0].record(stream)
         _lib.call("nvol_adam_flat_dev", _lib.ptr(model.flat_params), _lib.ptr(model.flat_grads), _lib.ptr(model.flat_m),
                   _lib.ptr(model.flat_v), model.flat_size, _lib.ptr(pipe.sched), pipe.sched.numel() // 3,
                   _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_flag), _lib.stream())
-        e[3].record(stream)
-        torch.cuda.synchronize()
-        phases["sample"].append(e[0].elapsed_time(e[1]))
-        phases["fwd_bwd"].append(e[1].elapsed_time(e[2]))
-        phases["adam"].append(e[2].elapsed_time(e[3]))
-    ph = {k: float(np.median(v)) for k, v in phases.items()}
+        ev[1].record(stream)
+
+    t_sample = float(_event_ms(torch, sample_fn)[0])
+    t_adam = float(_event_ms(torch, adam_fn)[0])
+    kernels = {"sample_incore_kernel": t_sample, "adam_flat_kernel": t_adam}
+    if args.mode == 1:
+        st = _event_ms(torch, stages_fn, nev=5)
+        kernels.update({"encode_tiles_kernel": float(st[0]), "mlp_tc_kernel": float(st[1] - st[0]),
+                        "scatter_kernel": float(st[2] - st[1]), "reduce_partials x2": float(st[3] - st[2])})
     n_flat = model.flat_size
     adam_bytes = 32 * n_flat
-    m_lv, nf = 16, 2
-    gather_bytes = B * m_lv * 8 * nf * 4
-    scatter_bytes = 2 * gather_bytes
+    gather_bytes = B * 16 * 8 * 2 * 4
     mlp_flops = 3 * 2 * B * (32 * 64 + 3 * 64 * 64 + 64)
-    dominant = max(ph, key=ph.get)
-    if dominant == "adam":
-        ach = adam_bytes / (ph["adam"] * 1e-3) / 1e9
-        roof = {"kernel": "adam_flat_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": None, "algorithmic_bytes_per_launch": adam_bytes,
-                "peak_source": peak_kind}
-    elif dominant == "fwd_bwd":
-        byts = gather_bytes + scatter_bytes + B * 16
-        ach = byts / (ph["fwd_bwd"] * 1e-3) / 1e9
-        roof = {"kernel": "train_fwd_bwd (encode gather + MLP + scatter)", "bound": "hbm", "achieved": ach,
-                "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
-                "algorithmic_bytes_per_launch": byts, "peak_source": peak_kind,
-                "mlp_tflops": mlp_flops / (ph["fwd_bwd"] * 1e-3) / 1e12}
+    # roofline of the dominant single kernel
+    dom = max(kernels, key=kernels.get)
+    per_unit = {"adam_flat_kernel": (adam_bytes, "hbm", "32 B/param x 12,181,396 flat params"),
+                "scatter_kernel": (2 * gather_bytes, "hbm", "16 levels x 8 corners x 2 feat x 4 B x 2 (RMW) per sample"),
+                "encode_tiles_kernel": (gather_bytes + B * 12 + B * 64 * 2, "hbm",
+                                        "1,024 B gathered + 12 B coords + 128 B fp16 tiles per sample"),
+                "sample_incore_kernel": (B * 48, "hbm", "48 B per sample")}
+    if dom in per_unit:
+        byts, bound, how = per_unit[dom]
+        ach = byts / (kernels[dom] * 1e-3) / 1e9
+        roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": None, "algorithmic_bytes_per_launch": byts, "algorithmic_basis": how,
+                "launch_ms": kernels[dom], "peak_source": peak_kind}
     else:
-        byts = B * 48
-        ach = byts / (ph["sample"] * 1e-3) / 1e9
-        roof = {"kernel": "sample_incore_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "traffic": None, "algorithmic_bytes_per_launch": byts, "peak_source": peak_kind}
-    step_bytes = adam_bytes + gather_bytes + scatter_bytes + B * 64
+        ach = mlp_flops / (kernels[dom] * 1e-3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tc_sus, "unit": "TFLOP/s",
+                "frac": ach / tc_sus, "traffic": None, "algorithmic_flops_per_launch": mlp_flops,
+                "launch_ms": kernels[dom], "peak_source": peak_kind}
+    step_bytes = adam_bytes + 3 * gather_bytes + B * 64
     roof["step_algorithmic_bytes"] = step_bytes
     roof["step_frac_of_hbm"] = step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm
+    roof["kernel_ms"] = kernels
+    if args.mode == 1:
+        roof["mlp_tc_tflops"] = mlp_flops / (kernels["mlp_tc_kernel"] * 1e-3) / 1e12
 
     # ---- e2e through the public API with host (pinned) buffers
     e2e = None
@@ -262,7 +299,7 @@ def run_ours(args):
                "d2h_bytes_per_step": 8, "api": "NeuralModel.train_step(SampleBatch(host pinned coords, targets))",
                "steps": e2e_steps}
 
-    # ---- decode (cfg3 shape, reported beside the headline)
+    # ---- decode (cfg3) and render (cfg4) beside the headline
     dec = None
     if world == 1 and not args.no_decode:
         dd = (args.decode_dim,) * 3
@@ -277,8 +314,15 @@ def run_ours(args):
         dms = d0.elapsed_time(d1)
         nvox = dd[0] * dd[1] * dd[2]
         dec = {"value": nvox / (dms / 1e3), "unit": "samples/s", "ms": dms, "dims": list(dd),
-               "mode": args.decode_mode, "mlp_tflops": nvox * 2 * (32 * 64 + 3 * 64 * 64 + 64) / (dms * 1e-3) / 1e12}
+               "mode": args.decode_mode, "workload": "cfg3: full-grid decode of the cfg2 model",
+               "gather_gbs": nvox * 1024 / (dms * 1e-3) / 1e9,
+               "mlp_tflops": nvox * 2 * 3 * (32 * 64 + 3 * 64 * 64) / (dms * 1e-3) / 1e12}
         del out
+        if rank == 0 and not args.no_cpu:
+            dec["cpu_baseline"] = cpu_decode_rate(model.blob().cpu().numpy())
+    rend = None
+    if world == 1 and not args.no_render:
+        rend = render_bench(torch, args)
 
     launches = pipe.launches_per_step() * K
     cpu = None
@@ -291,13 +335,55 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": "cfg2 training step (configs[1]): synthetic 256^3 mlobb volume, HashGrid "
                                        "16 levels x 2^19 x 2 feat, 4x64 ReLU MLP, B=65536/step global, L1 + Adam",
-                           "global_batch": B, "parallelism": f"dp{world}", "mode": "tcgen05" if mode else "simt",
+                           "global_batch": B, "parallelism": f"dp{world}",
+                           "engine": "tcgen05 (split-fp16 forward, fp16 backward, fp32 accumulate)" if args.mode
+                           else "simt fp32",
                            "l2": "inputs larger than L2: each step streams 390 MB of Adam state (> 126 MB L2)"},
-                "phases_ms": ph, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary(), "decode": dec, "final_loss": float(losses[-1])}
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "decode": dec, "render": rend, "final_loss": float(losses[-1])}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def render_bench(torch, args):
+    """cfg4: 1920x1080 macro-cell ray march of a cfg2 model trained on blobs 256^3."""
+    from paper_2207_11620_b200 import fields
+    from paper_2207_11620_b200.camera import default_camera
+    from paper_2207_11620_b200.macrocell import macrocell_from_model, macrocell_set_tf
+    from paper_2207_11620_b200.model import build_model
+    from paper_2207_11620_b200.render import RenderConfig, render_frame_device
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    from paper_2207_11620_b200.trainer import train
+    from paper_2207_11620_b200.transfer import default_tf
+    fld = fields.rasterize("blobs", DIMS)
+    m = build_model(CFG2, dims=DIMS, seed=0)
+    m.train_mode = args.mode
+    train(m, InCoreSampler(fld, seed=1), steps=args.render_train_steps)
+    tf = default_tf()
+    g0 = time.perf_counter()
+    grid = macrocell_from_model(m, n_g=16)
+    macrocell_set_tf(grid, tf)
+    torch.cuda.synchronize()
+    mc_ms = (time.perf_counter() - g0) * 1e3
+    cam = default_camera(DIMS, 1920, 1080)
+    cfg = RenderConfig(mode="raymarch", use_macrocells=True, k_batch=8, step_size=1.0, max_step=64.0)
+    res = {"workload": "cfg4: 1920x1080 raymarch, macro-cells n_g=16, K=8, step 1, cfg2 model trained "
+                       f"{args.render_train_steps} steps on blobs 256^3, default TF/camera",
+           "macrocell_from_model_ms": mc_ms}
+    for arch, mode in (("wavefront", "tensor"), ("wavefront", "exact"), ("reference", "exact")):
+        render_frame_device(m, tf, cam, cfg, grid, arch, mode)       # warm-up
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            img, st = render_frame_device(m, tf, cam, cfg, grid, arch, mode)
+            torch.cuda.synchronize()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        fms = float(np.median(ts))
+        res[f"{'inshader' if arch == 'reference' else arch}_{mode}"] = {"frame_ms": fms, "fps": 1e3 / fms, "evals": st.evals,
+                                 "evals_per_s": st.evals / (fms * 1e-3), "iterations": len(st.alive_per_iteration)}
+    return res
 
 
 def main():
@@ -306,10 +392,12 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", type=int, default=int(os.environ.get("NVOL_TRAIN_MODE", "0")))
-    ap.add_argument("--decode-dim", type=int, default=512)
-    ap.add_argument("--decode-mode", default="exact")
+    ap.add_argument("--mode", type=int, default=int(os.environ.get("NVOL_TRAIN_MODE", "1")))
+    ap.add_argument("--decode-dim", type=int, default=1024)
+    ap.add_argument("--decode-mode", default="tensor")
+    ap.add_argument("--render-train-steps", type=int, default=300)
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()

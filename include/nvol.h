@@ -213,6 +213,13 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
                        double *loss_sum, void *workspace, int64_t workspace_bytes, int32_t mode,
                        void *stream);
 
+/* Profiling hook (bench.py): with n >= 4 cudaEvent_t handles set,
+ * nvol_train_fwd_bwd mode 1 runs unchunked on the caller's stream and records
+ * events[0..3] before encode / after encode / after MLP / after scatter, so
+ * each stage kernel is timed with CUDA events on its launching stream.
+ * n = 0 disables.  [host] array of event handles. */
+int nvol_set_stage_events(void *const *events, int32_t n);
+
 /* Workspace bytes nvol_train_fwd_bwd needs for batch b. */
 int64_t nvol_train_workspace_bytes(int64_t b, int32_t n_levels, int32_t n_feat, int32_t n_neurons,
                                    int32_t n_hidden, int32_t mode);

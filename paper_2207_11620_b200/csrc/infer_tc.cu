@@ -1,13 +1,16 @@
 // tcgen05 field inference: fused encode + MLP forward for decode and render.
 //
 // Reference: trainer.py:80-106 (decode: Phi at voxel centres, denormalised)
-// and _kernels.py:154-176 / model.py:178-198 (batched Phi evaluation used by
-// the renderers' phi_eval_staged, _render_kernels.py:518-540).
-// Persistent CTAs (two per SM, 64 TMEM columns each) walk 128-sample tiles:
-// bit-exact fp32 hash-grid encode -> fp16 tile in smem -> one tcgen05.mma
-// chain per hidden layer into TMEM -> ReLU/fp16 epilogue -> output layer on
-// CUDA cores (fp32).  Accuracy: fp16 operands / fp32 accumulate (north-star
-// 1e-2 relative bar); the exact evaluator (field.cu) remains available.
+// and _kernels.py:154-176 / model.py:178-198 (batched Phi evaluation, the
+// renderers' phi_eval_staged, _render_kernels.py:518-540).
+// Persistent CTAs (two per SM, 128 TMEM columns each) walk 128-sample tiles:
+// bit-exact fp32 hash-grid encode -> split-fp16 (hi + lo) feature tiles in
+// smem -> per hidden layer one tcgen05.mma chain (hi*hi into one TMEM
+// accumulator, lo*hi + hi*lo into a second, see tc.cuh) -> ReLU epilogue
+// re-splitting the activations -> output layer on CUDA cores (fp32).  The
+// split forward keeps outputs within the north-star 1e-2 relative bar even
+// where plain fp16 rounding flips ReLU masks; the exact evaluator
+// (field.cu) remains available as infer_mode "exact".
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -20,7 +23,7 @@ constexpr int IT_TILE = 128;
 
 struct InferShape {
     int m, n, nin, ninp, nn, nh, relu_out;
-    uint32_t o_w[8], o_wout, o_x, o_h[2], smem_bytes, t_alloc;
+    uint32_t o_w[8], o_wout, o_wlo[8], o_x, o_xlo, o_h, o_hlo, o_part, smem_bytes, t_alloc;
 };
 
 static int build_infer_shape(InferShape &s, int m, int n, int nn, int nh, int relu_out) {
@@ -38,26 +41,36 @@ static int build_infer_shape(InferShape &s, int m, int n, int nn, int nh, int re
         off += (bytes + 127) & ~127u;
         return r;
     };
+    // [0, o_x): the packed weight image (hi tiles, fp32 output row, lo tiles)
     for (int i = 0; i < nh; ++i) s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
     s.o_wout = take(4u * nn);
+    for (int i = 0; i < nh; ++i) s.o_wlo[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
     s.o_x = take(2u * IT_TILE * s.ninp);
-    s.o_h[0] = take(2u * IT_TILE * nn);
-    s.o_h[1] = take(2u * IT_TILE * nn);
-    s.smem_bytes = off + 4u * IT_TILE;  // + output partials
-    s.t_alloc = nn < 32 ? 32 : nn;
-    return s.smem_bytes <= 110 * 1024;
+    s.o_xlo = take(2u * IT_TILE * s.ninp);
+    // one activation buffer (+ lo): a layer's epilogue overwrites the operand
+    // its own MMA already consumed
+    s.o_h = take(2u * IT_TILE * nn);
+    s.o_hlo = take(2u * IT_TILE * nn);
+    s.o_part = take(4u * IT_TILE);
+    s.smem_bytes = off;
+    s.t_alloc = 2 * nn < 32 ? 32 : 2 * nn;
+    return s.smem_bytes <= 112 * 1024;
 }
 
-__device__ __forceinline__ void st_f16x16(uint8_t *tile, int row, int c, int w, const float *v, bool relu) {
+__device__ __forceinline__ void st_f16x16(uint8_t *tile, int row, int c, int w, const float *v) {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        float a[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) a[e] = relu ? fmaxf(v[q * 8 + e], 0.0f) : v[q * 8 + e];
+        const float *a = v + q * 8;
         uint4 pk = make_uint4(tc::pack_half2(a[0], a[1]), tc::pack_half2(a[2], a[3]), tc::pack_half2(a[4], a[5]),
                               tc::pack_half2(a[6], a[7]));
         *reinterpret_cast<uint4 *>(tile + tc::tile_off(row, c + q * 8, w)) = pk;
     }
+}
+
+__device__ __forceinline__ uint32_t slot32i(uint32_t vx, uint32_t vy, uint32_t vz, uint32_t r1, uint32_t mask,
+                                            bool dense) {
+    if (dense) return (vz * r1 + vy) * r1 + vx;
+    return (vx ^ (vy * 2654435761u) ^ (vz * 805459861u)) & mask;
 }
 
 template <int NF>
@@ -72,11 +85,10 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int NN = sh.nn, NINP = sh.ninp, NH = sh.nh, M = sh.m;
     {
-        // pre-packed fp16 weight tiles + fp32 output row (nvol_mlp_pack)
         const uint4 *src = reinterpret_cast<const uint4 *>(wimg);
         uint4 *dst = reinterpret_cast<uint4 *>(smem);
         for (int q = tid; q < (int)(sh.o_x / 16); q += IT_THREADS) dst[q] = __ldg(src + q);
-        for (int q = tid; q < IT_TILE * NINP / 8; q += IT_THREADS)
+        for (int q = tid; q < 2 * IT_TILE * NINP / 8; q += IT_THREADS)   // hi + lo feature tiles (padding stays 0)
             reinterpret_cast<uint4 *>(smem + sh.o_x)[q] = make_uint4(0, 0, 0, 0);
     }
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, sh.t_alloc);
@@ -87,14 +99,14 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    const uint32_t tmem = tmem_base_sh;
+    const uint32_t tmem = tmem_base_sh, tlo = tmem + NN;
     uint32_t phase = 0;
     const float *s_wout = reinterpret_cast<const float *>(smem + sh.o_wout);
-    float *s_part = reinterpret_cast<float *>(smem + sh.smem_bytes - 4 * IT_TILE);
+    float *s_part = reinterpret_cast<float *>(smem + sh.o_part);
     const uint32_t idesc = tc::make_idesc(128, NN, 0, 0);
     const int mh = (M + 1) / 2, l_lo = h * mh, l_hi = min(M, (h + 1) * mh);
     const int64_t ntiles = (b + IT_TILE - 1) / IT_TILE;
-    int c0 = NN >= 32 ? h * (NN >> 1) : 0, nc = NN >= 32 ? (NN >> 1) : (h == 0 ? NN : 0);
+    const int c0 = NN >= 32 ? h * (NN >> 1) : 0, nc = NN >= 32 ? (NN >> 1) : (h == 0 ? NN : 0);
 
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t i = tile * IT_TILE + s;
@@ -112,59 +124,86 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
                 z = coords[3 * i + 2];
             }
         }
-        uint8_t *sx = smem + sh.o_x;
+        uint8_t *sx = smem + sh.o_x, *sxl = smem + sh.o_xlo;
         for (int l = l_lo; l < l_hi; ++l) {
             const int32_t res = tab.res[l];
+            const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
+            const bool dense = tab.dense[l] != 0;
+            const float *tb = params + tab.offset[l];
             Cell<float> c = cell_of<float>(x, y, z, res);
+            const uint32_t cx = (uint32_t)c.cx, cy = (uint32_t)c.cy, cz = (uint32_t)c.cz;
             float acc[NF];
 #pragma unroll
             for (int f = 0; f < NF; ++f) acc[f] = 0.0f;
+            uint32_t sl[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                int64_t slot = vertex_slot(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), res,
-                                           tab.entries[l], tab.dense[l] != 0);
-                float w = corner_weight<float>(c, k);
-                const float *p = params + tab.offset[l] + slot * NF;
-                if constexpr (NF == 2) {
-                    float2 v = __ldg(reinterpret_cast<const float2 *>(p));
-                    acc[0] = xadd(acc[0], xmul(w, v.x));
-                    acc[1] = xadd(acc[1], xmul(w, v.y));
-                } else {
+            for (int k = 0; k < 8; ++k) sl[k] = slot32i(cx + (k & 1), cy + ((k >> 1) & 1), cz + ((k >> 2) & 1), r1, mask, dense);
+            if constexpr (NF == 2) {
+                float2 v[8];
 #pragma unroll
-                    for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(p + f)));
+                for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float2 *>(tb) + sl[k]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    float w = corner_weight<float>(c, k);
+                    acc[0] = xadd(acc[0], xmul(w, v[k].x));
+                    acc[1] = xadd(acc[1], xmul(w, v[k].y));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    float w = corner_weight<float>(c, k);
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(tb + (size_t)sl[k] * NF + f)));
                 }
             }
 #pragma unroll
-            for (int f = 0; f < NF; ++f)
-                *reinterpret_cast<__half *>(sx + tc::tile_off(s, l * NF + f, NINP)) = __float2half_rn(acc[f] * tc::kActScale);
+            for (int f = 0; f < NF; ++f) {
+                __half hi, lw;
+                tc::split_f16(valid ? acc[f] * tc::kActScale : 0.0f, hi, lw);
+                const uint32_t o = tc::tile_off(s, l * NF + f, NINP);
+                *reinterpret_cast<__half *>(sx + o) = hi;
+                *reinterpret_cast<__half *>(sxl + o) = lw;
+            }
         }
         tc::fence_proxy_async();
         __syncthreads();
         float outp = 0.0f;
         for (int li = 0; li < NH; ++li) {
             const int win = li == 0 ? NINP : NN;
-            const uint8_t *a_tile = li == 0 ? smem + sh.o_x : smem + sh.o_h[(li - 1) & 1];
             if (tid == 0) {
                 tc::fence_after();
-                uint32_t a0 = tc::smem_u32(a_tile), b0 = tc::smem_u32(smem + sh.o_w[li]);
-                for (int k = 0; k < win / 16; ++k)
-                    tc::mma_f16(tmem, tc::make_desc(a0 + k * 256, 128, (win / 8) * 128),
-                                tc::make_desc(b0 + k * 256, 128, (win / 8) * 128), idesc, k > 0);
+                const uint32_t ah = tc::smem_u32(smem + (li == 0 ? sh.o_x : sh.o_h));
+                const uint32_t al = tc::smem_u32(smem + (li == 0 ? sh.o_xlo : sh.o_hlo));
+                const uint32_t bh = tc::smem_u32(smem + sh.o_w[li]), bl = tc::smem_u32(smem + sh.o_wlo[li]);
+                const uint32_t sbo = (win / 8) * 128;
+                for (int k = 0; k < win / 16; ++k) {
+                    const uint64_t adh = tc::make_desc(ah + k * 256, 128, sbo), adl = tc::make_desc(al + k * 256, 128, sbo);
+                    const uint64_t bdh = tc::make_desc(bh + k * 256, 128, sbo), bdl = tc::make_desc(bl + k * 256, 128, sbo);
+                    tc::mma_f16(tmem, adh, bdh, idesc, k > 0);
+                    tc::mma_f16(tlo, adl, bdh, idesc, k > 0);
+                    tc::mma_f16(tlo, adh, bdl, idesc, 1);
+                }
                 tc::mma_commit(&mbar);
             }
             tc::mbar_wait(&mbar, phase);
             phase ^= 1;
             tc::fence_after();
-            uint8_t *dst = smem + sh.o_h[li & 1];
+            uint8_t *dst = smem + sh.o_h, *dstl = smem + sh.o_hlo;
             for (int c = c0; c < c0 + nc; c += 16) {   // values carry kActScale (see tc.cuh)
-                float v[16];
+                float v[16], vl[16];
                 tc::tmem_ld16(tmem + lane_base + c, v);
+                tc::tmem_ld16(tlo + lane_base + c, vl);
                 tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
                 if (li < NH - 1) {
-                    st_f16x16(dst, s, c, NN, v, true);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) vl[e] = (v[e] - __half2float(__float2half_rn(v[e]))) * tc::kLoScale;
+                    st_f16x16(dst, s, c, NN, v);
+                    st_f16x16(dstl, s, c, NN, vl);
                 } else {
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * fmaxf(v[e], 0.0f);
+                    for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * v[e];
                 }
             }
             tc::fence_before();
@@ -196,8 +235,10 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
         set_error("MLP shape not supported by the tcgen05 inference path");
         return NVOL_EINVAL;
     }
+    for (int l = 0; l < tab.n_levels; ++l)
+        NVOL_REQUIRE(tab.entries[l] < (1ll << 31), "level too large for the tcgen05 inference path");
     NVOL_REQUIRE(wimg, "tcgen05 inference needs an mlp_image scratch buffer (nvol_mlp_image_bytes)");
-    int st = pack_mlp_image(wflat, sh.nin, sh.ninp, nn, nh, sh.o_w, sh.o_wout, wimg, s, nullptr);
+    int st = pack_mlp_image(wflat, sh.nin, sh.ninp, nn, nh, sh.o_w, sh.o_wout, wimg, s, sh.o_wlo);
     if (st) return st;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -289,7 +289,7 @@ int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const 
 __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
     const uint8_t *__restrict__ xtiles, const float *__restrict__ targets, int64_t b, double inv_bglobal, float dscale,
     const TcShape sh, const uint8_t *__restrict__ wimg, double *__restrict__ loss_sum, float *__restrict__ dfeat,
-    float *__restrict__ partials) {
+    int64_t stride, float *__restrict__ partials) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_sh;
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
                         // feature-major dL/dfeat [NIN][B]: a warp stores 32 consecutive rows per column
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
-                            if (c + e < NIN) dfeat[(int64_t)(c + e) * b + row] = v[e];
+                            if (c + e < NIN) dfeat[(int64_t)(c + e) * stride + row] = v[e];
                     }
                 }
             }
@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
 template <int NF>
 __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__restrict__ coords,
                                                                 const float *__restrict__ dfeat, int64_t b,
+                                                                int64_t stride,
                                                                 const GridTables tab, int n_coarse, int coarse_floats,
                                                                 float *__restrict__ grads,
                                                                 float *__restrict__ partials) {
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
         Cell32 c = cell32(__ldg(coords + 3 * i), __ldg(coords + 3 * i + 1), __ldg(coords + 3 * i + 2), res);
         float d[NF];
 #pragma unroll
-        for (int f = 0; f < NF; ++f) d[f] = __ldg(dfeat + (int64_t)(l * NF + f) * b + i);
+        for (int f = 0; f < NF; ++f) d[f] = __ldg(dfeat + (int64_t)(l * NF + f) * stride + i);
         const bool coarse = l < n_coarse;
         float *gl = coarse ? acc_s + tab.offset[l] : grads + tab.offset[l];
         if constexpr (NF == 2) {
@@ -648,10 +649,16 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float *__res
 }
 
 // ============================================================================ host side
+// The batch is processed in `nchunks` row chunks on three streams so the
+// L2-bound encode / scatter kernels of one chunk overlap the tensor-core
+// MLP kernel of another (encode(c+1) || mlp(c) || scatter(c-1)); all of it
+// is ordinary stream fork/join, so it captures into the step's CUDA graph.
+constexpr int MAX_CHUNKS = 4;
+
 struct TcPlan {
     TcShape sh;
-    int grid_mlp, grid_sc, n_coarse, coarse_floats;
-    int64_t ntiles, off_x, off_dfeat, off_wpart, off_cpart, off_img, total;
+    int grid_mlp, grid_sc, n_coarse, coarse_floats, nchunks;
+    int64_t ntiles, chunk_tiles, off_x, off_dfeat, off_wpart, off_cpart, off_img, total;
 };
 
 static int num_sms() {
@@ -671,7 +678,12 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
         if (tab.entries[l] >= (1ll << 31)) return 0;
     const int sms = num_sms();
     p.ntiles = (b + TILE - 1) / TILE;
-    p.grid_mlp = (int)(p.ntiles < sms ? p.ntiles : sms);
+    // chunks of >= ~1.5 MLP tiles per SM: 2 chunks at B = 65,536
+    p.nchunks = (int)(p.ntiles / (sms + sms / 2));
+    p.nchunks = p.nchunks < 1 ? 1 : (p.nchunks > MAX_CHUNKS ? MAX_CHUNKS : p.nchunks);
+    p.chunk_tiles = (p.ntiles + p.nchunks - 1) / p.nchunks;
+    p.nchunks = (int)((p.ntiles + p.chunk_tiles - 1) / p.chunk_tiles);  // every chunk non-empty
+    p.grid_mlp = (int)(p.chunk_tiles < sms ? p.chunk_tiles : sms);
     p.grid_sc = sms;
     p.n_coarse = 0;
     p.coarse_floats = 0;
@@ -685,26 +697,47 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
     p.off_x = 0;
     p.off_dfeat = al(p.ntiles * TILE * p.sh.ninp * 4);  // hi + lo fp16 tiles
     p.off_wpart = p.off_dfeat + al(b * p.sh.nin * 4);
-    p.off_cpart = p.off_wpart + al((int64_t)p.grid_mlp * p.sh.w_floats * 4);
-    p.off_img = p.off_cpart + al((int64_t)p.grid_sc * p.coarse_floats * 4);
+    p.off_cpart = p.off_wpart + al((int64_t)MAX_CHUNKS * p.grid_mlp * p.sh.w_floats * 4);
+    p.off_img = p.off_cpart + al((int64_t)MAX_CHUNKS * p.grid_sc * p.coarse_floats * 4);
     p.total = p.off_img + al(p.sh.o_x) + 256;
     return 1;
 }
 
 int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
-    GridTables tab{};
-    tab.n_levels = m;
-    tab.n_feat = n;
-    // workspace size does not depend on the level tables beyond m, n and the
-    // coarse prefix, which is bounded by COARSE_BYTES
+    // upper bound over level tables: the coarse prefix is capped by COARSE_BYTES
     TcPlan p;
     if (!build_shape(p.sh, m, n, nn, nh, 1, 0)) return 0;
     const int sms = num_sms();
     int64_t ntiles = (b + TILE - 1) / TILE;
     int grid_mlp = (int)(ntiles < sms ? ntiles : sms);
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
-    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) + al((int64_t)grid_mlp * p.sh.w_floats * 4) +
-           al((int64_t)sms * (COARSE_BYTES / 4) * 4) + al(p.sh.o_x) + 256;
+    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) +
+           al((int64_t)MAX_CHUNKS * grid_mlp * p.sh.w_floats * 4) +
+           al((int64_t)MAX_CHUNKS * sms * (COARSE_BYTES / 4) * 4) + al(p.sh.o_x) + 256;
+}
+
+static cudaEvent_t g_stage_events[8];
+static int g_stage_events_n = 0;
+
+struct SideStreams {
+    cudaStream_t enc = nullptr, sc = nullptr;
+    cudaEvent_t fork, join_enc, join_sc, enc_done[MAX_CHUNKS], mlp_done[MAX_CHUNKS];
+};
+
+static SideStreams &side_streams() {
+    static SideStreams ss;
+    if (ss.enc == nullptr) {
+        cudaStreamCreateWithFlags(&ss.enc, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&ss.sc, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ss.join_enc, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ss.join_sc, cudaEventDisableTiming);
+        for (int c = 0; c < MAX_CHUNKS; ++c) {
+            cudaEventCreateWithFlags(&ss.enc_done[c], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ss.mlp_done[c], cudaEventDisableTiming);
+        }
+    }
+    return ss;
 }
 
 int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_t b_global, const float *params,
@@ -725,46 +758,107 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
     int64_t enc = 0;
     for (int l = 0; l < tab.n_levels; ++l) enc = max(enc, tab.offset[l] + tab.entries[l] * tab.n_feat);
     const int64_t woff = (enc + 3) & ~(int64_t)3;
-    const unsigned egrid = grid_for(b * tab.n_levels, 256);
-    switch (tab.n_feat) {
-        case 1: encode_tiles_kernel<1><<<egrid, 256, 0, s>>>(coords, b, params, tab, p.sh.ninp, xt); break;
-        case 2: encode_tiles_kernel<2><<<egrid, 256, 0, s>>>(coords, b, params, tab, p.sh.ninp, xt); break;
-        case 4: encode_tiles_kernel<4><<<egrid, 256, 0, s>>>(coords, b, params, tab, p.sh.ninp, xt); break;
-        default: encode_tiles_kernel<8><<<egrid, 256, 0, s>>>(coords, b, params, tab, p.sh.ninp, xt); break;
-    }
-    int st = check_launch("encode_tiles_kernel");
-    if (st) return st;
-    st = pack_mlp_image(params + woff, p.sh.nin, p.sh.ninp, nn, nh, p.sh.o_w, p.sh.o_wout, wimg, s, p.sh.o_wlo);
+    int st = pack_mlp_image(params + woff, p.sh.nin, p.sh.ninp, nn, nh, p.sh.o_w, p.sh.o_wout, wimg, s, p.sh.o_wlo);
     if (st) return st;
     cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh.smem_bytes);
-    const float dscale = exp2f(rintf(log2f((float)b_global)));  // ~B: L1 deltas become +-1 in fp16
-    mlp_tc_kernel<<<p.grid_mlp, TC_THREADS, p.sh.smem_bytes, s>>>(xt, targets, b, 1.0 / (double)b_global, dscale, p.sh,
-                                                                   wimg, loss_sum, dfeat, wpart);
-    st = check_launch("mlp_tc_kernel");
-    if (st) return st;
     const size_t csm = (size_t)p.coarse_floats * 4;
     switch (tab.n_feat) {
-#define LAUNCH_SC(NFV)                                                                                        \
-    case NFV:                                                                                                 \
-        cudaFuncSetAttribute(scatter_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);     \
-        scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, s>>>(coords, dfeat, b, tab, p.n_coarse, p.coarse_floats, \
-                                                              grads, cpart);                                  \
-        break;
-        LAUNCH_SC(1)
-        LAUNCH_SC(2)
-        LAUNCH_SC(4)
-        LAUNCH_SC(8)
-#undef LAUNCH_SC
+        case 1: cudaFuncSetAttribute(scatter_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm); break;
+        case 2: cudaFuncSetAttribute(scatter_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm); break;
+        case 4: cudaFuncSetAttribute(scatter_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm); break;
+        default: cudaFuncSetAttribute(scatter_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm); break;
     }
-    st = check_launch("scatter_kernel");
-    if (st) return st;
-    reduce_partials_kernel<<<grid_for(p.sh.w_floats, 32), 256, 0, s>>>(wpart, p.grid_mlp, p.sh.w_floats, grads + woff);
+    const float dscale = exp2f(rintf(log2f((float)b_global)));  // ~B: L1 deltas become +-1 in fp16
+    // profiling: one chunk, events at the stage boundaries on the caller's stream
+    cudaEvent_t *pev = g_stage_events;
+    const bool prof = g_stage_events_n >= 4;
+    const int nc = prof ? 1 : p.nchunks;
+    if (prof) cudaEventRecord(pev[0], s);
+    SideStreams &ss = side_streams();
+    cudaStream_t se = nc > 1 ? ss.enc : s, sc = nc > 1 ? ss.sc : s;
+    if (nc > 1) {
+        cudaEventRecord(ss.fork, s);
+        cudaStreamWaitEvent(ss.enc, ss.fork, 0);
+        cudaStreamWaitEvent(ss.sc, ss.fork, 0);
+    }
+    const int64_t tile_bytes = 2 * TILE * p.sh.ninp * 2;
+    for (int c = 0; c < nc; ++c) {
+        const int64_t t0 = c * p.chunk_tiles;
+        const int64_t r0 = t0 * TILE;
+        if (r0 >= b) break;
+        const int64_t nb = (r0 + p.chunk_tiles * TILE < b ? p.chunk_tiles * TILE : b - r0);
+        const unsigned egrid = grid_for(nb * tab.n_levels, 256);
+        uint8_t *xtc = xt + t0 * tile_bytes;
+        const float *cc = coords + 3 * r0;
+        switch (tab.n_feat) {
+            case 1: encode_tiles_kernel<1><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+            case 2: encode_tiles_kernel<2><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+            case 4: encode_tiles_kernel<4><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+            default: encode_tiles_kernel<8><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+        }
+        st = check_launch("encode_tiles_kernel");
+        if (st) return st;
+        if (nc > 1) {
+            cudaEventRecord(ss.enc_done[c], se);
+            cudaStreamWaitEvent(s, ss.enc_done[c], 0);
+        }
+        if (prof) cudaEventRecord(pev[1], s);
+        const int64_t ct = (nb + TILE - 1) / TILE;
+        const int gm = (int)(ct < p.grid_mlp ? ct : p.grid_mlp);
+        float *wp = wpart + (int64_t)c * p.grid_mlp * p.sh.w_floats;
+        mlp_tc_kernel<<<gm, TC_THREADS, p.sh.smem_bytes, s>>>(xtc, targets + r0, nb, 1.0 / (double)b_global, dscale,
+                                                              p.sh, wimg, loss_sum, dfeat + r0, b, wp);
+        st = check_launch("mlp_tc_kernel");
+        if (st) return st;
+        if (gm < p.grid_mlp)  // unused partial slots of a short chunk must sum to zero
+            cudaMemsetAsync(wp + (int64_t)gm * p.sh.w_floats, 0, (size_t)(p.grid_mlp - gm) * p.sh.w_floats * 4, s);
+        if (nc > 1) {
+            cudaEventRecord(ss.mlp_done[c], s);
+            cudaStreamWaitEvent(sc, ss.mlp_done[c], 0);
+        }
+        if (prof) cudaEventRecord(pev[2], s);
+        float *cp = cpart + (int64_t)c * p.grid_sc * p.coarse_floats;
+        switch (tab.n_feat) {
+#define LAUNCH_SC(NFV)                                                                                             \
+    case NFV:                                                                                                      \
+        scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, sc>>>(cc, dfeat + r0, nb, b, tab, p.n_coarse,            \
+                                                                p.coarse_floats, grads, cp);                       \
+        break;
+            LAUNCH_SC(1)
+            LAUNCH_SC(2)
+            LAUNCH_SC(4)
+            LAUNCH_SC(8)
+#undef LAUNCH_SC
+        }
+        st = check_launch("scatter_kernel");
+        if (st) return st;
+        if (prof) cudaEventRecord(pev[3], s);
+    }
+    if (nc > 1) {
+        cudaEventRecord(ss.join_enc, ss.enc);
+        cudaEventRecord(ss.join_sc, ss.sc);
+        cudaStreamWaitEvent(s, ss.join_enc, 0);
+        cudaStreamWaitEvent(s, ss.join_sc, 0);
+    }
+    reduce_partials_kernel<<<grid_for(p.sh.w_floats, 32), 256, 0, s>>>(wpart, nc * p.grid_mlp, p.sh.w_floats,
+                                                                       grads + woff);
     if (p.coarse_floats > 0)
-        reduce_partials_kernel<<<grid_for(p.coarse_floats, 32), 256, 0, s>>>(cpart, p.grid_sc, p.coarse_floats, grads);
+        reduce_partials_kernel<<<grid_for(p.coarse_floats, 32), 256, 0, s>>>(cpart, nc * p.grid_sc, p.coarse_floats,
+                                                                             grads);
     return check_launch("reduce_partials");
 }
 
 }  // namespace nvol
+
+// Profiling hook: with >= 4 events set, nvol_train_fwd_bwd (mode 1) runs as a
+// single chunk on the caller's stream and records events[0..3] before encode,
+// after encode, after pack+MLP and after scatter.  n = 0 disables.
+extern "C" int nvol_set_stage_events(void *const *events, int32_t n) {
+    n = n > 8 ? 8 : (n < 0 ? 0 : n);
+    for (int i = 0; i < n; ++i) nvol::g_stage_events[i] = reinterpret_cast<cudaEvent_t>(events[i]);
+    nvol::g_stage_events_n = n;
+    return NVOL_OK;
+}
 
 extern "C" int nvol_has_tcgen05(int device) {
     int major = 0, minor = 0;

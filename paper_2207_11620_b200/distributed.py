@@ -1,0 +1,77 @@
+"""Data-parallel training: sample sharding + one gradient all-reduce per step.
+
+The reference is single-process; the north star adds data
+parallelism by sample sharding.  Rank r of G processes the rows
+[r*B/G, (r+1)*B/G) of the reference's global batch — the PCG64 stream
+offset of those rows is computed exactly, so the union of the shards IS the
+single-process batch — scales its loss gradient by 1/B_global
+(network.py:108), and all-reduces (sum) the flat gradient buffer plus the loss
+sum.  Every rank then applies the identical Adam update, so parameters stay
+bit-identical across ranks without a parameter broadcast.  On GPUs the
+collective is NCCL over NVLink/NVSwitch and is captured inside the step's
+CUDA graph (trainer.StepPipeline); the host logic here is device-agnostic and
+is exercised with gloo on CPU in the tests.
+"""
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+from .errors import ConfigError
+
+
+def shard_rows(batch_size: int, rank: int, world: int):
+    """(first row, rows) of this rank's shard of the global batch."""
+    if world < 1 or not 0 <= rank < world:
+        raise ConfigError(f"bad rank {rank} of world {world}")
+    if batch_size % world:
+        raise ConfigError(f"batch size {batch_size} is not divisible by world size {world}")
+    b = batch_size // world
+    return rank * b, b
+
+
+def shard_u32_offset(u32_base: int, step: int, batch_size: int, row0: int) -> int:
+    """u32 index of the first coordinate draw of rows [row0, ...) at `step`
+    (sampler.py:54-55: each step draws 3*B float32 from the stream)."""
+    return int(u32_base) + 3 * int(batch_size) * int(step) + 3 * int(row0)
+
+
+def allreduce_grads(flat_grads: torch.Tensor, loss_acc: torch.Tensor | None = None, group=None) -> None:
+    """Sum the flat gradient buffer (and the loss accumulator) over ranks."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    dist.all_reduce(flat_grads, op=dist.ReduceOp.SUM, group=group)
+    if loss_acc is not None:
+        dist.all_reduce(loss_acc, op=dist.ReduceOp.SUM, group=group)
+
+
+def init_from_env(backend: str = "nccl"):
+    """torchrun-style init (RANK / WORLD_SIZE / LOCAL_RANK / MASTER_*); returns (rank, world, local_rank)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        kw = {}
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            kw["device_id"] = torch.device("cuda", local)
+        dist.init_process_group(backend, **kw)
+    return rank, world, local
+
+
+class DataParallelTrainer:
+    """Device-resident data-parallel training of one NeuralModel per rank."""
+
+    def __init__(self, model, sampler, capacity: int, group=None):
+        from .trainer import StepPipeline
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.pipeline = StepPipeline(model, sampler, capacity, rank=rank, world=world, group=group)
+
+    def step(self, n: int = 1) -> None:
+        self.pipeline.step(n)
+
+    def finish(self):
+        return self.pipeline.finish()

@@ -80,11 +80,11 @@ class StepPipeline:
                  group=None, use_graph: bool = True):
         if not model._use_kernels():
             raise ConfigError("the device pipeline needs a float32 grid model")
+        from .distributed import shard_rows
         B = model.batch_size
-        if B % world:
-            raise ConfigError(f"batch size {B} is not divisible by world size {world}")
+        row0, b = shard_rows(B, rank, world)
         self.model, self.sampler = model, sampler
-        self.B, self.b, self.row0 = B, B // world, rank * (B // world)
+        self.B, self.b, self.row0 = B, b, row0
         self.world, self.group = world, group
         dev = model.flat_params.device
         self.coords = torch.empty((self.b, 3), dtype=torch.float32, device=dev)
@@ -117,9 +117,8 @@ class StepPipeline:
                   _lib.stream())
         m.fwd_bwd_device(self.coords, self.targets, self.acc, b_global=self.B)
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(m.flat_grads, group=self.group)
-            dist.all_reduce(self.acc, group=self.group)
+            from .distributed import allreduce_grads
+            allreduce_grads(m.flat_grads, self.acc, self.group)
         _lib.call("nvol_loss_record", _lib.ptr(self.acc), _lib.ptr(self.losses), _lib.ptr(self.counter), self.t0,
                   self.capacity, 1.0 / self.B, _lib.stream())
         _lib.call("nvol_adam_flat_dev", _lib.ptr(m.flat_params), _lib.ptr(m.flat_grads), _lib.ptr(m.flat_m),
@@ -128,7 +127,16 @@ class StepPipeline:
 
     def launches_per_step(self) -> int:
         """Kernels of one step from this library (for the bench's gpu_launches)."""
-        return 1 + (5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 if self.model.train_mode == 0 else 1) + 2
+        if self.model.train_mode == 0:
+            return 1 + 5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 + 2
+        # sample, pack image, nchunks x (encode, MLP, scatter), 2 partial reduces, loss record, Adam
+        # (chunk plan of train_tc.cu make_plan)
+        sms = torch.cuda.get_device_properties(self.model.flat_params.device).multi_processor_count
+        ntiles = (self.b + 127) // 128
+        nc = min(max(ntiles // (sms + sms // 2), 1), 4)
+        ct = (ntiles + nc - 1) // nc
+        nc = (ntiles + ct - 1) // ct
+        return 1 + 1 + 3 * nc + 2 + 1 + 1
 
     def step(self, n: int = 1) -> None:
         """Enqueue n steps (no host synchronisation)."""

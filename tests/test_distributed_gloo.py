@@ -1,0 +1,90 @@
+"""Data-parallel host logic on CPU with gloo (world_size 2).
+
+Each rank builds its shard of the reference batch with the package's
+sharding / stream-offset functions, computes its shard's gradients with the
+oracle (the reference's algorithm; gradients scaled by 1/B_global), and
+all-reduces them with the package's `allreduce_grads`.  The reduced
+gradients and loss must equal the single-process full-batch step, and the
+Adam-updated parameters must be identical on both ranks.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+CFG = {"encoding": {"otype": "HashGrid", "n_levels": 4, "n_features_per_level": 2,
+                    "log2_hashmap_size": 12, "base_resolution": 4},
+       "network": {"n_neurons": 16, "n_hidden_layers": 2}, "batch_size": 2048}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _shard_grads(rank, world, step):
+    import nvol_oracle as orc
+    from paper_2207_11620_b200.distributed import shard_rows, shard_u32_offset
+    model = orc.OracleModel(CFG, seed=0)
+    B = model.batch_size
+    row0, b = shard_rows(B, rank, world)
+    norm = orc.rasterize("mlobb", (16, 16, 16))
+    coords = orc.pcg64_random_f32(1, shard_u32_offset(0, step, B, row0), 3 * b).reshape(b, 3)
+    targets = orc.trilinear(norm, coords, clip=True)
+    feats, idx, w = model.encode_batch(coords)
+    pred, acts = orc.mlp_forward(feats, model.weights)
+    diff = pred.astype(np.float64) - targets.astype(np.float64)
+    dl = (np.sign(diff) / B).astype(np.float32)           # 1 / B_global (network.py:108)
+    dfeat = orc.mlp_backward(acts, model.weights, model.grads, dl)
+    orc.grid_encode_bwd(np.ascontiguousarray(dfeat, np.float32), idx, w, 2, model.param_grads)
+    flat = np.concatenate([model.param_grads] + [g.ravel() for g in model.grads])
+    return model, flat, float(np.abs(diff).sum())
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__)))
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    from paper_2207_11620_b200.distributed import allreduce_grads
+    model, flat, lsum = _shard_grads(rank, world, step=3)
+    g = torch.from_numpy(flat.copy())
+    loss = torch.tensor([lsum], dtype=torch.float64)
+    allreduce_grads(g, loss)
+    out[rank] = (g.numpy().copy(), float(loss.item()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_dp_gloo_matches_single_process(oracle):
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    model, full, lsum = _shard_grads(0, 1, step=3)
+    for r in range(world):
+        g, l = out[r]
+        # float sums in a different order: tolerance at fp32 rounding
+        np.testing.assert_allclose(g, full, rtol=1e-5, atol=1e-9)
+        assert l == pytest.approx(lsum, rel=1e-12)
+    np.testing.assert_array_equal(out[0][0], out[1][0])   # identical on every rank -> identical Adam
+
+
+def test_shard_rows_validation():
+    from paper_2207_11620_b200.distributed import shard_rows
+    from paper_2207_11620_b200.errors import ConfigError
+    assert shard_rows(65536, 3, 8) == (24576, 8192)
+    with pytest.raises(ConfigError):
+        shard_rows(1000, 0, 3)
+    with pytest.raises(ConfigError):
+        shard_rows(1024, 2, 2)
