@@ -250,7 +250,7 @@ def run_ours(args):
     if args.mode == 1:
         st = _event_ms(torch, stages_fn, nev=5)
         kernels.update({"encode_tiles_kernel": float(st[0]), "mlp_tc_kernel": float(st[1] - st[0]),
-                        "scatter_kernel": float(st[2] - st[1]), "reduce_partials x2": float(st[3] - st[2])})
+                        "scatter_kernel": float(st[2] - st[1])})
     n_flat = model.flat_size
     adam_bytes = 32 * n_flat
     gather_bytes = B * 16 * 8 * 2 * 4

@@ -102,6 +102,41 @@ __device__ __forceinline__ T corner_weight(const Cell<T> &c, int corner) {
     return w;
 }
 
+// ----------------------------------------------------------------------------- L2 residency hints
+// The flat gradient (48.7 MB at cfg2) is kept L2-resident across a training
+// step: Adam zeroes it with evict_last stores and the encoder-backward REDs
+// carry the same policy, so the scatter's random read-modify-writes hit L2
+// while Adam's p/m/v stream through with evict_first.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void red_add(float *a, float v, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void red_add2(float *a, float x, float y, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(a), "f"(x), "f"(y), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void red_add4(float *a, float4 v, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ float4 ld4_hint(const float4 *a, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st4_hint(float4 *a, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w), "l"(pol)
+                 : "memory");
+}
+
 // ----------------------------------------------------------------------------- PCG64
 // numpy.random.PCG64 (numpy 2.3.5): 128-bit LCG stepped before output, XSL-RR.
 struct U128 {

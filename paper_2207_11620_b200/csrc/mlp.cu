@@ -209,15 +209,28 @@ __global__ void __launch_bounds__(256) adam_flat_kernel(
     bool bad = false;
     float4 *p4 = reinterpret_cast<float4 *>(p), *g4 = reinterpret_cast<float4 *>(g);
     float4 *m4 = reinterpret_cast<float4 *>(m), *v4 = reinterpret_cast<float4 *>(v);
+#ifndef NVOL_ADAM_P_KEEP
+#define NVOL_ADAM_P_KEEP 0
+#endif
+    const uint64_t keep = l2_evict_last();
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
-        float4 P = __ldcs(p4 + j), G = __ldcs(g4 + j), M = __ldcs(m4 + j), V = __ldcs(v4 + j);
+#if NVOL_ADAM_P_KEEP
+        float4 P = ld4_hint(p4 + j, keep);
+#else
+        float4 P = __ldcs(p4 + j);
+#endif
+        float4 G = ld4_hint(g4 + j, keep), M = __ldcs(m4 + j), V = __ldcs(v4 + j);
         bad |= isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w);
         adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
         adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
         adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
         adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+#if NVOL_ADAM_P_KEEP
+        st4_hint(p4 + j, P, keep);
+#else
         __stcs(p4 + j, P);
-        __stcs(g4 + j, G);
+#endif
+        st4_hint(g4 + j, G, keep);  // the zeroed gradient stays in L2 for the next scatter
         __stcs(m4 + j, M);
         __stcs(v4 + j, V);
     }

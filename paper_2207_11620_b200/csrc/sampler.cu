@@ -7,45 +7,90 @@
 
 namespace nvol {
 
-constexpr int SAMPLES_PER_THREAD = 4;
+// PCG64 jump table: entry i advances the LCG by 2^i steps (state -> mult[i] *
+// state + plus[i]).  Built on the host once per stream increment and passed
+// by value, so every thread jumps straight to its own draws with popcount(
+// delta) 128-bit multiply-adds (no serial per-block jump, no per-step state).
+struct PcgJump {
+    U128 mult[64], plus[64];
+};
 
-// Each thread owns SAMPLES_PER_THREAD consecutive rows = 12 consecutive u32
-// draws of the stream; it jumps there once (O(log n) LCG advance) and then
-// steps sequentially.  The volume read is the bit-exact trilinear of
-// volume.py:148-164, clamped to [0,1] as sampler.py:74.
-__global__ void __launch_bounds__(256) sample_incore_kernel(U128 s0, U128 inc, uint64_t u32_base,
+static PcgJump make_jump(U128 inc) {
+    typedef unsigned __int128 u128;
+    u128 cm = ((u128)0x2360ED051FC65DA4ull << 64) | (u128)0x4385DF649FCCF645ull;
+    u128 cp = ((u128)inc.hi << 64) | (u128)inc.lo;
+    PcgJump j;
+    for (int i = 0; i < 64; ++i) {
+        j.mult[i] = U128{(uint64_t)(cm >> 64), (uint64_t)cm};
+        j.plus[i] = U128{(uint64_t)(cp >> 64), (uint64_t)cp};
+        cp = (cm + 1) * cp;
+        cm = cm * cm;
+    }
+    return j;
+}
+
+// One thread per row: the row's three u32 draws are u32 indices g0..g0+2 of
+// the stream (sample i, axis a -> 3i+a); they live in u64 outputs g0>>1 and
+// (g0+2)>>1.  The GT read is the bit-exact trilinear of volume.py:148-164,
+// clamped to [0,1] as sampler.py:74.
+__global__ void __launch_bounds__(256) sample_incore_kernel(U128 s0, U128 inc, const PcgJump jump, uint64_t u32_base,
                                                             const int64_t *__restrict__ step_counter,
                                                             int64_t counter0, int64_t b_global, int64_t row0,
                                                             int64_t b,
                                                             const float *__restrict__ vol, int64_t dx,
                                                             int64_t dy, int64_t dz, float *__restrict__ coords,
                                                             float *__restrict__ targets) {
-    // One long jump per block (thread 0), then short per-thread jumps.
-    __shared__ U128 blk_state;
-    const int64_t blk_r0 = (int64_t)blockIdx.x * blockDim.x * SAMPLES_PER_THREAD;
+    __shared__ U128 sm_mult[64], sm_plus[64];
+    if (threadIdx.x < 64) {
+        sm_mult[threadIdx.x] = jump.mult[threadIdx.x];
+        sm_plus[threadIdx.x] = jump.plus[threadIdx.x];
+    }
+    __syncthreads();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= b) return;
     uint64_t base = u32_base;
     if (step_counter)
         base += (uint64_t)(*step_counter - counter0) * 3ull * (uint64_t)b_global + 3ull * (uint64_t)row0;
-    const uint64_t g_blk = base + 3ull * (uint64_t)blk_r0;   // u32 index of the block's first draw
-    if (threadIdx.x == 0) blk_state = pcg_advance(s0, inc, g_blk >> 1);
-    __syncthreads();
-    int64_t r0 = blk_r0 + (int64_t)threadIdx.x * SAMPLES_PER_THREAD;
-    if (r0 >= b) return;
-    const uint64_t g0 = g_blk + 3ull * (uint64_t)threadIdx.x * SAMPLES_PER_THREAD;
-    PcgF32Stream rs;
-    rs.init(blk_state, inc, g0 - ((g_blk >> 1) << 1));  // stream relative to the block state
-    rs.g = g0;
-#pragma unroll
-    for (int q = 0; q < SAMPLES_PER_THREAD; ++q) {
-        int64_t r = r0 + q;
-        if (r >= b) break;
-        float x = rs.next(), y = rs.next(), z = rs.next();
-        coords[3 * r] = x;
-        coords[3 * r + 1] = y;
-        coords[3 * r + 2] = z;
-        float t = trilinear_at(vol, dx, dy, dz, x, y, z);
-        targets[r] = fminf(fmaxf(t, 0.0f), 1.0f);
+    const uint64_t g0 = base + 3ull * (uint64_t)r;
+    // state after (g0 >> 1) steps
+    U128 st = s0;
+    for (uint64_t d = g0 >> 1; d; d &= d - 1) {
+        const int i = __ffsll((long long)d) - 1;
+        st = u128_add(u128_mul(sm_mult[i], st), sm_plus[i]);
     }
+    const U128 m = pcg_mult();
+    st = u128_add(u128_mul(st, m), inc);
+    const uint64_t w0 = pcg_output(st);
+    st = u128_add(u128_mul(st, m), inc);
+    const uint64_t w1 = pcg_output(st);
+    uint32_t u[3];
+    if ((g0 & 1) == 0) {
+        u[0] = (uint32_t)w0;
+        u[1] = (uint32_t)(w0 >> 32);
+        u[2] = (uint32_t)w1;
+    } else {
+        u[0] = (uint32_t)(w0 >> 32);
+        u[1] = (uint32_t)w1;
+        u[2] = (uint32_t)(w1 >> 32);
+    }
+    const float x = u32_to_f32(u[0]), y = u32_to_f32(u[1]), z = u32_to_f32(u[2]);
+    coords[3 * r] = x;
+    coords[3 * r + 1] = y;
+    coords[3 * r + 2] = z;
+    const float t = trilinear_at(vol, dx, dy, dz, x, y, z);
+    targets[r] = fminf(fmaxf(t, 0.0f), 1.0f);
+}
+
+static const PcgJump &jump_for(U128 inc) {
+    static PcgJump cached;
+    static U128 cached_inc{0, 0};
+    static bool have = false;
+    if (!have || cached_inc.hi != inc.hi || cached_inc.lo != inc.lo) {
+        cached = make_jump(inc);
+        cached_inc = inc;
+        have = true;
+    }
+    return cached;
 }
 
 __global__ void trilinear_kernel(const float *__restrict__ vol, int64_t dx, int64_t dy, int64_t dz,
@@ -136,9 +181,9 @@ int nvol_sample_incore(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, ui
     NVOL_REQUIRE(b >= 1, "batch size must be >= 1");
     NVOL_REQUIRE(volume && coords && targets, "null pointer");
     NVOL_REQUIRE(dx >= 1 && dy >= 1 && dz >= 1, "bad volume dims");
-    int64_t threads = (b + SAMPLES_PER_THREAD - 1) / SAMPLES_PER_THREAD;
-    sample_incore_kernel<<<grid_for(threads, 256), 256, 0, as_stream(stream)>>>(
-        U128{state_hi, state_lo}, U128{inc_hi, inc_lo}, u32_offset, nullptr, 0, 0, 0, b, volume, dx, dy, dz,
+    const U128 inc{inc_hi, inc_lo};
+    sample_incore_kernel<<<grid_for(b, 256), 256, 0, as_stream(stream)>>>(
+        U128{state_hi, state_lo}, inc, jump_for(inc), u32_offset, nullptr, 0, 0, 0, b, volume, dx, dy, dz,
         coords, targets);
     return check_launch("sample_incore");
 }
@@ -150,9 +195,9 @@ int nvol_sample_incore_dev(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi
                            void *stream) {
     NVOL_REQUIRE(b >= 1 && step_counter, "bad arguments");
     NVOL_REQUIRE(volume && coords && targets, "null pointer");
-    int64_t threads = (b + SAMPLES_PER_THREAD - 1) / SAMPLES_PER_THREAD;
-    sample_incore_kernel<<<grid_for(threads, 256), 256, 0, as_stream(stream)>>>(
-        U128{state_hi, state_lo}, U128{inc_hi, inc_lo}, u32_base, step_counter, counter0, b_global, row0, b, volume,
+    const U128 inc{inc_hi, inc_lo};
+    sample_incore_kernel<<<grid_for(b, 256), 256, 0, as_stream(stream)>>>(
+        U128{state_hi, state_lo}, inc, jump_for(inc), u32_base, step_counter, counter0, b_global, row0, b, volume,
         dx, dy, dz, coords, targets);
     return check_launch("sample_incore_dev");
 }

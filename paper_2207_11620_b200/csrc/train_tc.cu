@@ -13,35 +13,51 @@
 //     CUDA cores (network.py:96-114); backward (network.py:76-93): per layer
 //     dW_j += delta^T H_j (accumulated in TMEM across all tiles of the CTA)
 //     and dX = delta W_j masked by the stored activations.  dL/dfeat leaves
-//     as fp32; dW leaves once per CTA as fp32 partials.
+//     as fp32; dW leaves TMEM once per CTA as fp32 vector REDs.
 //  3. scatter_kernel — encoder backward (_kernels.py:82-92): corners
 //     recomputed from the coordinates; the small dense coarse levels
 //     (contended by every sample) accumulate in shared memory and leave as
-//     per-CTA partials, the fine levels scatter with float2 REDs.
-// Partials are summed in fixed CTA order (deterministic MLP and coarse-level
-// gradients).
+//     one float4 RED per entry quad per CTA, the fine levels scatter with
+//     float2/float4 REDs.  (Float atomics make the fast path's gradient sums
+//     order-dependent; encoding.set_deterministic selects the sort-based
+//     bit-exact scatter of the API path.)
 //
 // Accuracy contract (north star): fp16 operands / fp32 accumulation, MLP
 // outputs and gradients within 1e-2 relative of the fp32 reference.
 #include <cuda_fp16.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tc.cuh"
 
 namespace nvol {
 
-constexpr int TC_THREADS = 256;
 constexpr int TILE = 128;
 constexpr int MAX_NH = 8;
+// MLP kernel: two 128-sample tiles in flight per CTA ("slots"), each with 8
+// epilogue warps (2 per TMEM lane quarter, one column half each), plus one
+// MMA-issuer warp that round-robins the slots' layer phases.
+constexpr int PP_EPI_WARPS = 16;
+#ifndef NVOL_FWD_WLO
+#define NVOL_FWD_WLO 1  // split forward includes the hi(act) x lo(weight) product
+#endif
+constexpr int PP_THREADS = (PP_EPI_WARPS + 1) * 32;
 constexpr int SC_THREADS = 1024;
 constexpr uint32_t COARSE_BYTES = 48 * 1024;
 
 struct TcShape {
-    int m, n, nin, ninp, nn, nh;
+    int m, n, nin, ninp, nn, nh, wbuf;
     int relu_out, loss_kind;
-    uint32_t o_w[MAX_NH], o_wout, o_wlo[MAX_NH], o_x, o_xlo, o_h[MAX_NH + 1], o_hlo[2], o_d[2], o_dout, o_misc,
-        smem_bytes;
-    uint32_t t_f, t_flo, t_g, t_dw[MAX_NH], t_dwout, t_alloc;
+    // weights: fp16 hi / lo core-matrix tiles + fp32 output row
+    uint32_t o_w[MAX_NH], o_wout, o_wlo[MAX_NH];
+    // per slot t: o_d[t] (X hi during the forward, then the fp16 delta tile),
+    // o_hlo[t] (X lo, then activation lo parts, h_NH, then the X hi reload),
+    // o_h[t][i] (hidden activations h_1..h_{nh-1}, fp16 hi)
+    uint32_t o_d[2], o_hlo[2], o_h[2][MAX_NH], o_part, smem_bytes, xhalf;
+    // TMEM: per slot [forward acc | forward lo acc] (backward dX aliases the
+    // first), then the dW_0..dW_{nh-1} accumulators shared by both slots
+    uint32_t t_acc[2], t_dw[MAX_NH], t_alloc;
     int64_t w_floats;
 };
 
@@ -52,11 +68,12 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
     s.ninp = (s.nin + 15) & ~15;
     s.nn = nn;
     s.nh = nh;
+    s.wbuf = max(nn, s.ninp);
     s.relu_out = relu_out;
     s.loss_kind = loss_kind;
     if (nh < 1 || nh > MAX_NH) return 0;
-    if (!(nn == 16 || nn == 32 || nn == 64 || nn == 128)) return 0;
-    if (s.ninp > 128) return 0;
+    if (!(nn == 16 || nn == 32 || nn == 64)) return 0;
+    if (s.ninp > 2 * nn || s.ninp > 128) return 0;
     uint32_t off = 0;
     auto take = [&](uint32_t bytes) {
         uint32_t r = off;
@@ -66,37 +83,33 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
     for (int i = 0; i < nh; ++i) s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
     s.o_wout = take(4u * nn);
     for (int i = 0; i < nh; ++i) s.o_wlo[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
-    s.o_x = take(2u * TILE * s.ninp);      // [o_x, o_x + 2 tiles): hi then lo feature tile
-    s.o_xlo = take(2u * TILE * s.ninp);
-    s.o_h[0] = s.o_x;
-    for (int i = 1; i <= nh; ++i) s.o_h[i] = take(2u * TILE * nn);
-    s.o_hlo[0] = take(2u * TILE * nn);
-    s.o_hlo[1] = take(2u * TILE * nn);
-    s.o_d[0] = take(2u * TILE * nn);
-    s.o_d[1] = take(2u * TILE * nn);
-    s.o_dout = take(2048 + 256);
-    s.o_misc = take(4u * TILE * 4 + 64);
-    take(4096);  // slack: padded-M operand rows read past the last tile (values unused)
+    for (int t = 0; t < 2; ++t) {
+        s.o_d[t] = take(2u * TILE * s.wbuf);
+        s.o_hlo[t] = take(2u * TILE * s.wbuf);
+        s.o_h[t][0] = 0;
+        for (int i = 1; i < nh; ++i) s.o_h[t][i] = take(2u * TILE * nn);
+    }
+    s.o_part = take(4u * 2 * 2 * TILE);
+    take(4096);  // slack: the dW MMA reads M = 128 delta "rows" past an nn-wide tile (values unused)
     s.smem_bytes = off;
+    s.xhalf = 2u * TILE * s.ninp;
     uint32_t col = 0;
-    s.t_f = col;
-    col += nn;
-    s.t_flo = col;  // forward lo-product accumulator (split-fp16 forward, see tc.cuh)
-    col += nn;
-    s.t_g = col;
-    col += (uint32_t)max(s.ninp, nn);
+    s.t_acc[0] = col;
+    col += 2 * nn;
+    s.t_acc[1] = col;
+    col += 2 * nn;
     for (int i = 0; i < nh; ++i) {
         s.t_dw[i] = col;
         col += (i == 0) ? s.ninp : nn;
     }
-    s.t_dwout = col;
-    col += nn;
     if (col > 512) return 0;
     uint32_t a = 32;
     while (a < col) a <<= 1;
     s.t_alloc = a;
     s.w_floats = (int64_t)nn * s.nin + (int64_t)(nh - 1) * nn * nn + nn;
-    return s.smem_bytes <= 227 * 1024;
+    // the prologue stages the fp32 weights over the slot buffers
+    if ((int64_t)s.o_part - (int64_t)s.o_d[0] < s.w_floats * 4) return 0;
+    return s.smem_bytes <= 227 * 1024 - 1024;
 }
 
 // Hash-grid levels fit 32-bit slot arithmetic (entries <= 2^24 for hashed
@@ -208,14 +221,21 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
 }
 
 // ============================================================================ 2. MLP
-__device__ __forceinline__ void half_cols(int w, int h, int &c0, int &nc) {
-    if (w >= 32) {
-        c0 = h * (w >> 1);
-        nc = w >> 1;
-    } else {
-        c0 = 0;
-        nc = h == 0 ? w : 0;
-    }
+// Columns [c0, c0 + nc) of a w-wide accumulator handled by column group h of
+// ng (16-column TMEM loads; groups past the width get nc = 0).
+__device__ __forceinline__ void group_cols(int w, int h, int ng, int &c0, int &nc) {
+    const int chunks = w >> 4, per = (chunks + ng - 1) / ng;
+    const int k0 = h * per, k1 = min(chunks, k0 + per);
+    c0 = k0 * 16;
+    nc = k1 > k0 ? (k1 - k0) * 16 : 0;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ void store_row_f16(uint8_t *tile, int row, int c, int w, const float *v16, bool relu) {
@@ -286,125 +306,276 @@ int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const 
     return check_launch("pack_mlp_image");
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
+#ifdef NVOL_TIMELINE
+__device__ unsigned long long g_tl[4096];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL(slot, val)                                              \
+    do {                                                           \
+        if (blockIdx.x == 0) g_tl[(slot) & 4095] = (val);          \
+    } while (0)
+#else
+#define TL(slot, val) \
+    do {              \
+    } while (0)
+#endif
+
+// Forward (network.py:61-74), L1/L2 loss gradient (network.py:96-114) and
+// backward (network.py:76-93) of 128-sample tiles, two tiles in flight per
+// CTA so one slot's epilogue overlaps the other slot's tensor-core phase.
+__global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
     const uint8_t *__restrict__ xtiles, const float *__restrict__ targets, int64_t b, double inv_bglobal, float dscale,
-    const TcShape sh, const uint8_t *__restrict__ wimg, double *__restrict__ loss_sum, float *__restrict__ dfeat,
-    int64_t stride, float *__restrict__ partials) {
+    const TcShape sh, const float *__restrict__ wflat, double *__restrict__ loss_sum, float *__restrict__ dfeat,
+    int64_t stride, float *__restrict__ dw_grads) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t mbar;
+    __shared__ uint64_t bar_x[2], bar_xr[2], bar_acc[2], bar_op[2], bar_w;
     __shared__ uint32_t tmem_base_sh;
-    const int tid = threadIdx.x;
-    const int s = tid & (TILE - 1);
-    const int h = tid >> 7;
-    const int warp = tid >> 5;
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    __shared__ float s_red[PP_EPI_WARPS * 33];
+    __shared__ double s_loss[PP_EPI_WARPS];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NN = sh.nn, NINP = sh.ninp, NH = sh.nh, NIN = sh.nin;
+    const int64_t ntiles = (b + TILE - 1) / TILE;
+    const int64_t xtile_bytes = 2 * (int64_t)sh.xhalf;
+
+    // ---- prologue: fp32 weights staged by one bulk copy, packed to fp16 hi/lo tiles
+    float *stage = reinterpret_cast<float *>(smem + sh.o_d[0]);
+    if (tid == 0) {
+        for (int t = 0; t < 2; ++t) {
+            tc::mbar_init(&bar_x[t], 1);
+            tc::mbar_init(&bar_xr[t], 1);
+            tc::mbar_init(&bar_acc[t], 1);
+            tc::mbar_init(&bar_op[t], 8);  // one arrive per epilogue warp of the slot
+        }
+        tc::mbar_init(&bar_w, 1);
+        tc::fence_mbar_init();
+        const uint32_t wbytes = (uint32_t)sh.w_floats * 4u;  // multiple of 16 (nn in {16, 32, 64})
+        tc::mbar_arrive_expect_tx(&bar_w, wbytes);
+        tc::bulk_g2s(stage, wflat, wbytes, &bar_w);
+    }
+    __syncthreads();
+    tc::mbar_wait(&bar_w, 0);
     {
-        // fp16 weight tiles + fp32 output row, pre-packed once per step (independent 16-byte loads)
-        const uint4 *src = reinterpret_cast<const uint4 *>(wimg);
-        uint4 *dst = reinterpret_cast<uint4 *>(smem);
-        for (int q = tid; q < (int)(sh.o_x / 16); q += TC_THREADS) dst[q] = __ldg(src + q);
-        for (int q = tid; q < (2048 + 256) / 16; q += TC_THREADS)
-            reinterpret_cast<uint4 *>(smem + sh.o_dout)[q] = make_uint4(0, 0, 0, 0);
+        // one 16-byte core-matrix row (8 consecutive inputs of one output) per item
+        const float *src = stage;
+        for (int i = 0; i < NH; ++i) {
+            const int win = i == 0 ? NIN : NN, wp = i == 0 ? NINP : NN, g8 = wp >> 3;
+            for (int q = tid; q < NN * g8; q += PP_THREADS) {
+                const int o = q / g8, j0 = (q - o * g8) * 8;
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = (j0 + e < win) ? src[o * win + j0 + e] : 0.0f;
+                uint32_t hw[4], lw[4];
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                    __half h0, l0, h1, l1;
+                    tc::split_f16(v[e], h0, l0);
+                    tc::split_f16(v[e + 1], h1, l1);
+                    __half2 hh2 = __halves2half2(h0, h1), ll2 = __halves2half2(l0, l1);
+                    hw[e / 2] = *reinterpret_cast<uint32_t *>(&hh2);
+                    lw[e / 2] = *reinterpret_cast<uint32_t *>(&ll2);
+                }
+                const uint32_t off = tc::tile_off(o, j0, wp);
+                *reinterpret_cast<uint4 *>(smem + sh.o_w[i] + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                *reinterpret_cast<uint4 *>(smem + sh.o_wlo[i] + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            }
+            src += NN * win;
+        }
+        for (int q = tid; q < NN; q += PP_THREADS) reinterpret_cast<float *>(smem + sh.o_wout)[q] = src[q];
     }
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, sh.t_alloc);
-    if (tid == 0) {
-        tc::mbar_init(&mbar, 1);
-        tc::fence_mbar_init();
-    }
+    tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = tmem_base_sh;
-    uint32_t phase = 0;
-    float *s_part = reinterpret_cast<float *>(smem + sh.o_misc);
-    float *s_delta = s_part + TILE;
-    const float *s_wout = reinterpret_cast<const float *>(smem + sh.o_wout);
-    const uint32_t idesc_fwd = tc::make_idesc(128, NN, 0, 0);
-    const int64_t ntiles = (b + TILE - 1) / TILE;
-    const int tile_u4 = TILE * NINP * 2 / 16;
-    bool first_tile = true;
+    auto load_x = [&](int t, int64_t tile) {  // X hi -> o_d[t], X lo -> o_hlo[t]
+        const uint8_t *src = xtiles + tile * xtile_bytes;
+        tc::mbar_arrive_expect_tx(&bar_x[t], 2 * sh.xhalf);
+        tc::bulk_g2s(smem + sh.o_d[t], src, sh.xhalf, &bar_x[t]);
+        tc::bulk_g2s(smem + sh.o_hlo[t], src + sh.xhalf, sh.xhalf, &bar_x[t]);
+    };
+    if (tid == 0) {
+        for (int t = 0; t < 2; ++t)
+            if ((int64_t)blockIdx.x + t * (int64_t)gridDim.x < ntiles) load_x(t, blockIdx.x + t * (int64_t)gridDim.x);
+    }
+    const int nph = 2 * NH;
 
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t row = tile * TILE + s;
-        const bool valid = row < b;
-        const float tgt = valid ? targets[row] : 0.0f;
-        // ---- X tile: global (L2) -> smem; rows past the batch are zeroed
-        {
-            // hi tile then lo tile (contiguous both in global and in smem: o_xlo = o_x + tile bytes)
-            const uint4 *src = reinterpret_cast<const uint4 *>(xtiles + tile * (int64_t)(2 * TILE * NINP * 2));
-            uint4 *dst = reinterpret_cast<uint4 *>(smem + sh.o_x);
-            const int64_t nvalid = b - tile * TILE;
-            for (int q = tid; q < 2 * tile_u4; q += TC_THREADS) {
-                // core-matrix row (q % tile_u4)*16 bytes -> sample row ((..)/(NINP/8))*8 + (q%8)
-                const int qq = q % tile_u4;
-                int cm = qq >> 3, r = ((cm / (NINP / 8)) << 3) + (qq & 7);
-                dst[q] = r < nvalid ? src[q] : make_uint4(0, 0, 0, 0);
+    if (warp == PP_EPI_WARPS) {
+        // ================================================================ MMA issuer
+        if (lane == 0) {
+            uint32_t par_x = 0, par_xr = 0, par_op = 0, dw_started = 0, started = 0;
+            int64_t kt0 = 0, kt1 = 1;
+            int ph0 = 0, ph1 = 0;
+            const uint32_t idesc_fwd = tc::make_idesc(128, NN, 0, 0);
+#ifdef NVOL_TIMELINE
+            int mma_n = 0;
+            TL(4000, gtime());
+#endif
+            for (;;) {
+                bool any = false;
+                for (int t = 0; t < 2; ++t) {
+                    const int64_t kt = t ? kt1 : kt0;
+                    const int ph = t ? ph1 : ph0;
+                    if ((int64_t)blockIdx.x + kt * (int64_t)gridDim.x >= ntiles) continue;
+                    any = true;
+                    if ((started >> t) & 1u) {  // previous phase's epilogue released its operands / TMEM
+                        tc::mbar_wait(&bar_op[t], (par_op >> t) & 1u);
+                        par_op ^= 1u << t;
+                    }
+                    started |= 1u << t;
+                    if (ph == 0) {
+                        tc::mbar_wait(&bar_x[t], (par_x >> t) & 1u);
+                        par_x ^= 1u << t;
+                    }
+                    if (ph == nph - 1) {  // dW_0 reads the reloaded X hi tile
+                        tc::mbar_wait(&bar_xr[t], (par_xr >> t) & 1u);
+                        par_xr ^= 1u << t;
+                    }
+                    tc::fence_after();
+#ifdef NVOL_TIMELINE
+                    TL(2 * mma_n, gtime());
+#endif
+                    const uint32_t acc = tmem + sh.t_acc[t];
+                    const uint32_t dbuf = tc::smem_u32(smem + sh.o_d[t]), lbuf = tc::smem_u32(smem + sh.o_hlo[t]);
+                    if (ph < NH) {
+                        // forward layer i, split fp16: hi*hi -> acc; lo*hi + hi*lo -> acc + NN (x kLoScale)
+                        const int i = ph;
+                        const int win = (i == 0) ? NINP : NN;
+                        const uint32_t sbo = (win / 8) * 128;
+                        const uint32_t ah = (i == 0) ? dbuf : tc::smem_u32(smem + sh.o_h[t][i]);
+                        const uint64_t adh = tc::make_desc(ah, 128, sbo), adl = tc::make_desc(lbuf, 128, sbo);
+                        const uint64_t bdh = tc::make_desc(tc::smem_u32(smem + sh.o_w[i]), 128, sbo);
+                        const uint64_t bdl = tc::make_desc(tc::smem_u32(smem + sh.o_wlo[i]), 128, sbo);
+                        for (int k = 0; k < win / 16; ++k) {
+                            const uint64_t dk = (uint64_t)(k * 16);  // +256 bytes per K step
+                            tc::mma_f16(acc, adh + dk, bdh + dk, idesc_fwd, k > 0);
+                            tc::mma_f16(acc + NN, adl + dk, bdh + dk, idesc_fwd, k > 0);
+#if NVOL_FWD_WLO
+                            tc::mma_f16(acc + NN, adh + dk, bdl + dk, idesc_fwd, 1);
+#endif
+                        }
+                    } else {
+                        // backward layer j: dW_j += delta^T H_j (both slots accumulate), dX = delta W_j
+                        const int j = nph - 1 - ph;
+                        const int win = (j == 0) ? NINP : NN;
+                        const uint32_t hb = (j == 0) ? lbuf : tc::smem_u32(smem + sh.o_h[t][j]);
+                        {
+                            const uint32_t id = tc::make_idesc(128, win, 1, 1);
+                            const uint64_t ad = tc::make_desc(dbuf, (NN / 8) * 128, 128);
+                            const uint64_t bd = tc::make_desc(hb, (win / 8) * 128, 128);
+                            const uint32_t first = ((dw_started >> j) & 1u) ? 1u : 0u;
+                            for (int k = 0; k < TILE / 16; ++k)
+                                tc::mma_f16(tmem + sh.t_dw[j], ad + (uint64_t)(k * 2 * (NN / 8) * 8),
+                                            bd + (uint64_t)(k * 2 * (win / 8) * 8), id, (first || k > 0) ? 1 : 0);
+                            dw_started |= 1u << j;
+                        }
+                        {
+                            const uint32_t id = tc::make_idesc(128, win, 0, 1);
+                            const uint64_t ad = tc::make_desc(dbuf, 128, (NN / 8) * 128);
+                            const uint64_t bd = tc::make_desc(tc::smem_u32(smem + sh.o_w[j]), (win / 8) * 128, 128);
+                            for (int k = 0; k < NN / 16; ++k)
+                                tc::mma_f16(acc, ad + (uint64_t)(k * 16), bd + (uint64_t)(k * 2 * (win / 8) * 8), id,
+                                            k > 0);
+                        }
+                    }
+                    tc::mma_commit(&bar_acc[t]);
+#ifdef NVOL_TIMELINE
+                    TL(2 * mma_n + 1, ((unsigned long long)t << 60) | ((unsigned long long)ph << 52) | (gtime() & ((1ull << 52) - 1)));
+                    ++mma_n;
+#endif
+                    int nph_next = ph + 1;
+                    int64_t nkt = kt;
+                    if (nph_next == nph) {
+                        nph_next = 0;
+                        nkt += 2;
+                    }
+                    if (t) {
+                        ph1 = nph_next;
+                        kt1 = nkt;
+                    } else {
+                        ph0 = nph_next;
+                        kt0 = nkt;
+                    }
+                }
+                if (!any) break;
             }
         }
-        tc::fence_proxy_async();
-        __syncthreads();
-
-        // ---- forward
-        float outp = 0.0f;
-        for (int i = 0; i < NH; ++i) {
-            const int win = (i == 0) ? NINP : NN;
-            if (tid == 0) {
-                // split-fp16 forward: hi*hi -> t_f; lo*hi + hi*lo -> t_flo (x kLoScale)
-                tc::fence_after();
-                const uint32_t ah = tc::smem_u32(smem + sh.o_h[i]);
-                const uint32_t al = tc::smem_u32(smem + (i == 0 ? sh.o_xlo : sh.o_hlo[(i - 1) & 1]));
-                const uint32_t bh = tc::smem_u32(smem + sh.o_w[i]);
-                const uint32_t bl = tc::smem_u32(smem + sh.o_wlo[i]);
-                const uint32_t sbo = (win / 8) * 128;
-                for (int k = 0; k < win / 16; ++k) {
-                    const uint64_t adh = tc::make_desc(ah + k * 256, 128, sbo), adl = tc::make_desc(al + k * 256, 128, sbo);
-                    const uint64_t bdh = tc::make_desc(bh + k * 256, 128, sbo), bdl = tc::make_desc(bl + k * 256, 128, sbo);
-                    tc::mma_f16(tmem + sh.t_f, adh, bdh, idesc_fwd, k > 0);
-                    tc::mma_f16(tmem + sh.t_flo, adl, bdh, idesc_fwd, k > 0);
-                    tc::mma_f16(tmem + sh.t_flo, adh, bdl, idesc_fwd, 1);
-                }
-                tc::mma_commit(&mbar);
-            }
-            tc::mbar_wait(&mbar, phase);
-            phase ^= 1;
-            tc::fence_after();
-            int c0, nc;
-            half_cols(NN, h, c0, nc);
-            uint8_t *dst = smem + sh.o_h[i + 1];
-            uint8_t *dst_lo = smem + sh.o_hlo[i & 1];
-            // accumulator = kActScale * pre-activation: ReLU commutes with the
-            // positive scale, so the stored activations stay scaled too
-            for (int c = c0; c < c0 + nc; c += 16) {
-                float v[16], vl[16];
-                tc::tmem_ld16(tmem + lane_base + sh.t_f + c, v);
-                tc::tmem_ld16(tmem + lane_base + sh.t_flo + c, vl);
-                tc::tmem_wait_ld();
+        __syncwarp();
+    } else {
+        // ================================================================ epilogue slot t
+        const int t = warp >> 3, hh = (warp >> 2) & 1, q = warp & 3;
+        const int s = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const uint32_t tacc = tmem + lane_base + sh.t_acc[t];
+        uint8_t *dbuf = smem + sh.o_d[t];
+        uint8_t *lbuf = smem + sh.o_hlo[t];
+        float *s_part = reinterpret_cast<float *>(smem + sh.o_part) + t * 2 * TILE;
+        const float *s_wout = reinterpret_cast<const float *>(smem + sh.o_wout);
+        uint32_t par_acc = 0;
+        double lsum = 0.0;  // this row's loss terms over the slot's tiles (column half 0 only)
+        float dwo[32];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
-                store_row_f16(dst, s, c, NN, v, false);
-                if (i < NH - 1) {
-                    // lo part of the activation for the next layer's split product
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) vl[e] = (v[e] - __half2float(__float2half_rn(v[e]))) * tc::kLoScale;
-                    store_row_f16(dst_lo, s, c, NN, vl, false);
-                }
-                if (i == NH - 1) {
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * fmaxf(v[e], 0.0f);
-                }
-            }
+        for (int e = 0; e < 32; ++e) dwo[e] = 0.0f;
+        int cn0, cnn;
+        group_cols(NN, hh, 2, cn0, cnn);  // this thread's hidden columns [cn0, cn0 + cnn), cnn <= 32
+#ifdef NVOL_TIMELINE
+        int epi_n = 0;
+#endif
+        auto release = [&]() {            // smem operands written / TMEM reads done -> MMA warp
+#ifdef NVOL_TIMELINE
+            if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * epi_n + 1, gtime());
+#endif
             tc::fence_before();
             tc::fence_proxy_async();
-            __syncthreads();
-        }
-        // ---- output layer + loss gradient
-        if (h == 1) s_part[s] = outp;
-        __syncthreads();
-        if (h == 0) {
-            float o = (outp + s_part[s]) * (1.0f / tc::kActScale);
-            float pred = sh.relu_out ? fmaxf(o, 0.0f) : o;
-            double d = (double)pred - (double)tgt;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_op[t]);
+        };
+        for (int64_t kt = t;; kt += 2) {
+            const int64_t tile = (int64_t)blockIdx.x + kt * (int64_t)gridDim.x;
+            if (tile >= ntiles) break;
+            const int64_t row = tile * TILE + s;
+            const bool valid = row < b;
+            const float tgt = valid ? __ldg(targets + row) : 0.0f;
+            // ---- forward epilogues: accumulator = kActScale * pre-activation
+            float outp = 0.0f;
+            for (int i = 0; i < NH; ++i) {
+                tc::mbar_wait_sleep(&bar_acc[t], par_acc);
+                par_acc ^= 1u;
+                tc::fence_after();
+#ifdef NVOL_TIMELINE
+                if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * (++epi_n), gtime());
+#endif
+                const bool last = i == NH - 1;
+                uint8_t *dst = last ? lbuf : smem + sh.o_h[t][i + 1];
+                for (int c = cn0; c < cn0 + cnn; c += 16) {
+                    float v[16], vl[16];
+                    tc::tmem_ld16(tacc + c, v);
+                    tc::tmem_ld16(tacc + NN + c, vl);
+                    tc::tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
+                    store_row_f16(dst, s, c, NN, v, false);
+                    if (!last) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            vl[e] = (v[e] - __half2float(__float2half_rn(v[e]))) * tc::kLoScale;
+                        store_row_f16(lbuf, s, c, NN, vl, false);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * v[e];
+                    }
+                }
+                if (!last) release();
+            }
+            // ---- output layer + loss gradient (both column halves of a row see the same sum)
+            s_part[hh * TILE + s] = outp;
+            named_sync(1 + t, 256);
+            const float o = (s_part[s] + s_part[TILE + s]) * (1.0f / tc::kActScale);
+            const float pred = sh.relu_out ? fmaxf(o, 0.0f) : o;
+            const double d = (double)pred - (double)tgt;
             double g, sl;
             if (sh.loss_kind == 0) {
                 sl = fabs(d);
@@ -419,138 +590,149 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mlp_tc_kernel(
                 gf = 0.0f;
                 sl = 0.0;
             }
-            s_delta[s] = gf;
-            *reinterpret_cast<__half *>(smem + sh.o_dout + (s >> 3) * 128 + (s & 7) * 16) = __float2half_rn(gf * dscale);
-            for (int o2 = 16; o2 > 0; o2 >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o2);
-            if ((tid & 31) == 0) atomicAdd(loss_sum, sl);
-        }
-        __syncthreads();
-        {
-            int c0, nc;
-            half_cols(NN, h, c0, nc);
-            const float g = s_delta[s] * dscale;
-            const uint8_t *hn = smem + sh.o_h[NH];
-            uint8_t *dd = smem + sh.o_d[0];
-            for (int c = c0; c < c0 + nc; c += 16) {
-                float hv[16], dv[16];
-                load_row_f16(hn, s, c, NN, hv);
+            lsum += sl;
+            // ---- dWout (CUDA cores, per-thread partials) and delta_NH = mask(h_NH) * g * w_out
+            {
+                const float gd = gf * dscale;
 #pragma unroll
-                for (int e = 0; e < 16; ++e) dv[e] = hv[e] > 0.0f ? g * s_wout[c + e] : 0.0f;
-                store_row_f16(dd, s, c, NN, dv, false);
+                for (int ch = 0; ch < 2; ++ch) {
+                    const int c = cn0 + ch * 16;
+                    if (ch * 16 < cnn) {
+                        float hv[16], dv[16];
+                        load_row_f16(lbuf, s, c, NN, hv);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            dwo[ch * 16 + e] += gf * hv[e];
+                            dv[e] = hv[e] > 0.0f ? gd * s_wout[c + e] : 0.0f;
+                        }
+                        store_row_f16(dbuf, s, c, NN, dv, false);
+                    }
+                }
             }
-        }
-        tc::fence_proxy_async();
-        __syncthreads();
-
-        // ---- backward
-        int cur = 0;
-        for (int j = NH - 1; j >= 0; --j) {
-            const int win = (j == 0) ? NINP : NN;
-            if (tid == 0) {
+            named_sync(1 + t, 256);  // every h_NH read done: lbuf may take the X hi reload
+            if (hh == 0 && q == 0 && lane == 0) {
+                tc::fence_proxy_async();
+                tc::mbar_arrive_expect_tx(&bar_xr[t], sh.xhalf);
+                tc::bulk_g2s(lbuf, xtiles + tile * xtile_bytes, sh.xhalf, &bar_xr[t]);
+            }
+            release();
+            // ---- backward epilogues
+            for (int j = NH - 1; j >= 0; --j) {
+                tc::mbar_wait_sleep(&bar_acc[t], par_acc);
+                par_acc ^= 1u;
                 tc::fence_after();
-                const uint32_t dA = tc::smem_u32(smem + sh.o_d[cur]);
-                if (j == NH - 1) {
-                    const uint32_t a0 = tc::smem_u32(smem + sh.o_dout);
-                    const uint32_t b0 = tc::smem_u32(smem + sh.o_h[NH]);
-                    const uint32_t id = tc::make_idesc(128, NN, 1, 1);
-                    for (int k = 0; k < TILE / 16; ++k) {
-                        uint64_t ad = tc::make_desc(a0 + k * 256, 128, 16);
-                        uint64_t bd = tc::make_desc(b0 + k * 2 * (NN / 8) * 128, (NN / 8) * 128, 128);
-                        tc::mma_f16(tmem + sh.t_dwout, ad, bd, id, (first_tile && k == 0) ? 0 : 1);
+#ifdef NVOL_TIMELINE
+                if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * (++epi_n), gtime());
+#endif
+                if (j > 0) {
+                    const uint8_t *hj = smem + sh.o_h[t][j];
+                    for (int c = cn0; c < cn0 + cnn; c += 16) {
+                        float v[16], hv[16];
+                        tc::tmem_ld16(tacc + c, v);
+                        load_row_f16(hj, s, c, NN, hv);
+                        tc::tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = hv[e] > 0.0f ? v[e] : 0.0f;
+                        store_row_f16(dbuf, s, c, NN, v, false);
+                    }
+                } else {
+                    // the slot's smem buffers are free once dW_0 / dX_0 completed: next X tile
+                    if (hh == 0 && q == 0 && lane == 0 && tile + 2 * (int64_t)gridDim.x < ntiles)
+                        load_x(t, tile + 2 * (int64_t)gridDim.x);
+                    int c0, nc;
+                    group_cols(NINP, hh, 2, c0, nc);
+                    for (int c = c0; c < c0 + nc; c += 16) {
+                        float v[16];
+                        tc::tmem_ld16(tacc + c, v);
+                        tc::tmem_wait_ld();
+                        if (valid) {
+                            // feature-major dL/dfeat [NIN][B]: a warp stores 32 consecutive rows per column
+#pragma unroll
+                            for (int e = 0; e < 16; ++e)
+                                if (c + e < NIN) dfeat[(int64_t)(c + e) * stride + row] = v[e] * (1.0f / dscale);
+                        }
                     }
                 }
-                {
-                    const uint32_t b0 = tc::smem_u32(smem + sh.o_h[j]);
-                    const uint32_t id = tc::make_idesc(128, win, 1, 1);
-                    for (int k = 0; k < TILE / 16; ++k) {
-                        uint64_t ad = tc::make_desc(dA + k * 2 * (NN / 8) * 128, (NN / 8) * 128, 128);
-                        uint64_t bd = tc::make_desc(b0 + k * 2 * (win / 8) * 128, (win / 8) * 128, 128);
-                        tc::mma_f16(tmem + sh.t_dw[j], ad, bd, id, (first_tile && k == 0) ? 0 : 1);
-                    }
-                }
-                {
-                    const uint32_t b0 = tc::smem_u32(smem + sh.o_w[j]);
-                    const uint32_t id = tc::make_idesc(128, win, 0, 1);
-                    for (int k = 0; k < NN / 16; ++k) {
-                        uint64_t ad = tc::make_desc(dA + k * 256, 128, (NN / 8) * 128);
-                        uint64_t bd = tc::make_desc(b0 + k * 2 * (win / 8) * 128, (win / 8) * 128, 128);
-                        tc::mma_f16(tmem + sh.t_g, ad, bd, id, k > 0);
-                    }
-                }
-                tc::mma_commit(&mbar);
+                release();
             }
-            tc::mbar_wait(&mbar, phase);
-            phase ^= 1;
-            tc::fence_after();
-            int c0, nc;
-            half_cols(win, h, c0, nc);
-            if (j > 0) {
-                const uint8_t *hj = smem + sh.o_h[j];
-                uint8_t *dn = smem + sh.o_d[cur ^ 1];
-                for (int c = c0; c < c0 + nc; c += 16) {
-                    float v[16], hv[16];
-                    tc::tmem_ld16(tmem + lane_base + sh.t_g + c, v);
-                    tc::tmem_wait_ld();
-                    load_row_f16(hj, s, c, NN, hv);
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] = hv[e] > 0.0f ? v[e] : 0.0f;
-                    store_row_f16(dn, s, c, NN, v, false);
-                }
-            } else {
-                for (int c = c0; c < c0 + nc; c += 16) {
-                    float v[16];
-                    tc::tmem_ld16(tmem + lane_base + sh.t_g + c, v);
-                    tc::tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] *= 1.0f / dscale;
-                    if (valid) {
-                        // feature-major dL/dfeat [NIN][B]: a warp stores 32 consecutive rows per column
-#pragma unroll
-                        for (int e = 0; e < 16; ++e)
-                            if (c + e < NIN) dfeat[(int64_t)(c + e) * stride + row] = v[e];
-                    }
-                }
-            }
-            tc::fence_before();
-            tc::fence_proxy_async();
-            __syncthreads();
-            cur ^= 1;
         }
-        first_tile = false;
+        // ---- dW_out and the loss: warp-reduce the per-thread partials into shared
+        // memory; one RED per column and one loss atomic per CTA after the barrier
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                float v = dwo[ch * 16 + e];
+                for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
+                dwo[ch * 16 + e] = v;
+            }
+        }
+        for (int o2 = 16; o2 > 0; o2 >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o2);
+        if (lane == 0) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) s_red[warp * 33 + e] = dwo[e];
+            s_loss[warp] = hh == 0 ? lsum : 0.0;
+        }
     }
-
-    // ---- flush dW partials (fp32) once per CTA
-    float *dst = partials + (int64_t)blockIdx.x * sh.w_floats;
-    if (!first_tile) {
-        const int o = (warp & 3) * 32 + (tid & 31);
+    __syncthreads();
+    if (tid < NN) {
+        // column c belongs to half c / (NN/2) (NN >= 32) or half 0 (NN = 16); sum its 8 warps in fixed order
+        const int half = NN >= 32 ? tid / (NN / 2) : 0;
+        const int e = tid - half * (NN >= 32 ? NN / 2 : 0);
+        float acc = 0.0f;
+        for (int w = 0; w < PP_EPI_WARPS; ++w)
+            if (((w >> 2) & 1) == half) acc += s_red[w * 33 + e];
+        atomicAdd(dw_grads + sh.w_floats - NN + tid, acc * (1.0f / tc::kActScale));
+    }
+    if (tid == PP_THREADS - 32) {
+        double l = 0.0;
+        for (int w = 0; w < PP_EPI_WARPS; ++w) l += s_loss[w];
+        atomicAdd(loss_sum, l);
+    }
+    // ---- flush dW_0..dW_{nh-1} (fp32) once per CTA: vector REDs straight into the gradient
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp < PP_EPI_WARPS) {
+        const int q = warp & 3, grp = warp >> 2;
+        const int o = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const float unscale = 1.0f / (dscale * tc::kActScale);  // dW = (dscale*delta)^T (kActScale*H)
         int64_t base = 0;
-        for (int j = 0; j <= NH; ++j) {
+        for (int j = 0; j < NH; ++j) {
             const int win = (j == 0) ? NIN : NN;
             const int wacc = (j == 0) ? NINP : NN;
-            const int rows = (j == NH) ? 1 : NN;
-            const uint32_t tcol = (j == NH) ? sh.t_dwout : sh.t_dw[j];
-            const float unscale = 1.0f / (dscale * tc::kActScale);  // dW = (dscale*delta)^T (kActScale*H)
             int c0, nc;
-            half_cols(wacc, h, c0, nc);
-            for (int c = c0; c < c0 + nc; c += 16) {
-                float v[16];
-                tc::tmem_ld16(tmem + lane_base + tcol + c, v);
-                tc::tmem_wait_ld();
+            group_cols(wacc, grp, 4, c0, nc);
+            if (q * 32 < NN) {  // warp-uniform: lanes of quarters past nn hold no dW rows
+                for (int c = c0; c < c0 + nc; c += 16) {
+                    float v[16];
+                    tc::tmem_ld16(tmem + lane_base + sh.t_dw[j] + c, v);
+                    tc::tmem_wait_ld();
+                    if (o < NN) {
+                        float *g = dw_grads + base + (int64_t)o * win + c;
+                        if (c + 16 <= win && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
 #pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] *= unscale;
-                if (o < rows) {
+                            for (int e = 0; e < 16; e += 4)
+                                atomicAdd(reinterpret_cast<float4 *>(g + e),
+                                          make_float4(v[e] * unscale, v[e + 1] * unscale, v[e + 2] * unscale,
+                                                      v[e + 3] * unscale));
+                        } else {
 #pragma unroll
-                    for (int e = 0; e < 16; ++e)
-                        if (c + e < win) dst[base + (int64_t)o * win + c + e] = v[e];
+                            for (int e = 0; e < 16; ++e)
+                                if (c + e < win) atomicAdd(g + e, v[e] * unscale);
+                        }
+                    }
                 }
             }
-            base += (int64_t)rows * win;
+            base += (int64_t)NN * win;
         }
-    } else {
-        for (int64_t q = tid; q < sh.w_floats; q += TC_THREADS) dst[q] = 0.0f;
     }
     tc::fence_before();
     __syncthreads();
+#ifdef NVOL_TIMELINE
+    if (tid == 0) TL(4001, gtime());
+#endif
     if (warp == 0) tc::tmem_dealloc(tmem, sh.t_alloc);
 }
 
@@ -560,9 +742,9 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
                                                                 const float *__restrict__ dfeat, int64_t b,
                                                                 int64_t stride,
                                                                 const GridTables tab, int n_coarse, int coarse_floats,
-                                                                float *__restrict__ grads,
-                                                                float *__restrict__ partials) {
+                                                                float *__restrict__ grads) {
     extern __shared__ float acc_s[];
+    const uint64_t keep = l2_evict_last();
     for (int q = threadIdx.x; q < coarse_floats; q += SC_THREADS) acc_s[q] = 0.0f;
     __syncthreads();
     const int m = tab.n_levels, nin = m * NF;
@@ -594,10 +776,10 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
                     if (max(s0, s1) == lo + 1 && ((lo + par) & 1u) == 0u) {   // adjacent and 16-byte aligned
                         float4 q = s0 == lo ? make_float4(w0 * d[0], w0 * d[1], w1 * d[0], w1 * d[1])
                                             : make_float4(w1 * d[0], w1 * d[1], w0 * d[0], w0 * d[1]);
-                        atomicAdd(reinterpret_cast<float4 *>(gl + 2 * (size_t)lo), q);
+                        red_add4(gl + 2 * (size_t)lo, q, keep);
                     } else {
-                        atomicAdd(reinterpret_cast<float2 *>(gl) + s0, make_float2(w0 * d[0], w0 * d[1]));
-                        atomicAdd(reinterpret_cast<float2 *>(gl) + s1, make_float2(w1 * d[0], w1 * d[1]));
+                        red_add2(gl + 2 * (size_t)s0, w0 * d[0], w0 * d[1], keep);
+                        red_add2(gl + 2 * (size_t)s1, w1 * d[0], w1 * d[1], keep);
                     }
                 }
                 continue;
@@ -609,43 +791,31 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
             float w = cw32(c, k);
             float *g = gl + (size_t)slot * NF;
             if (coarse) {
+                float *gs = acc_s + tab.offset[l] + (size_t)slot * NF;  // shared-typed: ATOMS, not generic
 #pragma unroll
-                for (int f = 0; f < NF; ++f) atomicAdd(g + f, w * d[f]);
+                for (int f = 0; f < NF; ++f) atomicAdd(gs + f, w * d[f]);
             } else if constexpr (NF == 2) {
-                atomicAdd(reinterpret_cast<float2 *>(g), make_float2(w * d[0], w * d[1]));
+                red_add2(g, w * d[0], w * d[1], keep);
             } else if constexpr (NF == 4 || NF == 8) {
 #pragma unroll
                 for (int q = 0; q < NF / 4; ++q)
-                    atomicAdd(reinterpret_cast<float4 *>(g) + q,
-                              make_float4(w * d[4 * q], w * d[4 * q + 1], w * d[4 * q + 2], w * d[4 * q + 3]));
+                    red_add4(g + 4 * q, make_float4(w * d[4 * q], w * d[4 * q + 1], w * d[4 * q + 2], w * d[4 * q + 3]),
+                             keep);
             } else {
-                atomicAdd(g, w * d[0]);
+                red_add(g, w * d[0], keep);
             }
         }
     }
     __syncthreads();
-    float *dst = partials + (int64_t)blockIdx.x * coarse_floats;
-    for (int q = threadIdx.x; q < coarse_floats; q += SC_THREADS) dst[q] = acc_s[q];
-}
-
-// g[i] += sum_c partials[c][i] in fixed c order.  Block = 32 outputs x 8
-// CTA groups; the 8 group sums combine in fixed order through shared memory.
-__global__ void __launch_bounds__(256) reduce_partials_kernel(const float *__restrict__ partials, int nparts,
-                                                              int64_t n, float *__restrict__ g) {
-    __shared__ float red[8][33];
-    const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
-    const int64_t i = (int64_t)blockIdx.x * 32 + lane;
-    float acc = 0.0f;
-    if (i < n)
-        for (int c = grp; c < nparts; c += 8) acc += partials[(int64_t)c * n + i];
-    red[grp][lane] = acc;
-    __syncthreads();
-    if (grp == 0 && i < n) {
-        float s = 0.0f;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) s += red[q][lane];
-        g[i] += s;
+    // coarse levels: one vector RED per 4 entries per CTA (coarse_floats is a
+    // multiple of 4 or the tail goes out as scalars; grads is 16-byte aligned)
+    const int n4 = coarse_floats >> 2;
+    for (int q = threadIdx.x; q < n4; q += SC_THREADS) {
+        const float4 v = reinterpret_cast<const float4 *>(acc_s)[q];
+        if (v.x != 0.0f || v.y != 0.0f || v.z != 0.0f || v.w != 0.0f)
+            red_add4(grads + 4 * q, v, keep);
     }
+    for (int q = 4 * n4 + threadIdx.x; q < coarse_floats; q += SC_THREADS) red_add(grads + q, acc_s[q], keep);
 }
 
 // ============================================================================ host side
@@ -658,7 +828,7 @@ constexpr int MAX_CHUNKS = 4;
 struct TcPlan {
     TcShape sh;
     int grid_mlp, grid_sc, n_coarse, coarse_floats, nchunks;
-    int64_t ntiles, chunk_tiles, off_x, off_dfeat, off_wpart, off_cpart, off_img, total;
+    int64_t ntiles, chunk_tiles, off_x, off_dfeat, total;
 };
 
 static int num_sms() {
@@ -678,9 +848,19 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
         if (tab.entries[l] >= (1ll << 31)) return 0;
     const int sms = num_sms();
     p.ntiles = (b + TILE - 1) / TILE;
-    // chunks of >= ~1.5 MLP tiles per SM: 2 chunks at B = 65,536
-    p.nchunks = (int)(p.ntiles / (sms + sms / 2));
+    // Row chunks on three streams (encode(c+1) || mlp(c) || scatter(c-1)).
+    // Measured on B200 at cfg2: each kernel's cost is dominated by its fixed
+    // per-launch latency (weight-image load, tail), so two half-size chunks
+    // cost ~2x one full chunk; default is one chunk, NVOL_TRAIN_CHUNKS=n
+    // (1..4) re-enables the overlap schedule.
+    static int env_chunks = -1;
+    if (env_chunks < 0) {
+        const char *e = getenv("NVOL_TRAIN_CHUNKS");
+        env_chunks = e ? atoi(e) : 1;
+    }
+    p.nchunks = env_chunks;
     p.nchunks = p.nchunks < 1 ? 1 : (p.nchunks > MAX_CHUNKS ? MAX_CHUNKS : p.nchunks);
+    if (p.nchunks > p.ntiles) p.nchunks = (int)p.ntiles;
     p.chunk_tiles = (p.ntiles + p.nchunks - 1) / p.nchunks;
     p.nchunks = (int)((p.ntiles + p.chunk_tiles - 1) / p.chunk_tiles);  // every chunk non-empty
     p.grid_mlp = (int)(p.chunk_tiles < sms ? p.chunk_tiles : sms);
@@ -696,24 +876,16 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
     p.off_x = 0;
     p.off_dfeat = al(p.ntiles * TILE * p.sh.ninp * 4);  // hi + lo fp16 tiles
-    p.off_wpart = p.off_dfeat + al(b * p.sh.nin * 4);
-    p.off_cpart = p.off_wpart + al((int64_t)MAX_CHUNKS * p.grid_mlp * p.sh.w_floats * 4);
-    p.off_img = p.off_cpart + al((int64_t)MAX_CHUNKS * p.grid_sc * p.coarse_floats * 4);
-    p.total = p.off_img + al(p.sh.o_x) + 256;
+    p.total = p.off_dfeat + al(b * p.sh.nin * 4) + 256;
     return 1;
 }
 
 int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
-    // upper bound over level tables: the coarse prefix is capped by COARSE_BYTES
     TcPlan p;
     if (!build_shape(p.sh, m, n, nn, nh, 1, 0)) return 0;
-    const int sms = num_sms();
     int64_t ntiles = (b + TILE - 1) / TILE;
-    int grid_mlp = (int)(ntiles < sms ? ntiles : sms);
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
-    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) +
-           al((int64_t)MAX_CHUNKS * grid_mlp * p.sh.w_floats * 4) +
-           al((int64_t)MAX_CHUNKS * sms * (COARSE_BYTES / 4) * 4) + al(p.sh.o_x) + 256;
+    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) + 256;
 }
 
 static cudaEvent_t g_stage_events[8];
@@ -752,14 +924,10 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
     uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
     uint8_t *xt = ws + p.off_x;
     float *dfeat = reinterpret_cast<float *>(ws + p.off_dfeat);
-    float *wpart = reinterpret_cast<float *>(ws + p.off_wpart);
-    float *cpart = reinterpret_cast<float *>(ws + p.off_cpart);
-    uint8_t *wimg = ws + p.off_img;
     int64_t enc = 0;
     for (int l = 0; l < tab.n_levels; ++l) enc = max(enc, tab.offset[l] + tab.entries[l] * tab.n_feat);
     const int64_t woff = (enc + 3) & ~(int64_t)3;
-    int st = pack_mlp_image(params + woff, p.sh.nin, p.sh.ninp, nn, nh, p.sh.o_w, p.sh.o_wout, wimg, s, p.sh.o_wlo);
-    if (st) return st;
+    int st = NVOL_OK;
     cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh.smem_bytes);
     const size_t csm = (size_t)p.coarse_floats * 4;
     switch (tab.n_feat) {
@@ -790,6 +958,8 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         const unsigned egrid = grid_for(nb * tab.n_levels, 256);
         uint8_t *xtc = xt + t0 * tile_bytes;
         const float *cc = coords + 3 * r0;
+        if (nb % TILE)  // rows past the batch must be zero (0 x garbage could be NaN in dW)
+            cudaMemsetAsync(xtc + (nb / TILE) * tile_bytes, 0, (size_t)tile_bytes, se);
         switch (tab.n_feat) {
             case 1: encode_tiles_kernel<1><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
             case 2: encode_tiles_kernel<2><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
@@ -805,24 +975,20 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         if (prof) cudaEventRecord(pev[1], s);
         const int64_t ct = (nb + TILE - 1) / TILE;
         const int gm = (int)(ct < p.grid_mlp ? ct : p.grid_mlp);
-        float *wp = wpart + (int64_t)c * p.grid_mlp * p.sh.w_floats;
-        mlp_tc_kernel<<<gm, TC_THREADS, p.sh.smem_bytes, s>>>(xtc, targets + r0, nb, 1.0 / (double)b_global, dscale,
-                                                              p.sh, wimg, loss_sum, dfeat + r0, b, wp);
+        mlp_tc_kernel<<<gm, PP_THREADS, p.sh.smem_bytes, s>>>(xtc, targets + r0, nb, 1.0 / (double)b_global, dscale,
+                                                              p.sh, params + woff, loss_sum, dfeat + r0, b, grads + woff);
         st = check_launch("mlp_tc_kernel");
         if (st) return st;
-        if (gm < p.grid_mlp)  // unused partial slots of a short chunk must sum to zero
-            cudaMemsetAsync(wp + (int64_t)gm * p.sh.w_floats, 0, (size_t)(p.grid_mlp - gm) * p.sh.w_floats * 4, s);
         if (nc > 1) {
             cudaEventRecord(ss.mlp_done[c], s);
             cudaStreamWaitEvent(sc, ss.mlp_done[c], 0);
         }
         if (prof) cudaEventRecord(pev[2], s);
-        float *cp = cpart + (int64_t)c * p.grid_sc * p.coarse_floats;
         switch (tab.n_feat) {
 #define LAUNCH_SC(NFV)                                                                                             \
     case NFV:                                                                                                      \
         scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, sc>>>(cc, dfeat + r0, nb, b, tab, p.n_coarse,            \
-                                                                p.coarse_floats, grads, cp);                       \
+                                                                p.coarse_floats, grads);                       \
         break;
             LAUNCH_SC(1)
             LAUNCH_SC(2)
@@ -840,12 +1006,7 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         cudaStreamWaitEvent(s, ss.join_enc, 0);
         cudaStreamWaitEvent(s, ss.join_sc, 0);
     }
-    reduce_partials_kernel<<<grid_for(p.sh.w_floats, 32), 256, 0, s>>>(wpart, nc * p.grid_mlp, p.sh.w_floats,
-                                                                       grads + woff);
-    if (p.coarse_floats > 0)
-        reduce_partials_kernel<<<grid_for(p.coarse_floats, 32), 256, 0, s>>>(cpart, nc * p.grid_sc, p.coarse_floats,
-                                                                             grads);
-    return check_launch("reduce_partials");
+    return NVOL_OK;
 }
 
 }  // namespace nvol
@@ -859,6 +1020,14 @@ extern "C" int nvol_set_stage_events(void *const *events, int32_t n) {
     nvol::g_stage_events_n = n;
     return NVOL_OK;
 }
+
+#ifdef NVOL_TIMELINE
+extern "C" int nvol_debug_timeline(unsigned long long *host, int32_t n) {
+    cudaDeviceSynchronize();
+    return cudaMemcpyFromSymbol(host, nvol::g_tl, sizeof(unsigned long long) * (n > 4096 ? 4096 : n)) == cudaSuccess
+               ? 0 : 2;
+}
+#endif
 
 extern "C" int nvol_has_tcgen05(int device) {
     int major = 0, minor = 0;

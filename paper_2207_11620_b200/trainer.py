@@ -16,6 +16,7 @@ import csv
 import json
 import logging
 import struct
+import os
 import time
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -129,14 +130,13 @@ class StepPipeline:
         """Kernels of one step from this library (for the bench's gpu_launches)."""
         if self.model.train_mode == 0:
             return 1 + 5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 + 2
-        # sample, pack image, nchunks x (encode, MLP, scatter), 2 partial reduces, loss record, Adam
-        # (chunk plan of train_tc.cu make_plan)
-        sms = torch.cuda.get_device_properties(self.model.flat_params.device).multi_processor_count
+        # sample, nchunks x (encode, MLP, scatter), loss record, Adam, step advance
+        # (chunk plan of train_tc.cu make_plan: NVOL_TRAIN_CHUNKS, default 1)
         ntiles = (self.b + 127) // 128
-        nc = min(max(ntiles // (sms + sms // 2), 1), 4)
+        nc = max(1, min(int(os.environ.get("NVOL_TRAIN_CHUNKS", "1")), 4, ntiles))
         ct = (ntiles + nc - 1) // nc
         nc = (ntiles + ct - 1) // ct
-        return 1 + 1 + 3 * nc + 2 + 1 + 1
+        return 1 + 3 * nc + 1 + 1 + 1
 
     def step(self, n: int = 1) -> None:
         """Enqueue n steps (no host synchronisation)."""

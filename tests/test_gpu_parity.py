@@ -326,19 +326,25 @@ def test_tcgen05_step_matches_oracle(nv, name):
 
 
 def test_tcgen05_training_converges(nv):
-    """cfg1-shaped training with the tcgen05 engine tracks the fp32 engine."""
+    """cfg2-encoder training with the tcgen05 engine tracks the fp32 engine.
+    Single trajectories are chaotic under float-atomic summation order
+    (the reference itself spreads by dB between seeds), so the bar
+    is on the mean PSNR over three sampler seeds per engine."""
     from paper_2207_11620_b200 import fields, trainer
     from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
     from paper_2207_11620_b200.sampler import InCoreSampler
+    from paper_2207_11620_b200.volume import psnr
     cfg = dict(golden_config(golden("encode_cfg2.npz")), batch_size=16384)
     fld = fields.rasterize("mlobb", (48, 48, 48), host=True)
     res = {}
     for mode in (0, MODE_TCGEN05):
-        m = build_model(cfg, dims=(48, 48, 48), seed=0)
-        m.train_mode = mode
-        trainer.train(m, InCoreSampler(fld, seed=1), steps=200)
-        from paper_2207_11620_b200.volume import psnr
-        res[mode] = psnr(fld, trainer.decode(m, dims=(48, 48, 48)))
+        runs = []
+        for seed in (1, 2, 3):
+            m = build_model(cfg, dims=(48, 48, 48), seed=0)
+            m.train_mode = mode
+            trainer.train(m, InCoreSampler(fld, seed=seed), steps=200)
+            runs.append(psnr(fld, trainer.decode(m, dims=(48, 48, 48))))
+        res[mode] = float(np.mean(runs))
     assert res[MODE_TCGEN05] > 20.0
     assert abs(res[MODE_TCGEN05] - res[0]) < 1.5, res
 
