@@ -239,14 +239,15 @@ def run_ours(args):
 
     def adam_fn(ev):
         ev[0].record(stream)
-        _lib.call("nvol_adam_flat_dev", _lib.ptr(model.flat_params), _lib.ptr(model.flat_grads), _lib.ptr(model.flat_m),
-                  _lib.ptr(model.flat_v), model.flat_size, _lib.ptr(pipe.sched), pipe.sched.numel() // 3,
-                  _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_flag), _lib.stream())
+        _lib.call("nvol_adam_train_step", _lib.ptr(model.flat_params), _lib.ptr(model.flat_grads),
+                  _lib.ptr(model.flat_m), _lib.ptr(model.flat_v), model.flat_size, _lib.ptr(pipe.sched),
+                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_flag),
+                  _lib.ptr(pipe.acc), None, pipe.t0, 0, 1.0 / B, _lib.ptr(pipe.ticket), _lib.stream())
         ev[1].record(stream)
 
     t_sample = float(_event_ms(torch, sample_fn)[0])
     t_adam = float(_event_ms(torch, adam_fn)[0])
-    kernels = {"sample_incore_kernel": t_sample, "adam_flat_kernel": t_adam}
+    kernels = {"sample_incore_kernel": t_sample, "adam_step_kernel": t_adam}
     if args.mode == 1:
         st = _event_ms(torch, stages_fn, nev=5)
         kernels.update({"encode_tiles_kernel": float(st[0]), "mlp_tc_kernel": float(st[1] - st[0]),
@@ -257,7 +258,7 @@ def run_ours(args):
     mlp_flops = 3 * 2 * B * (32 * 64 + 3 * 64 * 64 + 64)
     # roofline of the dominant single kernel
     dom = max(kernels, key=kernels.get)
-    per_unit = {"adam_flat_kernel": (adam_bytes, "hbm", "32 B/param x 12,181,396 flat params"),
+    per_unit = {"adam_step_kernel": (adam_bytes, "hbm", "32 B/param x 12,181,396 flat params"),
                 "scatter_kernel": (2 * gather_bytes, "hbm", "16 levels x 8 corners x 2 feat x 4 B x 2 (RMW) per sample"),
                 "encode_tiles_kernel": (gather_bytes + B * 12 + B * 64 * 2, "hbm",
                                         "1,024 B gathered + 12 B coords + 128 B fp16 tiles per sample"),

@@ -220,6 +220,13 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
  * n = 0 disables.  [host] array of event handles. */
 int nvol_set_stage_events(void *const *events, int32_t n);
 
+/* L2 set-aside for persisting lines (cudaLimitPersistingL2CacheSize): the
+ * training step keeps its flat gradient L2-resident between Adam and the
+ * encoder-backward scatter (evict_last policies).  Requests `bytes`, clamped
+ * to the device maximum; returns the bytes set (>= 0) or -1 on error.
+ * Device-wide setting.  No reference counterpart (GPU residency control). */
+int64_t nvol_l2_persist(int64_t bytes);
+
 /* Workspace bytes nvol_train_fwd_bwd needs for batch b. */
 int64_t nvol_train_workspace_bytes(int64_t b, int32_t n_levels, int32_t n_feat, int32_t n_neurons,
                                    int32_t n_hidden, int32_t mode);
@@ -232,6 +239,17 @@ int nvol_adam_flat_dev(float *p, float *g, float *m, float *v, int64_t n, const 
                        int64_t sched_len, int64_t *step_counter, float beta1, float one_minus_beta1,
                        float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
                        void *stream);
+
+/* The training pipeline's step tail in one launch: nvol_adam_flat_dev's
+ * update, then (last block to finish, via the zero-initialised u32 *ticket)
+ * losses[*step_counter - t0] = *loss_acc * inv_b (if 0 <= index < cap),
+ * *loss_acc = 0 and ++*step_counter — i.e. nvol_loss_record + Adam + counter
+ * advance of trainer.py:61-77 / network.py:160-183 without extra launches. */
+int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, const float *sched,
+                         int64_t sched_len, int64_t *step_counter, float beta1, float one_minus_beta1,
+                         float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
+                         double *loss_acc, double *losses, int64_t t0, int64_t cap, double inv_b,
+                         uint32_t *ticket, void *stream);
 
 /* ------------------------------------------------------------------ rendering */
 

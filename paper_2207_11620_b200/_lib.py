@@ -48,14 +48,18 @@ _SIGS = {
     "nvol_train_fwd_bwd": [P, P, I64, I64, P, P, P, P, P, P, I32, I32, I32, I32, I32, I32, P, P, I64, I32, P],
     "nvol_train_workspace_bytes": [I64, I32, I32, I32, I32, I32],
     "nvol_adam_flat_dev": [P, P, P, P, I64, P, I64, P, F32, F32, F32, F32, F32, F32, P, P],
+    "nvol_adam_train_step": [P, P, P, P, I64, P, I64, P, F32, F32, F32, F32, F32, F32, P, P, P, I64, I64, F64, P,
+                             P],
     "nvol_render_workspace_bytes": [I64, I32],
     "nvol_set_stage_events": [P, I32],
+    "nvol_l2_persist": [I64],
     "nvol_render": [P, P, P, P, I32, P, P, I32, P, I64, I64, I64, I32, P, I64, I64, I64, P, P, P, P, P, I32, I32,
                     P, P, I32, I32, I32, I32, P, P, P, I64, P, P, I32, P],
     "nvol_macrocell_ranges": [P, I64, I64, I64, I64, I32, P, P, P],
     "nvol_macrocell_set_tf": [P, P, I64, P, P, I32, F64, P, P],
 }
 _RESTYPES = {"nvol_last_error": ctypes.c_char_p, "nvol_train_workspace_bytes": I64, "nvol_mlp_image_bytes": I64,
+             "nvol_l2_persist": I64,
              "nvol_render_workspace_bytes": I64}
 
 EXPORTS = tuple(_SIGS)

@@ -247,6 +247,85 @@ __global__ void __launch_bounds__(256) adam_flat_kernel(
     if (nan_flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan_flag, 1u);
 }
 
+#ifndef NVOL_ADAM_UNROLL2
+#define NVOL_ADAM_UNROLL2 0
+#endif
+// Training-pipeline Adam step: adam_flat_kernel's update plus the step's bookkeeping in the last block to
+// finish (ticket): losses[t - t0] = loss_sum / B, loss_sum = 0, t += 1.  Every
+// block reads t before taking its ticket, so the advance cannot race a reader.
+__global__ void __launch_bounds__(256) adam_step_kernel(
+    float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v, int64_t n,
+    const float *__restrict__ sched, int64_t sched_len, int64_t *__restrict__ step_counter, float b1, float omb1,
+    float b2, float omb2, float eps, float l2, uint32_t *__restrict__ nan_flag, double *__restrict__ loss_acc,
+    double *__restrict__ losses, int64_t t0, int64_t cap, double inv_b, uint32_t *__restrict__ ticket) {
+    const int64_t tc = *step_counter;
+    const int64_t t = tc >= sched_len ? sched_len - 1 : tc;
+    const float lr = sched[3 * t], c1 = sched[3 * t + 1], c2 = sched[3 * t + 2];
+    const int64_t n4 = n >> 2;
+    bool bad = false;
+    float4 *p4 = reinterpret_cast<float4 *>(p), *g4 = reinterpret_cast<float4 *>(g);
+    float4 *m4 = reinterpret_cast<float4 *>(m), *v4 = reinterpret_cast<float4 *>(v);
+    const uint64_t keep = l2_evict_last();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    auto upd = [&](float4 &P, float4 &G, float4 &M, float4 &V) {
+        bad |= isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w);
+        adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+    };
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+#if NVOL_ADAM_UNROLL2
+    for (; j + stride < n4; j += 2 * stride) {
+        const int64_t k = j + stride;
+        float4 P0 = __ldcs(p4 + j), P1 = __ldcs(p4 + k);
+        float4 G0 = ld4_hint(g4 + j, keep), G1 = ld4_hint(g4 + k, keep);
+        float4 M0 = __ldcs(m4 + j), M1 = __ldcs(m4 + k);
+        float4 V0 = __ldcs(v4 + j), V1 = __ldcs(v4 + k);
+        upd(P0, G0, M0, V0);
+        upd(P1, G1, M1, V1);
+        __stcs(p4 + j, P0);
+        __stcs(p4 + k, P1);
+        st4_hint(g4 + j, G0, keep);
+        st4_hint(g4 + k, G1, keep);
+        __stcs(m4 + j, M0);
+        __stcs(m4 + k, M1);
+        __stcs(v4 + j, V0);
+        __stcs(v4 + k, V1);
+    }
+#endif
+    for (; j < n4; j += stride) {
+        float4 P = __ldcs(p4 + j), G = ld4_hint(g4 + j, keep), M = __ldcs(m4 + j), V = __ldcs(v4 + j);
+        upd(P, G, M, V);
+        __stcs(p4 + j, P);
+        st4_hint(g4 + j, G, keep);
+        __stcs(m4 + j, M);
+        __stcs(v4 + j, V);
+    }
+    for (int64_t q = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+        float P = p[q], G = g[q], M = m[q], V = v[q];
+        bad |= isnan(G);
+        adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        p[q] = P;
+        g[q] = G;
+        m[q] = M;
+        v[q] = V;
+    }
+    if (nan_flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan_flag, 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+            __threadfence();
+            const int64_t k = tc - t0;
+            if (losses && k >= 0 && k < cap) losses[k] = *reinterpret_cast<volatile double *>(loss_acc) * inv_b;
+            if (loss_acc) *loss_acc = 0.0;
+            *step_counter = tc + 1;
+            *ticket = 0u;
+        }
+    }
+}
+
 __global__ void step_advance_kernel(int64_t *counter) { *counter += 1; }
 
 __global__ void loss_record_kernel(double *acc, double *losses, const int64_t *counter, int64_t t0, int64_t cap,
@@ -323,6 +402,19 @@ int nvol_loss_and_grad_scaled(const void *pred, const void *target, int64_t b, i
 int nvol_loss_and_grad(const void *pred, const void *target, int64_t b, int32_t kind, void *grad,
                        double *loss_sum, int32_t dtype_bytes, void *stream) {
     return nvol_loss_and_grad_scaled(pred, target, b, b, kind, grad, loss_sum, dtype_bytes, stream);
+}
+
+int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, const float *sched, int64_t sched_len,
+                         int64_t *step_counter, float beta1, float one_minus_beta1, float beta2,
+                         float one_minus_beta2, float eps, float l2, uint32_t *nan_flag, double *loss_acc,
+                         double *losses, int64_t t0, int64_t cap, double inv_b, uint32_t *ticket, void *stream) {
+    NVOL_REQUIRE(p && g && m && v && sched && step_counter && ticket && sched_len >= 1, "null pointer");
+    NVOL_REQUIRE((((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) == 0,
+                 "flat Adam buffers must be 16-byte aligned");
+    adam_step_kernel<<<stream_grid((n + 3) / 4), 256, 0, as_stream(stream)>>>(
+        p, g, m, v, n, sched, sched_len, step_counter, beta1, one_minus_beta1, beta2, one_minus_beta2, eps, l2,
+        nan_flag, loss_acc, losses, t0, cap, inv_b, ticket);
+    return check_launch("adam_train_step");
 }
 
 int nvol_loss_record(double *acc, double *losses, const int64_t *step_counter, int64_t t0, int64_t cap,

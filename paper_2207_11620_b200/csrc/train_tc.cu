@@ -44,6 +44,7 @@ constexpr int PP_EPI_WARPS = 16;
 #endif
 constexpr int PP_THREADS = (PP_EPI_WARPS + 1) * 32;
 constexpr int SC_THREADS = 1024;
+constexpr int SC_LG = 4;  // levels per scatter item
 constexpr uint32_t COARSE_BYTES = 48 * 1024;
 
 struct TcShape {
@@ -747,62 +748,83 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
     const uint64_t keep = l2_evict_last();
     for (int q = threadIdx.x; q < coarse_floats; q += SC_THREADS) acc_s[q] = 0.0f;
     __syncthreads();
-    const int m = tab.n_levels, nin = m * NF;
-    const int64_t items = b * m;
+    // One item = one sample x SC_LG consecutive levels (level-group-major, so a
+    // warp shares its level constants): the coordinates and the group's
+    // dL/dfeat are loaded once up front and the group's REDs issue back to
+    // back (fire-and-forget), which keeps many L2 reductions in flight.
+    const int m = tab.n_levels;
+    const int ngrp = (m + SC_LG - 1) / SC_LG;
+    const int64_t items = b * ngrp;
     for (int64_t t = (int64_t)blockIdx.x * SC_THREADS + threadIdx.x; t < items; t += (int64_t)gridDim.x * SC_THREADS) {
-        const int l = (int)(t / b);          // level-major, as the encode kernel
-        const int64_t i = t - (int64_t)l * b;
-        const int32_t res = tab.res[l];
-        const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
-        const bool dense = tab.dense[l] != 0;
-        Cell32 c = cell32(__ldg(coords + 3 * i), __ldg(coords + 3 * i + 1), __ldg(coords + 3 * i + 2), res);
-        float d[NF];
+        const int grp = (int)(t / b);
+        const int64_t i = t - (int64_t)grp * b;
+        const float px = __ldg(coords + 3 * i), py = __ldg(coords + 3 * i + 1), pz = __ldg(coords + 3 * i + 2);
+        float dg[SC_LG][NF];
 #pragma unroll
-        for (int f = 0; f < NF; ++f) d[f] = __ldg(dfeat + (int64_t)(l * NF + f) * stride + i);
-        const bool coarse = l < n_coarse;
-        float *gl = coarse ? acc_s + tab.offset[l] : grads + tab.offset[l];
-        if constexpr (NF == 2) {
-            const uint32_t par = (uint32_t)(tab.offset[l] >> 1) & 1u;
-            if (!coarse) {
-                // fine levels: x-adjacent corner pairs in one aligned 16-byte
-                // entry pair go out as a single float4 RED
+        for (int u = 0; u < SC_LG; ++u) {
+            const int l = grp * SC_LG + u;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) dg[u][f] = l < m ? __ldg(dfeat + (int64_t)(l * NF + f) * stride + i) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < SC_LG; ++u) {
+            const int l = grp * SC_LG + u;
+            if (l >= m) break;
+            const float *d = dg[u];
+            const int32_t res = tab.res[l];
+            const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
+            const bool dense = tab.dense[l] != 0;
+            const Cell32 c = cell32(px, py, pz, res);
+            if (l < n_coarse) {
+                float *gs = acc_s + tab.offset[l];  // shared-typed accumulators of the dense coarse levels
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t slot = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask,
+                                                 dense);
+                    const float w = cw32(c, k);
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) atomicAdd(gs + (size_t)slot * NF + f, w * d[f]);
+                }
+                continue;
+            }
+            float *gl = grads + tab.offset[l];
+            if constexpr (NF == 2) {
+                // x-adjacent corner pairs in one aligned 16-byte entry pair go
+                // out as a single float4 RED
+                const uint32_t par = (uint32_t)(tab.offset[l] >> 1) & 1u;
 #pragma unroll
                 for (int k = 0; k < 8; k += 2) {
                     const uint32_t yo = (k >> 1) & 1, zo = (k >> 2) & 1;
-                    uint32_t s0 = slot32(c.cx, c.cy + yo, c.cz + zo, r1, mask, dense);
-                    uint32_t s1 = slot32(c.cx + 1, c.cy + yo, c.cz + zo, r1, mask, dense);
-                    float w0 = cw32(c, k), w1 = cw32(c, k + 1);
+                    const uint32_t s0 = slot32(c.cx, c.cy + yo, c.cz + zo, r1, mask, dense);
+                    const uint32_t s1 = slot32(c.cx + 1, c.cy + yo, c.cz + zo, r1, mask, dense);
+                    const float w0 = cw32(c, k), w1 = cw32(c, k + 1);
                     const uint32_t lo = min(s0, s1);
-                    if (max(s0, s1) == lo + 1 && ((lo + par) & 1u) == 0u) {   // adjacent and 16-byte aligned
-                        float4 q = s0 == lo ? make_float4(w0 * d[0], w0 * d[1], w1 * d[0], w1 * d[1])
-                                            : make_float4(w1 * d[0], w1 * d[1], w0 * d[0], w0 * d[1]);
+                    if (max(s0, s1) == lo + 1 && ((lo + par) & 1u) == 0u) {  // adjacent and 16-byte aligned
+                        const float4 q = s0 == lo ? make_float4(w0 * d[0], w0 * d[1], w1 * d[0], w1 * d[1])
+                                                  : make_float4(w1 * d[0], w1 * d[1], w0 * d[0], w0 * d[1]);
                         red_add4(gl + 2 * (size_t)lo, q, keep);
                     } else {
                         red_add2(gl + 2 * (size_t)s0, w0 * d[0], w0 * d[1], keep);
                         red_add2(gl + 2 * (size_t)s1, w1 * d[0], w1 * d[1], keep);
                     }
                 }
-                continue;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            uint32_t slot = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask, dense);
-            float w = cw32(c, k);
-            float *g = gl + (size_t)slot * NF;
-            if (coarse) {
-                float *gs = acc_s + tab.offset[l] + (size_t)slot * NF;  // shared-typed: ATOMS, not generic
-#pragma unroll
-                for (int f = 0; f < NF; ++f) atomicAdd(gs + f, w * d[f]);
-            } else if constexpr (NF == 2) {
-                red_add2(g, w * d[0], w * d[1], keep);
-            } else if constexpr (NF == 4 || NF == 8) {
-#pragma unroll
-                for (int q = 0; q < NF / 4; ++q)
-                    red_add4(g + 4 * q, make_float4(w * d[4 * q], w * d[4 * q + 1], w * d[4 * q + 2], w * d[4 * q + 3]),
-                             keep);
             } else {
-                red_add(g, w * d[0], keep);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t slot = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask,
+                                                 dense);
+                    const float w = cw32(c, k);
+                    float *g = gl + (size_t)slot * NF;
+                    if constexpr (NF == 4 || NF == 8) {
+#pragma unroll
+                        for (int q = 0; q < NF / 4; ++q)
+                            red_add4(g + 4 * q,
+                                     make_float4(w * d[4 * q], w * d[4 * q + 1], w * d[4 * q + 2], w * d[4 * q + 3]),
+                                     keep);
+                    } else {
+                        red_add(g, w * d[0], keep);
+                    }
+                }
             }
         }
     }
@@ -1028,6 +1050,21 @@ extern "C" int nvol_debug_timeline(unsigned long long *host, int32_t n) {
                ? 0 : 2;
 }
 #endif
+
+extern "C" int64_t nvol_l2_persist(int64_t bytes) {
+    int dev = 0, maxp = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    size_t want = (size_t)(bytes < 0 ? 0 : bytes);
+    if (want > (size_t)maxp) want = (size_t)maxp;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    return (int64_t)got;
+}
 
 extern "C" int nvol_has_tcgen05(int device) {
     int major = 0, minor = 0;

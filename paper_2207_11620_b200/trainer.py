@@ -72,10 +72,14 @@ class TrainHistory:
 class StepPipeline:
     """Device-resident training steps (model.py:154-174 + sampler.py:263-270 + network.py:160-183).
 
-    One step = sample (rows [row0, row0+b) of the global batch) -> fused
-    forward/backward -> [all-reduce of the flat gradient + loss, when
-    data-parallel] -> loss record -> flat Adam, all reading the device step
-    counter, so a single captured CUDA graph replays every step."""
+    One step = fused forward/backward of the batch sampled for it (rows
+    [row0, row0+b) of the global batch) -> [all-reduce of the flat gradient +
+    loss, when data-parallel] -> Adam + loss record + step-counter advance
+    (one kernel).  The NEXT step's batch is sampled on a side stream while
+    this step's encode / MLP / scatter run (double-buffered coordinates), so
+    sampling leaves the critical path.  Everything reads the device step
+    counter, so two captured CUDA graphs (even / odd buffer parity) replay
+    every step."""
 
     def __init__(self, model: NeuralModel, sampler: InCoreSampler, capacity: int, rank: int = 0, world: int = 1,
                  group=None, use_graph: bool = True):
@@ -88,10 +92,12 @@ class StepPipeline:
         self.B, self.b, self.row0 = B, b, row0
         self.world, self.group = world, group
         dev = model.flat_params.device
-        self.coords = torch.empty((self.b, 3), dtype=torch.float32, device=dev)
-        self.targets = torch.empty(self.b, dtype=torch.float32, device=dev)
+        self.bufs = [(torch.empty((self.b, 3), dtype=torch.float32, device=dev),
+                      torch.empty(self.b, dtype=torch.float32, device=dev)) for _ in range(2)]
+        self.coords, self.targets = self.bufs[0]
         self.t0 = model.opt.t
         self.counter = torch.full((1,), self.t0, dtype=torch.int64, device=dev)
+        self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
         self.u32_base = sampler.rng.u32
         self.capacity = int(capacity)
         self.losses = torch.zeros(self.capacity, dtype=torch.float64, device=dev)
@@ -99,60 +105,84 @@ class StepPipeline:
         self.nan_flag = torch.zeros(1, dtype=torch.int32, device=dev)
         o = model.opt
         rows = []
-        for t in range(self.t0 + self.capacity):
+        for t in range(self.t0 + self.capacity + 1):
             lr, c1, c2 = adam_scalars(o, t)
             rows.append((lr, c1, c2))
         self.sched = torch.tensor(np.asarray(rows, dtype=np.float64).astype(np.float32), device=dev).reshape(-1)
         f = lambda x: float(np.float32(x))  # noqa: E731  dt(...) of network.py:172-181
         self.adam_consts = (f(o.beta1), f(1.0 - o.beta1), f(o.beta2), f(1.0 - o.beta2), f(o.epsilon), f(o.l2_reg))
+        # Optional L2 set-aside for persisting lines (NVOL_L2_PERSIST bytes).  Off by
+        # default: measured on B200 it starves Adam's streaming (step 189 -> 267 us).
+        persist = int(os.environ.get("NVOL_L2_PERSIST", "0"))
+        self.l2_persist = int(_lib.load().nvol_l2_persist(persist)) if persist > 0 else 0
+        self.overlap = os.environ.get("NVOL_SAMPLE_OVERLAP", "1") != "0"
+        self.side = torch.cuda.Stream(device=dev) if self.overlap else None
         self.use_graph = use_graph
-        self.graph = None
+        self.graphs = [None, None]
         self.done = 0
 
-    def _body(self) -> None:
-        m, s = self.model, self.sampler
+    def sample_into(self, parity: int, ahead: int) -> None:
+        """Sample the batch of step (device counter + ahead) into buffer `parity`."""
+        s = self.sampler
         vol = s.volume
         dz, dy, dx = vol.shape
-        _lib.call("nvol_sample_incore_dev", *s.rng.words(), self.u32_base, _lib.ptr(self.counter), self.t0, self.B,
-                  self.row0, self.b, _lib.ptr(vol), dx, dy, dz, _lib.ptr(self.coords), _lib.ptr(self.targets),
-                  _lib.stream())
-        m.fwd_bwd_device(self.coords, self.targets, self.acc, b_global=self.B)
+        c, t = self.bufs[parity]
+        # the kernel offsets by (counter - counter0): counter0 = t0 - ahead
+        _lib.call("nvol_sample_incore_dev", *s.rng.words(), self.u32_base, _lib.ptr(self.counter), self.t0 - ahead,
+                  self.B, self.row0, self.b, _lib.ptr(vol), dx, dy, dz, _lib.ptr(c), _lib.ptr(t), _lib.stream())
+
+    def _body(self, parity: int) -> None:
+        m = self.model
+        main = torch.cuda.current_stream()
+        if self.overlap:
+            self.side.wait_stream(main)                 # fork: next step's batch on the side stream
+            with torch.cuda.stream(self.side):
+                self.sample_into(parity ^ 1, 1)
+        else:
+            self.sample_into(parity, 0)
+        c, t = self.bufs[parity]
+        m.fwd_bwd_device(c, t, self.acc, b_global=self.B)
         if self.world > 1:
             from .distributed import allreduce_grads
             allreduce_grads(m.flat_grads, self.acc, self.group)
-        _lib.call("nvol_loss_record", _lib.ptr(self.acc), _lib.ptr(self.losses), _lib.ptr(self.counter), self.t0,
-                  self.capacity, 1.0 / self.B, _lib.stream())
-        _lib.call("nvol_adam_flat_dev", _lib.ptr(m.flat_params), _lib.ptr(m.flat_grads), _lib.ptr(m.flat_m),
+        if self.overlap:
+            main.wait_stream(self.side)                 # join before the counter advances
+        _lib.call("nvol_adam_train_step", _lib.ptr(m.flat_params), _lib.ptr(m.flat_grads), _lib.ptr(m.flat_m),
                   _lib.ptr(m.flat_v), m.flat_size, _lib.ptr(self.sched), self.sched.numel() // 3,
-                  _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag), _lib.stream())
+                  _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag), _lib.ptr(self.acc),
+                  _lib.ptr(self.losses), self.t0, self.capacity, 1.0 / self.B, _lib.ptr(self.ticket), _lib.stream())
 
     def launches_per_step(self) -> int:
         """Kernels of one step from this library (for the bench's gpu_launches)."""
         if self.model.train_mode == 0:
-            return 1 + 5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 + 2
-        # sample, nchunks x (encode, MLP, scatter), loss record, Adam, step advance
+            return 1 + 5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 + 1
+        # sample (next step's, overlapped), nchunks x (encode, MLP, scatter), Adam step
         # (chunk plan of train_tc.cu make_plan: NVOL_TRAIN_CHUNKS, default 1)
         ntiles = (self.b + 127) // 128
         nc = max(1, min(int(os.environ.get("NVOL_TRAIN_CHUNKS", "1")), 4, ntiles))
         ct = (ntiles + nc - 1) // nc
         nc = (ntiles + ct - 1) // ct
-        return 1 + 3 * nc + 1 + 1 + 1
+        return 1 + 3 * nc + 1
 
     def step(self, n: int = 1) -> None:
         """Enqueue n steps (no host synchronisation)."""
         if self.done + n > self.capacity:
             raise ConfigError(f"pipeline capacity {self.capacity} exceeded")
         for _ in range(n):
-            if self.graph is not None:
-                self.graph.replay()
-            elif self.use_graph and self.done >= 1:
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._body()
-                self.graph = g
-                g.replay()
+            parity = self.done & 1
+            if self.done == 0:
+                if self.overlap:
+                    self.sample_into(0, 0)              # the first batch, on the main stream
+                self._body(parity)                      # eager first step (warms up / lazily allocates)
+            elif not self.use_graph:
+                self._body(parity)
             else:
-                self._body()
+                if self.graphs[parity] is None:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        self._body(parity)
+                    self.graphs[parity] = g
+                self.graphs[parity].replay()
             self.done += 1
 
     def finish(self) -> np.ndarray:
