@@ -30,6 +30,10 @@ __device__ __forceinline__ void encode_exact(float x, float y, float z, const fl
             int64_t slot = vertex_slot(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), res,
                                        tab.entries[l], tab.dense[l] != 0);
             float w = corner_weight<float>(c, k);
+            // w == 0 adds +-0 to a sum that starts at +0: skipping the gather is
+            // bit-exact for finite tables (voxel-centre decodes: every level finer
+            // than the output grid has fx = fy = fz = 0, i.e. one live corner)
+            if (w == 0.0f) continue;
             const float *p = params + tab.offset[l] + slot * n;
             for (int f = 0; f < n; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(p + f)));
         }

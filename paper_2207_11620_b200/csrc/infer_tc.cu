@@ -13,6 +13,8 @@
 // (field.cu) remains available as infer_mode "exact".
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -20,6 +22,7 @@ namespace nvol {
 
 constexpr int IT_THREADS = 256;
 constexpr int IT_TILE = 128;
+constexpr int IT_LB = 4;  // levels whose corner gathers are in flight together
 
 struct InferShape {
     int m, n, nin, ninp, nn, nh, relu_out;
@@ -77,7 +80,7 @@ template <int NF>
 __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
     const float *__restrict__ coords, int64_t b, const float *__restrict__ params, const GridTables tab,
     const InferShape sh, const uint8_t *__restrict__ wimg, int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
-    double lo, double scale, float *__restrict__ out) {
+    double lo, double scale, float *__restrict__ out, int split) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_sh;
@@ -125,44 +128,71 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
             }
         }
         uint8_t *sx = smem + sh.o_x, *sxl = smem + sh.o_xlo;
-        for (int l = l_lo; l < l_hi; ++l) {
-            const int32_t res = tab.res[l];
-            const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
-            const bool dense = tab.dense[l] != 0;
-            const float *tb = params + tab.offset[l];
-            Cell<float> c = cell_of<float>(x, y, z, res);
-            const uint32_t cx = (uint32_t)c.cx, cy = (uint32_t)c.cy, cz = (uint32_t)c.cz;
-            float acc[NF];
+        // levels in batches of IT_LB: every corner load of the batch is issued
+        // before any is consumed (IT_LB x 8 gathers in flight per thread)
+        for (int lb = l_lo; lb < l_hi; lb += IT_LB) {
+            float vals[IT_LB][8][NF];
+            float fxs[IT_LB], fys[IT_LB], fzs[IT_LB];
 #pragma unroll
-            for (int f = 0; f < NF; ++f) acc[f] = 0.0f;
-            uint32_t sl[8];
+            for (int u = 0; u < IT_LB; ++u) {
+                const int l = min(lb + u, l_hi - 1);  // a past-the-end slot recomputes the last level (discarded)
+                {
+                    const int32_t res = tab.res[l];
+                    const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
+                    const bool dense = tab.dense[l] != 0;
+                    const float *tb = params + tab.offset[l];
+                    const Cell<float> c = cell_of<float>(x, y, z, res);
+                    fxs[u] = c.fx;
+                    fys[u] = c.fy;
+                    fzs[u] = c.fz;
+                    const uint32_t cx = (uint32_t)c.cx, cy = (uint32_t)c.cy, cz = (uint32_t)c.cz;
+                    // corners whose weight is exactly 0 contribute w*v = +-0 to a
+                    // sum that starts at +0, i.e. nothing: their gathers are skipped
+                    // (bit-exact for finite tables).  Voxel-centre decodes hit this
+                    // on every level finer than the output grid (fx = fy = fz = 0).
+                    const bool zx = c.fx == 0.0f, zy = c.fy == 0.0f, zz = c.fz == 0.0f;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) sl[k] = slot32i(cx + (k & 1), cy + ((k >> 1) & 1), cz + ((k >> 2) & 1), r1, mask, dense);
-            if constexpr (NF == 2) {
-                float2 v[8];
+                    for (int k = 0; k < 8; ++k) {
+                        const bool skip = ((k & 1) && zx) || ((k & 2) && zy) || ((k & 4) && zz);
+                        const uint32_t sl =
+                            slot32i(cx + (k & 1), cy + ((k >> 1) & 1), cz + ((k >> 2) & 1), r1, mask, dense);
+                        if constexpr (NF == 2) {
+                            const float2 v = skip ? make_float2(0.0f, 0.0f)
+                                                  : __ldg(reinterpret_cast<const float2 *>(tb) + sl);
+                            vals[u][k][0] = v.x;
+                            vals[u][k][1] = v.y;
+                        } else {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = __ldg(reinterpret_cast<const float2 *>(tb) + sl[k]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    float w = corner_weight<float>(c, k);
-                    acc[0] = xadd(acc[0], xmul(w, v[k].x));
-                    acc[1] = xadd(acc[1], xmul(w, v[k].y));
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    float w = corner_weight<float>(c, k);
-#pragma unroll
-                    for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(tb + (size_t)sl[k] * NF + f)));
+                            for (int f = 0; f < NF; ++f) vals[u][k][f] = skip ? 0.0f : __ldg(tb + (size_t)sl * NF + f);
+                        }
+                    }
                 }
             }
 #pragma unroll
-            for (int f = 0; f < NF; ++f) {
-                __half hi, lw;
-                tc::split_f16(valid ? acc[f] * tc::kActScale : 0.0f, hi, lw);
-                const uint32_t o = tc::tile_off(s, l * NF + f, NINP);
-                *reinterpret_cast<__half *>(sx + o) = hi;
-                *reinterpret_cast<__half *>(sxl + o) = lw;
+            for (int u = 0; u < IT_LB; ++u) {
+                const int l = lb + u;
+                if (l < l_hi) {
+                    float acc[NF];
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) acc[f] = 0.0f;
+                    // corner weights in the reference order w = (wx * wy) * wz (_kernels.py:59-61)
+                    const float ox = xsub(1.0f, fxs[u]), oy = xsub(1.0f, fys[u]), oz = xsub(1.0f, fzs[u]);
+                    const float wxy[4] = {xmul(ox, oy), xmul(fxs[u], oy), xmul(ox, fys[u]), xmul(fxs[u], fys[u])};
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float w = xmul(wxy[k & 3], (k & 4) ? fzs[u] : oz);
+#pragma unroll
+                        for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, vals[u][k][f]));
+                    }
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) {
+                        __half hi, lw;
+                        tc::split_f16(valid ? acc[f] * tc::kActScale : 0.0f, hi, lw);
+                        const uint32_t o = tc::tile_off(s, l * NF + f, NINP);
+                        *reinterpret_cast<__half *>(sx + o) = hi;
+                        *reinterpret_cast<__half *>(sxl + o) = lw;
+                    }
+                }
             }
         }
         tc::fence_proxy_async();
@@ -180,22 +210,30 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
                     const uint64_t adh = tc::make_desc(ah + k * 256, 128, sbo), adl = tc::make_desc(al + k * 256, 128, sbo);
                     const uint64_t bdh = tc::make_desc(bh + k * 256, 128, sbo), bdl = tc::make_desc(bl + k * 256, 128, sbo);
                     tc::mma_f16(tmem, adh, bdh, idesc, k > 0);
-                    tc::mma_f16(tlo, adl, bdh, idesc, k > 0);
-                    tc::mma_f16(tlo, adh, bdl, idesc, 1);
+                    if (split) {
+                        tc::mma_f16(tlo, adl, bdh, idesc, k > 0);
+                        tc::mma_f16(tlo, adh, bdl, idesc, 1);
+                    }
                 }
                 tc::mma_commit(&mbar);
             }
-            tc::mbar_wait(&mbar, phase);
+            tc::mbar_wait_sleep(&mbar, phase);
             phase ^= 1;
             tc::fence_after();
             uint8_t *dst = smem + sh.o_h, *dstl = smem + sh.o_hlo;
             for (int c = c0; c < c0 + nc; c += 16) {   // values carry kActScale (see tc.cuh)
                 float v[16], vl[16];
                 tc::tmem_ld16(tmem + lane_base + c, v);
-                tc::tmem_ld16(tlo + lane_base + c, vl);
-                tc::tmem_wait_ld();
+                if (split) {
+                    tc::tmem_ld16(tlo + lane_base + c, vl);
+                    tc::tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
+                    for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
+                } else {
+                    tc::tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e], 0.0f);
+                }
                 if (li < NH - 1) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) vl[e] = (v[e] - __half2float(__float2half_rn(v[e]))) * tc::kLoScale;
@@ -243,6 +281,11 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static int split = -1;
+    if (split < 0) {
+        const char *e = getenv("NVOL_INFER_SPLIT");
+        split = e ? atoi(e) : 1;
+    }
     int64_t ntiles = (b + IT_TILE - 1) / IT_TILE;
     int64_t cap = (int64_t)sms * 2;
     int grid = (int)(ntiles < cap ? ntiles : cap);
@@ -252,7 +295,7 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
     case NFV:                                                                                                  \
         cudaFuncSetAttribute(infer_tc_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes); \
         infer_tc_kernel<NFV><<<grid, IT_THREADS, sh.smem_bytes, s>>>(coords, b, params, tab, sh, wimg, decode, dx, dy, \
-                                                                    dz, z0, lo, scale, out);                   \
+                                                                    dz, z0, lo, scale, out, split);            \
         break;
         LAUNCH_IT(1)
         LAUNCH_IT(2)
