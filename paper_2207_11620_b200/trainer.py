@@ -89,6 +89,7 @@ class StepPipeline:
         B = model.batch_size
         row0, b = shard_rows(B, rank, world)
         self.model, self.sampler = model, sampler
+        self.train_mode = model.train_mode
         self.B, self.b, self.row0 = B, b, row0
         self.world, self.group = world, group
         dev = model.flat_params.device
@@ -98,7 +99,11 @@ class StepPipeline:
         self.t0 = model.opt.t
         self.counter = torch.full((1,), self.t0, dtype=torch.int64, device=dev)
         self.ticket = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.u32_base = sampler.rng.u32
+        # host feed: any sampler yielding host batches (sampler.py:263-297 protocol);
+        # each step's batch is DMA'd from pinned memory on a copy stream while the
+        # previous step computes, and each step's loss is read back asynchronously
+        self.host_feed = not isinstance(sampler, InCoreSampler)
+        self.u32_base = 0 if self.host_feed else sampler.rng.u32
         self.capacity = int(capacity)
         self.losses = torch.zeros(self.capacity, dtype=torch.float64, device=dev)
         self.acc = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -115,8 +120,15 @@ class StepPipeline:
         # default: measured on B200 it starves Adam's streaming (step 189 -> 267 us).
         persist = int(os.environ.get("NVOL_L2_PERSIST", "0"))
         self.l2_persist = int(_lib.load().nvol_l2_persist(persist)) if persist > 0 else 0
-        self.overlap = os.environ.get("NVOL_SAMPLE_OVERLAP", "1") != "0"
+        self.overlap = (not self.host_feed) and os.environ.get("NVOL_SAMPLE_OVERLAP", "1") != "0"
         self.side = torch.cuda.Stream(device=dev) if self.overlap else None
+        if self.host_feed:
+            self.copy_stream = torch.cuda.Stream(device=dev)
+            self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+            self.free = [torch.cuda.Event(), torch.cuda.Event()]
+            self.staged = [None, None]          # host tensors whose DMA may still be in flight
+            self.staging = [None, None]         # pinned staging for non-pinned host batches
+            self.loss_host = torch.zeros(self.capacity, dtype=torch.float64).pin_memory()
         self.use_graph = use_graph
         self.graphs = [None, None]
         self.done = 0
@@ -131,10 +143,45 @@ class StepPipeline:
         _lib.call("nvol_sample_incore_dev", *s.rng.words(), self.u32_base, _lib.ptr(self.counter), self.t0 - ahead,
                   self.B, self.row0, self.b, _lib.ptr(vol), dx, dy, dz, _lib.ptr(c), _lib.ptr(t), _lib.stream())
 
+    def _feed(self, parity: int) -> None:
+        """H2D of this step's host batch into device buffer `parity` (copy stream)."""
+        batch = self.sampler.sample(self.B)
+        if len(batch) != self.B:
+            raise ConfigError(f"batch size {len(batch)} != configured {self.B}")
+        hc, ht = batch.coords, batch.targets
+        r0, r1 = self.row0, self.row0 + self.b
+        on_device = isinstance(hc, torch.Tensor) and hc.is_cuda
+        if on_device:
+            hc = hc.to(torch.float32)[r0:r1]
+            ht = ht.to(torch.float32)[r0:r1]
+            self.copy_stream.wait_stream(torch.cuda.current_stream())
+        elif not (isinstance(hc, torch.Tensor) and hc.is_pinned() and hc.dtype == torch.float32
+                  and isinstance(ht, torch.Tensor) and ht.is_pinned() and ht.dtype == torch.float32):
+            if self.staging[parity] is None:
+                self.staging[parity] = (torch.empty((self.b, 3), dtype=torch.float32).pin_memory(),
+                                        torch.empty(self.b, dtype=torch.float32).pin_memory())
+            self.ready[parity].synchronize()    # the staging buffer's previous DMA is done
+            sc, st = self.staging[parity]
+            sc.numpy()[...] = np.asarray(hc[r0:r1], dtype=np.float32)
+            st.numpy()[...] = np.asarray(ht[r0:r1], dtype=np.float32)
+            hc, ht = sc, st
+        elif not on_device:
+            hc, ht = hc[r0:r1], ht[r0:r1]
+        c, t = self.bufs[parity]
+        self.copy_stream.wait_event(self.free[parity])   # the step that last read this buffer is done
+        with torch.cuda.stream(self.copy_stream):
+            c.copy_(hc, non_blocking=True)
+            t.copy_(ht, non_blocking=True)
+        self.ready[parity].record(self.copy_stream)
+        self.staged[parity] = (hc, ht)
+        torch.cuda.current_stream().wait_event(self.ready[parity])
+
     def _body(self, parity: int) -> None:
         m = self.model
         main = torch.cuda.current_stream()
-        if self.overlap:
+        if self.host_feed:
+            pass
+        elif self.overlap:
             self.side.wait_stream(main)                 # fork: next step's batch on the side stream
             with torch.cuda.stream(self.side):
                 self.sample_into(parity ^ 1, 1)
@@ -170,6 +217,8 @@ class StepPipeline:
             raise ConfigError(f"pipeline capacity {self.capacity} exceeded")
         for _ in range(n):
             parity = self.done & 1
+            if self.host_feed:
+                self._feed(parity)
             if self.done == 0:
                 if self.overlap:
                     self.sample_into(0, 0)              # the first batch, on the main stream
@@ -183,21 +232,49 @@ class StepPipeline:
                         self._body(parity)
                     self.graphs[parity] = g
                 self.graphs[parity].replay()
+            if self.host_feed:
+                main = torch.cuda.current_stream()
+                self.free[parity].record(main)
+                self.loss_host[self.done:self.done + 1].copy_(self.losses[self.done:self.done + 1], non_blocking=True)
             self.done += 1
 
     def finish(self) -> np.ndarray:
         """Synchronise, commit host-side state, return the per-step losses."""
-        losses = self.losses[:self.done].cpu().numpy()
+        if self.host_feed:
+            torch.cuda.current_stream().synchronize()
+            losses = self.loss_host[:self.done].numpy().copy()
+            self.staged = [None, None]
+        else:
+            losses = self.losses[:self.done].cpu().numpy()
+            self.sampler.rng.u32 = self.u32_base + 3 * self.B * self.done
         self.model.opt.t = self.t0 + self.done
-        self.sampler.rng.u32 = self.u32_base + 3 * self.B * self.done
         if int(self.nan_flag.item()):
             raise FloatingPointError("NaN gradient encountered during device-resident training")
         return losses
 
 
+def _cached_pipeline(model: NeuralModel, sampler, steps: int) -> "StepPipeline":
+    """Reuse the model's pipeline (and its captured graphs) across train() calls
+    while nothing it baked in changed: same sampler object, optimizer step and
+    (device sampling) stream position, and capacity left."""
+    p = getattr(model, "_pipeline", None)
+    if p is not None:
+        ok = (p.sampler is sampler and p.t0 + p.done == model.opt.t and p.done + steps <= p.capacity
+              and p.train_mode == model.train_mode and p.B == model.batch_size
+              and (p.host_feed or sampler.rng.u32 == p.u32_base + 3 * p.B * p.done))
+        if ok:
+            return p
+    p = StepPipeline(model, sampler, max(steps, 256))
+    model._pipeline = p
+    return p
+
+
 def _fast_path(model, sampler, tap) -> bool:
-    return (tap is None and model._use_kernels() and isinstance(sampler, InCoreSampler)
-            and sampler.interpolation == "trilinear")
+    if tap is not None or not model._use_kernels():
+        return False
+    if isinstance(sampler, InCoreSampler):
+        return sampler.interpolation == "trilinear"
+    return os.environ.get("NVOL_HOST_FEED", "1") != "0"   # host batches: the H2D-overlapped pipeline
 
 
 def train(model: NeuralModel, sampler, steps: int, tap=None, log_every: int = 0) -> TrainHistory:
@@ -207,10 +284,11 @@ def train(model: NeuralModel, sampler, steps: int, tap=None, log_every: int = 0)
     history = TrainHistory()
     if _fast_path(model, sampler, tap):
         t0 = model.opt.t
-        pipe = StepPipeline(model, sampler, steps)
+        pipe = _cached_pipeline(model, sampler, steps)
         start = time.perf_counter()
+        first = pipe.done
         pipe.step(steps)
-        losses = pipe.finish()
+        losses = pipe.finish()[first:]
         ms = (time.perf_counter() - start) * 1e3 / steps
         for k in range(steps):
             history.append(t0 + k, float(losses[k]), lr_at(model.opt, t0 + k), ms)

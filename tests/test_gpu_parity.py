@@ -241,6 +241,48 @@ def test_train_step_api_matches_pipeline(nv):
     assert a.opt.t == b.opt.t == 5
 
 
+def test_host_feed_pipeline_matches_train_step(nv):
+    """trainer.train over a host sampler (H2D-overlapped graph pipeline, async loss
+    read-back) == model.train_step per batch on the same batches; a second train()
+    call reuses the cached pipeline and continues the trajectory."""
+    from paper_2207_11620_b200 import fields, trainer
+    from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
+    from paper_2207_11620_b200.sampler import InCoreSampler, SampleBatch
+    cfg = {"encoding": {"otype": "HashGrid", "n_levels": 4, "n_features_per_level": 2,
+                        "log2_hashmap_size": 12, "base_resolution": 4},
+           "network": {"n_neurons": 16, "n_hidden_layers": 2}, "batch_size": 4096}
+    fld = fields.rasterize("mlobb", (24, 24, 24), host=True)
+    src = InCoreSampler(fld, seed=1)
+    batches = []
+    for i in range(8):
+        bt = src.sample(4096)
+        c, t = bt.coords.cpu(), bt.targets.cpu()
+        # mix numpy (staged) and pinned-tensor (direct DMA) host batches
+        batches.append(SampleBatch(c.numpy(), t.numpy()) if i % 2 else SampleBatch(c.pin_memory(), t.pin_memory()))
+
+    class Feed:
+        def __init__(self):
+            self.i = 0
+
+        def sample(self, b):
+            self.i += 1
+            return batches[self.i - 1]
+
+    for mode in (0, MODE_TCGEN05):
+        a = build_model(cfg, dims=(24, 24, 24), seed=0)
+        b = build_model(cfg, dims=(24, 24, 24), seed=0)
+        a.train_mode = b.train_mode = mode
+        la = [a.train_step(bt) for bt in batches]
+        feed = Feed()
+        h1 = trainer.train(b, feed, steps=5)
+        h2 = trainer.train(b, feed, steps=3)
+        lb = list(h1.losses) + list(h2.losses)
+        assert la[0] == pytest.approx(lb[0], rel=1e-6)
+        np.testing.assert_allclose(la, lb, rtol=1e-3)
+        assert a.opt.t == b.opt.t == 8
+        np.testing.assert_allclose(b.flat_params.cpu().numpy(), a.flat_params.cpu().numpy(), rtol=0, atol=1e-4)
+
+
 def test_decode_invariants(nv):
     from paper_2207_11620_b200 import trainer
     from paper_2207_11620_b200.model import build_model
