@@ -144,6 +144,23 @@ int nvol_sample_incore_dev(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi
                            const float *volume, int64_t dx, int64_t dy, int64_t dz, float *coords,
                            float *targets, void *stream);
 
+/* nvol_sample_incore_dev with the online macro-cell update fused in
+ * (macrocell.py:101-133 macrocell_update_online on each sampled row, as the
+ * reference's live session does per training step, service.py:279): every
+ * row's target widens value_lo / value_hi [gz][gy][gx] (cells of n_g voxels)
+ * with exact int-ordered atomics.  mc_lo = NULL disables the update. */
+int nvol_sample_incore_dev_mc(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                              uint64_t u32_base, const int64_t *step_counter, int64_t counter0,
+                              int64_t b_global, int64_t row0, int64_t b, const float *volume, int64_t dx,
+                              int64_t dy, int64_t dz, float *coords, float *targets, float *mc_lo, float *mc_hi,
+                              int64_t gx, int64_t gy, int64_t gz, int64_t n_g, void *stream);
+
+/* macrocell.py:101-133 macrocell_update_online for a batch already on the device
+ * (coords f32 [n,3], targets f32 [n] in [0,1]); bit-exact with the reference. */
+int nvol_macrocell_update_online(const float *coords, const float *targets, int64_t n, int64_t dx, int64_t dy,
+                                 int64_t dz, float *lo, float *hi, int64_t gx, int64_t gy, int64_t gz,
+                                 int64_t n_g, void *stream);
+
 /* volume.py:167-171 sample_trilinear_many (no clamp). */
 int nvol_trilinear(const float *volume, int64_t dx, int64_t dy, int64_t dz, const float *pts,
                    int64_t n, float *out, void *stream);

@@ -129,6 +129,25 @@ def ranges_from_array(norm, dims, ng):
     return lo, hi
 
 
+def update_online(lo, hi, coords, targets, dims, ng):
+    """macrocell.py:101-133 macrocell_update_online (in place on lo / hi)."""
+    gx, gy, gz = grid_dims(dims, ng)
+    d = np.array(dims, dtype=np.float32)
+    s = coords.astype(np.float32) * d - np.float32(0.5)
+    i0 = np.floor(s).astype(np.int64)
+    vmax = np.array(dims, dtype=np.int64) - 1
+    v_lo = np.clip(i0, 0, vmax)
+    v_hi = np.clip(i0 + (s > i0.astype(np.float32)), 0, vmax)
+    bound = np.array((gx, gy, gz), dtype=np.int64) - 1
+    c_lo = np.clip((v_hi + ng - 1) // ng - 1, 0, bound)
+    c_hi = np.clip((v_lo + 1) // ng, 0, bound)
+    flat = np.concatenate([(iz * gy + iy) * gx + ix for iz in (c_lo[:, 2], c_hi[:, 2])
+                           for iy in (c_lo[:, 1], c_hi[:, 1]) for ix in (c_lo[:, 0], c_hi[:, 0])])
+    t = np.tile(targets.astype(np.float32), 8)
+    np.minimum.at(lo.reshape(-1), flat, t)
+    np.maximum.at(hi.reshape(-1), flat, t)
+
+
 def voxel_centre_coords(dims):
     """macrocell.py:87-94: centres computed in float64, then cast to float32."""
     dx, dy, dz = dims

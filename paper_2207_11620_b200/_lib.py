@@ -38,6 +38,9 @@ _SIGS = {
     "nvol_find_nan": [P, I64, P, I32, P],
     "nvol_sample_incore": [U64, U64, U64, U64, U64, I64, P, I64, I64, I64, P, P, P],
     "nvol_sample_incore_dev": [U64, U64, U64, U64, U64, P, I64, I64, I64, I64, P, I64, I64, I64, P, P, P],
+    "nvol_sample_incore_dev_mc": [U64, U64, U64, U64, U64, P, I64, I64, I64, I64, P, I64, I64, I64, P, P, P, P,
+                                  I64, I64, I64, I64, P],
+    "nvol_macrocell_update_online": [P, P, I64, I64, I64, I64, P, P, I64, I64, I64, I64, P],
     "nvol_trilinear": [P, I64, I64, I64, P, I64, P, P],
     "nvol_rasterize": [I32, I64, I64, I64, I64, I64, P, I32, P],
     "nvol_sq_err_sum": [P, P, I64, P, P],

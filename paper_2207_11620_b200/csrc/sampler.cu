@@ -29,6 +29,52 @@ static PcgJump make_jump(U128 inc) {
     return j;
 }
 
+// macrocell.py:101-133 macrocell_update_online for one sample: widen the
+// value range of every cell whose bordered scan window contains the sample's
+// trilinear stencil (the containing cell, plus a neighbour where the stencil
+// straddles a cell boundary).  Stencil arithmetic is the float32 lookup path
+// (s = p*D - 0.5, two roundings).  Targets are in [0, 1], so IEEE order equals
+// signed-int order of the bit patterns (lo starts at +inf, hi at -inf): int
+// atomicMin / atomicMax are exact and order-independent (bit-exact with the
+// reference's np.minimum.at / np.maximum.at).
+struct McGrid {
+    float *lo, *hi;
+    int64_t gx, gy, gz, n_g;
+};
+
+__device__ __forceinline__ void mc_widen(const McGrid &g, int64_t dx, int64_t dy, int64_t dz, float px, float py,
+                                         float pz, float t) {
+    const float ps[3] = {px, py, pz};
+    const int64_t dims[3] = {dx, dy, dz}, gd[3] = {g.gx, g.gy, g.gz};
+    int64_t clo[3], chi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float sa = xsub(xmul(ps[a], (float)dims[a]), 0.5f);
+        const int64_t i0 = (int64_t)floorf(sa);
+        const int64_t vmax = dims[a] - 1;
+        const int64_t vlo = min(max(i0, (int64_t)0), vmax);
+        const int64_t vhi = min(max(i0 + (sa > (float)i0 ? 1 : 0), (int64_t)0), vmax);
+        const int64_t bound = gd[a] - 1;
+        // floor division of non-negative values
+        clo[a] = min(max((vhi + g.n_g - 1) / g.n_g - 1, (int64_t)0), bound);
+        chi[a] = min(max((vlo + 1) / g.n_g, (int64_t)0), bound);
+    }
+    const int ti = __float_as_int(t);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int64_t ix = (k & 1) ? chi[0] : clo[0], iy = (k & 2) ? chi[1] : clo[1], iz = (k & 4) ? chi[2] : clo[2];
+        const int64_t c = (iz * g.gy + iy) * g.gx + ix;
+        atomicMin(reinterpret_cast<int *>(g.lo) + c, ti);
+        atomicMax(reinterpret_cast<int *>(g.hi) + c, ti);
+    }
+}
+
+__global__ void mc_update_kernel(const float *__restrict__ coords, const float *__restrict__ targets, int64_t n,
+                                 int64_t dx, int64_t dy, int64_t dz, const McGrid g) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) mc_widen(g, dx, dy, dz, coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], targets[i]);
+}
+
 // One thread per row: the row's three u32 draws are u32 indices g0..g0+2 of
 // the stream (sample i, axis a -> 3i+a); they live in u64 outputs g0>>1 and
 // (g0+2)>>1.  The GT read is the bit-exact trilinear of volume.py:148-164,
@@ -39,7 +85,7 @@ __global__ void __launch_bounds__(256) sample_incore_kernel(U128 s0, U128 inc, c
                                                             int64_t b,
                                                             const float *__restrict__ vol, int64_t dx,
                                                             int64_t dy, int64_t dz, float *__restrict__ coords,
-                                                            float *__restrict__ targets) {
+                                                            float *__restrict__ targets, const McGrid mc) {
     __shared__ U128 sm_mult[64], sm_plus[64];
     if (threadIdx.x < 64) {
         sm_mult[threadIdx.x] = jump.mult[threadIdx.x];
@@ -77,8 +123,9 @@ __global__ void __launch_bounds__(256) sample_incore_kernel(U128 s0, U128 inc, c
     coords[3 * r] = x;
     coords[3 * r + 1] = y;
     coords[3 * r + 2] = z;
-    const float t = trilinear_at(vol, dx, dy, dz, x, y, z);
-    targets[r] = fminf(fmaxf(t, 0.0f), 1.0f);
+    const float t = fminf(fmaxf(trilinear_at(vol, dx, dy, dz, x, y, z), 0.0f), 1.0f);
+    targets[r] = t;
+    if (mc.lo) mc_widen(mc, dx, dy, dz, x, y, z, t);  // online macro-cells fused into the sampler
 }
 
 static const PcgJump &jump_for(U128 inc) {
@@ -184,8 +231,23 @@ int nvol_sample_incore(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, ui
     const U128 inc{inc_hi, inc_lo};
     sample_incore_kernel<<<grid_for(b, 256), 256, 0, as_stream(stream)>>>(
         U128{state_hi, state_lo}, inc, jump_for(inc), u32_offset, nullptr, 0, 0, 0, b, volume, dx, dy, dz,
-        coords, targets);
+        coords, targets, McGrid{nullptr, nullptr, 0, 0, 0, 1});
     return check_launch("sample_incore");
+}
+
+int nvol_sample_incore_dev_mc(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                              uint64_t u32_base, const int64_t *step_counter, int64_t counter0, int64_t b_global,
+                              int64_t row0, int64_t b, const float *volume, int64_t dx, int64_t dy, int64_t dz,
+                              float *coords, float *targets, float *mc_lo, float *mc_hi, int64_t gx, int64_t gy,
+                              int64_t gz, int64_t n_g, void *stream) {
+    NVOL_REQUIRE(b >= 1 && step_counter, "bad arguments");
+    NVOL_REQUIRE(volume && coords && targets, "null pointer");
+    NVOL_REQUIRE(!mc_lo || (mc_hi && n_g >= 1 && gx >= 1 && gy >= 1 && gz >= 1), "bad macro-cell grid");
+    const U128 inc{inc_hi, inc_lo};
+    sample_incore_kernel<<<grid_for(b, 256), 256, 0, as_stream(stream)>>>(
+        U128{state_hi, state_lo}, inc, jump_for(inc), u32_base, step_counter, counter0, b_global, row0, b, volume,
+        dx, dy, dz, coords, targets, McGrid{mc_lo, mc_hi, gx, gy, gz, n_g});
+    return check_launch("sample_incore_dev");
 }
 
 int nvol_sample_incore_dev(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
@@ -193,13 +255,20 @@ int nvol_sample_incore_dev(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi
                            int64_t row0, int64_t b,
                            const float *volume, int64_t dx, int64_t dy, int64_t dz, float *coords, float *targets,
                            void *stream) {
-    NVOL_REQUIRE(b >= 1 && step_counter, "bad arguments");
-    NVOL_REQUIRE(volume && coords && targets, "null pointer");
-    const U128 inc{inc_hi, inc_lo};
-    sample_incore_kernel<<<grid_for(b, 256), 256, 0, as_stream(stream)>>>(
-        U128{state_hi, state_lo}, inc, jump_for(inc), u32_base, step_counter, counter0, b_global, row0, b, volume,
-        dx, dy, dz, coords, targets);
-    return check_launch("sample_incore_dev");
+    return nvol_sample_incore_dev_mc(state_hi, state_lo, inc_hi, inc_lo, u32_base, step_counter, counter0, b_global,
+                                     row0, b, volume, dx, dy, dz, coords, targets, nullptr, nullptr, 0, 0, 0, 1,
+                                     stream);
+}
+
+int nvol_macrocell_update_online(const float *coords, const float *targets, int64_t n, int64_t dx, int64_t dy,
+                                 int64_t dz, float *lo, float *hi, int64_t gx, int64_t gy, int64_t gz, int64_t n_g,
+                                 void *stream) {
+    if (n == 0) return NVOL_OK;
+    NVOL_REQUIRE(coords && targets && lo && hi, "null pointer");
+    NVOL_REQUIRE(n_g >= 1 && gx >= 1 && gy >= 1 && gz >= 1 && dx >= 1 && dy >= 1 && dz >= 1, "bad grid");
+    mc_update_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(coords, targets, n, dx, dy, dz,
+                                                                      McGrid{lo, hi, gx, gy, gz, n_g});
+    return check_launch("macrocell_update_online");
 }
 
 int nvol_trilinear(const float *volume, int64_t dx, int64_t dy, int64_t dz, const float *pts, int64_t n, float *out,

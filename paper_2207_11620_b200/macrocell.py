@@ -84,34 +84,32 @@ def macrocell_from_model(model, n_g: int = DEFAULT_CELL_SIZE, chunk: int = 0) ->
 
 
 def macrocell_update_online(grid: MacroCellGrid, batch) -> None:
-    """Widen cell ranges with a training batch (macrocell.py:101-133), on the device."""
-    c = batch.coords if isinstance(batch.coords, torch.Tensor) else torch.as_tensor(batch.coords)
-    t = batch.targets if isinstance(batch.targets, torch.Tensor) else torch.as_tensor(batch.targets)
-    if c.shape[0] == 0:
+    """Widen cell ranges with a training batch (macrocell.py:101-133), on the device
+    (nvol_macrocell_update_online: int-ordered atomic min / max, bit-exact)."""
+    c = batch.coords if isinstance(batch.coords, torch.Tensor) else torch.as_tensor(np.asarray(batch.coords))
+    t = batch.targets if isinstance(batch.targets, torch.Tensor) else torch.as_tensor(np.asarray(batch.targets))
+    n = int(c.shape[0])
+    if n == 0:
         return
     dev = grid.value_lo.device
-    c = c.to(dev, torch.float32)
-    t = t.to(dev, torch.float32)
+    c = c.to(dev, torch.float32).contiguous()
+    t = t.to(dev, torch.float32).contiguous()
+    dx, dy, dz = grid.vol_dims
     gx, gy, gz = grid.grid_dims
-    n = grid.n_g
-    dims = torch.tensor(grid.vol_dims, dtype=torch.float32, device=dev)
-    s = c * dims - 0.5
-    i0 = torch.floor(s).to(torch.int64)
-    vmax = torch.tensor(grid.vol_dims, dtype=torch.int64, device=dev) - 1
-    zero = torch.zeros_like(vmax)
-    v_lo = torch.minimum(torch.maximum(i0, zero), vmax)
-    v_hi = torch.minimum(torch.maximum(i0 + (s > i0.to(torch.float32)).to(torch.int64), zero), vmax)
-    bound = torch.tensor((gx, gy, gz), dtype=torch.int64, device=dev) - 1
-    c_lo = torch.minimum(torch.maximum(torch.div(v_hi + n - 1, n, rounding_mode="floor") - 1, zero), bound)
-    c_hi = torch.minimum(torch.maximum(torch.div(v_lo + 1, n, rounding_mode="floor"), zero), bound)
-    flat = torch.cat([(iz * gy + iy) * gx + ix
-                      for iz in (c_lo[:, 2], c_hi[:, 2]) for iy in (c_lo[:, 1], c_hi[:, 1])
-                      for ix in (c_lo[:, 0], c_hi[:, 0])])
-    tt = t.repeat(8)
-    lo = grid.value_lo.view(-1)
-    hi = grid.value_hi.view(-1)
-    lo.scatter_reduce_(0, flat, tt, reduce="amin")
-    hi.scatter_reduce_(0, flat, tt, reduce="amax")
+    _lib.call("nvol_macrocell_update_online", _lib.ptr(c), _lib.ptr(t), n, dx, dy, dz, _lib.ptr(grid.value_lo),
+              _lib.ptr(grid.value_hi), gx, gy, gz, grid.n_g, _lib.stream())
+
+
+class OnlineMacrocells:
+    """Training tap `tap(batch) = macrocell_update_online(grid, batch)` (the
+    reference's live session, service.py:279).  trainer.train recognises it and
+    fuses the update into the device sampler kernel (no extra launch)."""
+
+    def __init__(self, grid: MacroCellGrid):
+        self.grid = grid
+
+    def __call__(self, batch) -> None:
+        macrocell_update_online(self.grid, batch)
 
 
 def macrocell_set_tf(grid: MacroCellGrid, tf: TransferFunction) -> None:

@@ -82,7 +82,7 @@ class StepPipeline:
     every step."""
 
     def __init__(self, model: NeuralModel, sampler: InCoreSampler, capacity: int, rank: int = 0, world: int = 1,
-                 group=None, use_graph: bool = True):
+                 group=None, use_graph: bool = True, mc_grid=None):
         if not model._use_kernels():
             raise ConfigError("the device pipeline needs a float32 grid model")
         from .distributed import shard_rows
@@ -120,7 +120,12 @@ class StepPipeline:
         # default: measured on B200 it starves Adam's streaming (step 189 -> 267 us).
         persist = int(os.environ.get("NVOL_L2_PERSIST", "0"))
         self.l2_persist = int(_lib.load().nvol_l2_persist(persist)) if persist > 0 else 0
-        self.overlap = (not self.host_feed) and os.environ.get("NVOL_SAMPLE_OVERLAP", "1") != "0"
+        # online macro-cells (OnlineMacrocells tap): fused into the sampler kernel /
+        # applied to the staged host batch; sampling stays in step (no look-ahead)
+        # so the grid sees exactly the trained batches
+        self.mc_grid = mc_grid
+        self.overlap = ((not self.host_feed) and mc_grid is None
+                        and os.environ.get("NVOL_SAMPLE_OVERLAP", "1") != "0")
         self.side = torch.cuda.Stream(device=dev) if self.overlap else None
         if self.host_feed:
             self.copy_stream = torch.cuda.Stream(device=dev)
@@ -140,8 +145,12 @@ class StepPipeline:
         dz, dy, dx = vol.shape
         c, t = self.bufs[parity]
         # the kernel offsets by (counter - counter0): counter0 = t0 - ahead
-        _lib.call("nvol_sample_incore_dev", *s.rng.words(), self.u32_base, _lib.ptr(self.counter), self.t0 - ahead,
-                  self.B, self.row0, self.b, _lib.ptr(vol), dx, dy, dz, _lib.ptr(c), _lib.ptr(t), _lib.stream())
+        g = self.mc_grid
+        gx, gy, gz = g.grid_dims if g is not None else (0, 0, 0)
+        _lib.call("nvol_sample_incore_dev_mc", *s.rng.words(), self.u32_base, _lib.ptr(self.counter),
+                  self.t0 - ahead, self.B, self.row0, self.b, _lib.ptr(vol), dx, dy, dz, _lib.ptr(c), _lib.ptr(t),
+                  _lib.ptr(g.value_lo) if g is not None else None, _lib.ptr(g.value_hi) if g is not None else None,
+                  gx, gy, gz, g.n_g if g is not None else 1, _lib.stream())
 
     def _feed(self, parity: int) -> None:
         """H2D of this step's host batch into device buffer `parity` (copy stream)."""
@@ -180,7 +189,10 @@ class StepPipeline:
         m = self.model
         main = torch.cuda.current_stream()
         if self.host_feed:
-            pass
+            if self.mc_grid is not None:
+                from .macrocell import macrocell_update_online
+                from .sampler import SampleBatch
+                macrocell_update_online(self.mc_grid, SampleBatch(*self.bufs[parity], trusted=True))
         elif self.overlap:
             self.side.wait_stream(main)                 # fork: next step's batch on the side stream
             with torch.cuda.stream(self.side):
@@ -253,24 +265,26 @@ class StepPipeline:
         return losses
 
 
-def _cached_pipeline(model: NeuralModel, sampler, steps: int) -> "StepPipeline":
+def _cached_pipeline(model: NeuralModel, sampler, steps: int, mc_grid=None) -> "StepPipeline":
     """Reuse the model's pipeline (and its captured graphs) across train() calls
     while nothing it baked in changed: same sampler object, optimizer step and
     (device sampling) stream position, and capacity left."""
     p = getattr(model, "_pipeline", None)
     if p is not None:
-        ok = (p.sampler is sampler and p.t0 + p.done == model.opt.t and p.done + steps <= p.capacity
+        ok = (p.sampler is sampler and p.mc_grid is mc_grid and p.t0 + p.done == model.opt.t
+              and p.done + steps <= p.capacity
               and p.train_mode == model.train_mode and p.B == model.batch_size
               and (p.host_feed or sampler.rng.u32 == p.u32_base + 3 * p.B * p.done))
         if ok:
             return p
-    p = StepPipeline(model, sampler, max(steps, 256))
+    p = StepPipeline(model, sampler, max(steps, 256), mc_grid=mc_grid)
     model._pipeline = p
     return p
 
 
 def _fast_path(model, sampler, tap) -> bool:
-    if tap is not None or not model._use_kernels():
+    from .macrocell import OnlineMacrocells
+    if (tap is not None and not isinstance(tap, OnlineMacrocells)) or not model._use_kernels():
         return False
     if isinstance(sampler, InCoreSampler):
         return sampler.interpolation == "trilinear"
@@ -284,7 +298,7 @@ def train(model: NeuralModel, sampler, steps: int, tap=None, log_every: int = 0)
     history = TrainHistory()
     if _fast_path(model, sampler, tap):
         t0 = model.opt.t
-        pipe = _cached_pipeline(model, sampler, steps)
+        pipe = _cached_pipeline(model, sampler, steps, mc_grid=tap.grid if tap is not None else None)
         start = time.perf_counter()
         first = pipe.done
         pipe.step(steps)

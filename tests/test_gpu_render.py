@@ -151,3 +151,37 @@ def test_online_macrocells_inside_precomputed(nv):
     touched = lo <= hi
     assert touched.mean() > 0.9
     assert np.all(lo[touched] >= plo[touched] - 1e-7) and np.all(hi[touched] <= phi[touched] + 1e-7)
+
+
+def test_online_macrocells_bit_exact(nv):
+    """nvol_macrocell_update_online on the reference's golden batches == the reference."""
+    from paper_2207_11620_b200 import macrocell
+    from paper_2207_11620_b200.sampler import SampleBatch
+    z = golden("macrocell_online.npz")
+    dims, ng = tuple(int(x) for x in z["dims"]), int(z["n_g"])
+    grid = macrocell.macrocell_empty(dims, n_g=ng)
+    for c, t in zip(z["coords"], z["targets"]):
+        macrocell.macrocell_update_online(grid, SampleBatch(c, t))
+    np.testing.assert_array_equal(grid.value_lo.cpu().numpy(), z["lo"])
+    np.testing.assert_array_equal(grid.value_hi.cpu().numpy(), z["hi"])
+
+
+def test_online_macrocells_fused_into_training(nv):
+    """train(..., tap=OnlineMacrocells(grid)) fuses the update into the device sampler:
+    after 5 steps the grid equals the reference's update over the same 5 batches."""
+    from paper_2207_11620_b200 import fields, macrocell, trainer
+    from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    z = golden("macrocell_online.npz")
+    dims, ng = tuple(int(x) for x in z["dims"]), int(z["n_g"])
+    fld = fields.rasterize("blobs", dims, host=True)
+    cfg = {"encoding": {"otype": "HashGrid", "n_levels": 4, "n_features_per_level": 2,
+                        "log2_hashmap_size": 12, "base_resolution": 4},
+           "network": {"n_neurons": 16, "n_hidden_layers": 2}, "batch_size": 4096}
+    for mode in (0, MODE_TCGEN05):
+        model = build_model(cfg, dims=dims, seed=0)
+        model.train_mode = mode
+        grid = macrocell.macrocell_empty(dims, n_g=ng)
+        trainer.train(model, InCoreSampler(fld, seed=3), steps=5, tap=macrocell.OnlineMacrocells(grid))
+        np.testing.assert_array_equal(grid.value_lo.cpu().numpy(), z["lo"])
+        np.testing.assert_array_equal(grid.value_hi.cpu().numpy(), z["hi"])

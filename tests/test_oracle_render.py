@@ -57,3 +57,17 @@ def test_render_grid_golden(scene):
     img, evals = ro.render(z["norm"], ro.default_tf(), cam, mu=z["mcf_mu"], ng=8, dims=dims)
     assert evals == int(z["evals_grid_mc"])
     np.testing.assert_array_equal(img, z["img_grid_mc"])
+
+
+def test_online_macrocells_golden():
+    """oracle update_online (macrocell.py:101-133) == the reference on its golden batches."""
+    import render_oracle as ro
+    z = golden("macrocell_online.npz")
+    dims, ng = tuple(int(x) for x in z["dims"]), int(z["n_g"])
+    gx, gy, gz = ro.grid_dims(dims, ng)
+    lo = np.full((gz, gy, gx), np.inf, dtype=np.float32)
+    hi = np.full((gz, gy, gx), -np.inf, dtype=np.float32)
+    for c, t in zip(z["coords"], z["targets"]):
+        ro.update_online(lo, hi, c, t, dims, ng)
+    np.testing.assert_array_equal(lo, z["lo"])
+    np.testing.assert_array_equal(hi, z["hi"])
