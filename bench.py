@@ -326,28 +326,38 @@ def run_ours(args):
 
     # ---- decode (cfg3) and render (cfg4) beside the headline
     dec = None
-    if world == 1 and not args.no_decode:
+    if not args.no_decode:
+        # cfg3: z-slab bricks sharded over the ranks (distributed.decode_shard), no exchange;
+        # device time per rank with CUDA events, max over ranks
+        from paper_2207_11620_b200.distributed import decode_shard
         dd = (args.decode_dim,) * 3
         model.infer_mode = args.decode_mode
         decode(model, dims=(64, 64, 64))
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         d0.record(stream)
-        out = decode(model, dims=dd)
+        z0, out = decode_shard(model, dd, rank, world)
         d1.record(stream)
         torch.cuda.synchronize()
         dms = d0.elapsed_time(d1)
+        if world > 1:
+            t = torch.tensor([dms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dms = float(t.item())
         nvox = dd[0] * dd[1] * dd[2]
         dec = {"value": nvox / (dms / 1e3), "unit": "samples/s", "ms": dms, "dims": list(dd),
                "mode": args.decode_mode, "workload": "cfg3: full-grid decode of the cfg2 model",
+               "sharding": f"z-slabs over {world} GPU(s), max over ranks",
                "gather_gbs": nvox * 1024 / (dms * 1e-3) / 1e9,
                "mlp_tflops": nvox * 2 * 3 * (32 * 64 + 3 * 64 * 64) / (dms * 1e-3) / 1e12}
         del out
-        if rank == 0 and not args.no_cpu:
+        if rank == 0 and world == 1 and not args.no_cpu:
             dec["cpu_baseline"] = cpu_decode_rate(model.blob().cpu().numpy())
     rend = None
-    if world == 1 and not args.no_render:
-        rend = render_bench(torch, args)
+    if not args.no_render:
+        rend = render_bench(torch, args, rank, world)
 
     launches = pipe.launches_per_step() * K
     cpu = None
@@ -371,8 +381,9 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def render_bench(torch, args):
-    """cfg4: 1920x1080 macro-cell ray march of a cfg2 model trained on blobs 256^3."""
+def render_bench(torch, args, rank=0, world=1):
+    """cfg4: 1920x1080 macro-cell ray march of a cfg2 model trained on blobs 256^3
+    (image row tiles over the ranks, distributed.render_tile; max over ranks)."""
     from paper_2207_11620_b200 import fields
     from paper_2207_11620_b200.camera import default_camera
     from paper_2207_11620_b200.macrocell import macrocell_from_model, macrocell_set_tf
@@ -396,18 +407,29 @@ def render_bench(torch, args):
     res = {"workload": "cfg4: 1920x1080 raymarch, macro-cells n_g=16, K=8, step 1, cfg2 model trained "
                        f"{args.render_train_steps} steps on blobs 256^3, default TF/camera",
            "macrocell_from_model_ms": mc_ms}
+    from paper_2207_11620_b200.distributed import render_tile
+    import torch.distributed as dist
+    res["sharding"] = f"image row tiles over {world} GPU(s), frame time = max over ranks"
     for arch, mode in (("wavefront", "tensor"), ("wavefront", "exact"), ("reference", "exact")):
-        render_frame_device(m, tf, cam, cfg, grid, arch, mode)       # warm-up
+        render_tile(m, tf, cam, cfg, grid, rank, world, arch, mode)       # warm-up
         torch.cuda.synchronize()
         ts = []
         for _ in range(3):
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            img, st = render_frame_device(m, tf, cam, cfg, grid, arch, mode)
+            _, img, st = render_tile(m, tf, cam, cfg, grid, rank, world, arch, mode)
             torch.cuda.synchronize()
             ts.append((time.perf_counter() - t0) * 1e3)
-        fms = float(np.median(ts))
-        res[f"{'inshader' if arch == 'reference' else arch}_{mode}"] = {"frame_ms": fms, "fps": 1e3 / fms, "evals": st.evals,
-                                 "evals_per_s": st.evals / (fms * 1e-3), "iterations": len(st.alive_per_iteration)}
+        fms, evals = float(np.median(ts)), st.evals
+        if world > 1:
+            t = torch.tensor([fms, float(evals)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+            e = t[1:].clone()
+            dist.all_reduce(e, op=dist.ReduceOp.SUM)
+            fms, evals = float(t[0].item()), int(e.item())
+        res[f"{'inshader' if arch == 'reference' else arch}_{mode}"] = {"frame_ms": fms, "fps": 1e3 / fms, "evals": evals,
+                                 "evals_per_s": evals / (fms * 1e-3), "iterations": len(st.alive_per_iteration)}
     return res
 
 

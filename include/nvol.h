@@ -46,7 +46,8 @@ extern "C" {
 
 /* ------------------------------------------------------------------ library */
 
-/* ABI version (bumped on any signature change). */
+/* ABI version (bumped on any signature change; 2: the nvol_render camera parameter array gained
+ * the image tile rows row0, nrows). */
 int nvol_abi_version(void);
 /* Static string describing the last non-zero status (thread-local). */
 const char *nvol_last_error(void);
@@ -278,15 +279,17 @@ int64_t nvol_render_workspace_bytes(int64_t n_pixels, int32_t k_batch);
  * (architecture 0 = render_wavefront, render.py:383-454: rm_coord ->
  * batched Phi (eval_mode 0 exact / 1 tcgen05) -> rm_shade -> compaction) or
  * the in-shader mega-kernel (architecture 1 = render_reference,
- * render.py:347-380).  [host] cam_params[16] = eye[3], fwd[3], right[3],
- * up[3] (camera.py:44-56 basis, float64), tan_half, aspect, width, height;
+ * render.py:347-380).  [host] cam_params[18] = eye[3], fwd[3], right[3],
+ * up[3] (camera.py:44-56 basis, float64), tan_half, aspect, width, height,
+ * row0, nrows (the image tile rendered: rows [row0, row0+nrows) of the frame;
+ * multi-GPU renders give each rank a tile);
  * [host] render_params[20] = mode_shadow, use_mc, skip_empty, k_batch, s1,
  * s2, pexp, termination, ambient, density_scale, n_g, -light[3],
  * background[3], Dx, Dy, Dz.  TF tables as TransferFunction.tables
  * (transfer.py:43-47) [host].  mu: device macro-cell majorants (gz,gy,gx)
  * (a 1x1x1 dummy without macro-cells).  Field: a dense normalised grid
  * (use_grid) or the hash-grid model (tables [host], params/weights device).
- * img: device (H*W*3) float32.  stats_out [host]: {field evaluations,
+ * img: device (nrows*W*3) float32.  stats_out [host]: {field evaluations,
  * iterations}; alive_hist [host]: rays alive per iteration (up to max_hist). */
 int nvol_render(const double *cam_params, const double *render_params, const float *tf_cv,
                 const float *tf_crgb, int32_t ncv, const float *tf_ov, const float *tf_oa,

@@ -48,7 +48,7 @@ int pack_tables(GridTables &t, const int64_t *level_off, const int64_t *level_re
 
 extern "C" {
 
-int nvol_abi_version(void) { return 1; }
+int nvol_abi_version(void) { return 2; }  // 2: nvol_render camera params carry an image tile (row0, nrows)
 
 const char *nvol_last_error(void) { return nvol::g_last_error; }
 

@@ -295,18 +295,20 @@ struct CamParams {
     double fwd[3], right[3], up[3];
     double tan_half, aspect;
     int64_t width, height;
+    int64_t row0, nrows;  // image tile: rows [row0, row0 + nrows) of the width x height frame
 };
 
 // camera.py:117-143 (float64, cast to float32) + render.py:225-243 slab test
 __global__ void raygen_kernel(const CamParams cam, const RmScene S, RayState *__restrict__ rays,
                               uint8_t *__restrict__ hit, float *__restrict__ img) {
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n = cam.width * cam.height;
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel within the tile
+    const int64_t n = cam.width * cam.nrows;
     if (p >= n) return;
     img[3 * p] = S.bg[0];
     img[3 * p + 1] = S.bg[1];
     img[3 * p + 2] = S.bg[2];
-    double ii = (double)(p % cam.width), jj = floor((double)p / (double)cam.width);
+    const int64_t pf = p + cam.row0 * cam.width;  // pixel index in the full frame (camera.py:117-125)
+    double ii = (double)(pf % cam.width), jj = floor((double)pf / (double)cam.width);
     double nx = ((ii + 0.5) / (double)cam.width * 2.0 - 1.0) * (cam.tan_half * cam.aspect);
     double ny = (1.0 - (jj + 0.5) / (double)cam.height * 2.0) * cam.tan_half;
     double d[3];
@@ -596,7 +598,7 @@ static int fill_scene(RmScene &S, const double *rp, const float *tf_cv, const fl
 }
 
 static void fill_cam(CamParams &C, const double *cp) {
-    // cp: eye[3], fwd[3], right[3], up[3], tan_half, aspect, width, height
+    // cp: eye[3], fwd[3], right[3], up[3], tan_half, aspect, width, height, row0, nrows
     for (int a = 0; a < 3; ++a) {
         C.eye[a] = (float)cp[a];
         C.fwd[a] = cp[3 + a];
@@ -607,6 +609,8 @@ static void fill_cam(CamParams &C, const double *cp) {
     C.aspect = cp[13];
     C.width = (int64_t)cp[14];
     C.height = (int64_t)cp[15];
+    C.row0 = (int64_t)cp[16];
+    C.nrows = (int64_t)cp[17];
 }
 
 struct RenderWs {
@@ -688,7 +692,8 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
     NVOL_REQUIRE(mu && img && workspace && stats_out, "null pointer");
     CamParams C;
     fill_cam(C, cam_params);
-    const int64_t npix = C.width * C.height;
+    NVOL_REQUIRE(C.row0 >= 0 && C.nrows >= 1 && C.row0 + C.nrows <= C.height, "bad image tile rows");
+    const int64_t npix = C.width * C.nrows;
     const int K = S.k_batch < 1 ? 1 : S.k_batch;
     RenderWs w = carve(workspace, npix, K);
     NVOL_REQUIRE(workspace_bytes >= w.total, "render workspace too small");

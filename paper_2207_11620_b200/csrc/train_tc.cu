@@ -55,10 +55,10 @@ struct TcShape {
     // per slot t: o_d[t] (X hi during the forward, then the fp16 delta tile),
     // o_hlo[t] (X lo, then activation lo parts, h_NH, then the X hi reload),
     // o_h[t][i] (hidden activations h_1..h_{nh-1}, fp16 hi)
-    uint32_t o_d[2], o_hlo[2], o_h[2][MAX_NH], o_part, smem_bytes, xhalf;
+    uint32_t o_d[2], o_hlo[2], o_h[2][MAX_NH], o_dout[2], o_part, smem_bytes, xhalf;
     // TMEM: per slot [forward acc | forward lo acc] (backward dX aliases the
     // first), then the dW_0..dW_{nh-1} accumulators shared by both slots
-    uint32_t t_acc[2], t_dw[MAX_NH], t_alloc;
+    uint32_t t_acc[2], t_dw[MAX_NH], t_dwout, t_alloc;
     int64_t w_floats;
 };
 
@@ -90,8 +90,12 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
         s.o_h[t][0] = 0;
         for (int i = 1; i < nh; ++i) s.o_h[t][i] = take(2u * TILE * nn);
     }
+    // per slot: the output-layer delta as an N = 8 K-major B operand (column 0 = delta_out)
+    s.o_dout[0] = take(2u * 8 * TILE);
+    s.o_dout[1] = take(2u * 8 * TILE);
     s.o_part = take(4u * 2 * 2 * TILE);
-    take(4096);  // slack: the dW MMA reads M = 128 delta "rows" past an nn-wide tile (values unused)
+    // no slack needed: the M = 128 MN-major A operands (delta^T for dW, h_NH^T for dW_out) read up to
+    // ~2 KB past an nn-wide tile (rows >= nn, values unused), which lands in the next slot buffer
     s.smem_bytes = off;
     s.xhalf = 2u * TILE * s.ninp;
     uint32_t col = 0;
@@ -103,6 +107,8 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
         s.t_dw[i] = col;
         col += (i == 0) ? s.ninp : nn;
     }
+    s.t_dwout = col;  // dW_out^T = h_NH^T delta_out: lanes = hidden units, column 0
+    col += 8;
     if (col > 512) return 0;
     uint32_t a = 32;
     while (a < col) a <<= 1;
@@ -334,7 +340,6 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar_x[2], bar_xr[2], bar_acc[2], bar_op[2], bar_w;
     __shared__ uint32_t tmem_base_sh;
-    __shared__ float s_red[PP_EPI_WARPS * 33];
     __shared__ double s_loss[PP_EPI_WARPS];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NN = sh.nn, NINP = sh.ninp, NH = sh.nh, NIN = sh.nin;
@@ -386,6 +391,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
         }
         for (int q = tid; q < NN; q += PP_THREADS) reinterpret_cast<float *>(smem + sh.o_wout)[q] = src[q];
     }
+    for (int q = tid; q < 2 * 8 * TILE * 2 / 16; q += PP_THREADS)  // both dout tiles (contiguous)
+        reinterpret_cast<uint4 *>(smem + sh.o_dout[0])[q] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, sh.t_alloc);
     tc::fence_proxy_async();
     tc::fence_before();
@@ -463,6 +470,17 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                         const int j = nph - 1 - ph;
                         const int win = (j == 0) ? NINP : NN;
                         const uint32_t hb = (j == 0) ? lbuf : tc::smem_u32(smem + sh.o_h[t][j]);
+                        if (j == NH - 1) {
+                            // dW_out^T [hidden x 8] += h_NH^T (lbuf, MN-major A) x delta_out (K-major B, N = 8)
+                            const uint32_t id = tc::make_idesc(128, 8, 1, 0);
+                            const uint64_t ad = tc::make_desc(lbuf, (NN / 8) * 128, 128);
+                            const uint64_t bd = tc::make_desc(tc::smem_u32(smem + sh.o_dout[t]), 128, 2048);
+                            const uint32_t first = ((dw_started >> 31) & 1u) ? 1u : 0u;
+                            for (int k = 0; k < TILE / 16; ++k)
+                                tc::mma_f16(tmem + sh.t_dwout, ad + (uint64_t)(k * 2 * (NN / 8) * 8),
+                                            bd + (uint64_t)(k * 16), id, (first || k > 0) ? 1 : 0);
+                            dw_started |= 1u << 31;
+                        }
                         {
                             const uint32_t id = tc::make_idesc(128, win, 1, 1);
                             const uint64_t ad = tc::make_desc(dbuf, (NN / 8) * 128, 128);
@@ -517,9 +535,6 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
         const float *s_wout = reinterpret_cast<const float *>(smem + sh.o_wout);
         uint32_t par_acc = 0;
         double lsum = 0.0;  // this row's loss terms over the slot's tiles (column half 0 only)
-        float dwo[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) dwo[e] = 0.0f;
         int cn0, cnn;
         group_cols(NN, hh, 2, cn0, cnn);  // this thread's hidden columns [cn0, cn0 + cnn), cnn <= 32
 #ifdef NVOL_TIMELINE
@@ -551,23 +566,32 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
 #endif
                 const bool last = i == NH - 1;
                 uint8_t *dst = last ? lbuf : smem + sh.o_h[t][i + 1];
-                for (int c = cn0; c < cn0 + cnn; c += 16) {
-                    float v[16], vl[16];
-                    tc::tmem_ld16(tacc + c, v);
-                    tc::tmem_ld16(tacc + NN + c, vl);
-                    tc::tmem_wait_ld();
+                // chunk 0's hi + lo and chunk 1's hi in flight together; chunk 1's lo
+                // is fetched while chunk 0 is processed
+                float v0[16], vl[16], v1[16];
+                const bool two = cnn > 16;
+                tc::tmem_ld16(tacc + cn0, v0);
+                tc::tmem_ld16(tacc + NN + cn0, vl);
+                if (two) tc::tmem_ld16(tacc + cn0 + 16, v1);
+                tc::tmem_wait_ld();
+                auto chunk = [&](float(&v)[16], int c) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
                     store_row_f16(dst, s, c, NN, v, false);
                     if (!last) {
 #pragma unroll
-                        for (int e = 0; e < 16; ++e)
-                            vl[e] = (v[e] - __half2float(__float2half_rn(v[e]))) * tc::kLoScale;
+                        for (int e = 0; e < 16; ++e) vl[e] = (v[e] - __half2float(__float2half_rn(v[e]))) * tc::kLoScale;
                         store_row_f16(lbuf, s, c, NN, vl, false);
                     } else {
 #pragma unroll
                         for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * v[e];
                     }
+                };
+                if (cnn > 0) chunk(v0, cn0);
+                if (two) {
+                    tc::tmem_ld16(tacc + NN + cn0 + 16, vl);
+                    tc::tmem_wait_ld();
+                    chunk(v1, cn0 + 16);
                 }
                 if (!last) release();
             }
@@ -592,9 +616,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                 sl = 0.0;
             }
             lsum += sl;
-            // ---- dWout (CUDA cores, per-thread partials) and delta_NH = mask(h_NH) * g * w_out
+            // ---- delta_out for the dW_out MMA (fp16, x dscale) and delta_NH = mask(h_NH) * g * w_out
             {
                 const float gd = gf * dscale;
+                if (hh == 0)
+                    *reinterpret_cast<__half *>(smem + sh.o_dout[t] + tc::tile_off(0, s, TILE)) = __float2half_rn(gd);
 #pragma unroll
                 for (int ch = 0; ch < 2; ++ch) {
                     const int c = cn0 + ch * 16;
@@ -602,19 +628,10 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                         float hv[16], dv[16];
                         load_row_f16(lbuf, s, c, NN, hv);
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            dwo[ch * 16 + e] += gf * hv[e];
-                            dv[e] = hv[e] > 0.0f ? gd * s_wout[c + e] : 0.0f;
-                        }
+                        for (int e = 0; e < 16; ++e) dv[e] = hv[e] > 0.0f ? gd * s_wout[c + e] : 0.0f;
                         store_row_f16(dbuf, s, c, NN, dv, false);
                     }
                 }
-            }
-            named_sync(1 + t, 256);  // every h_NH read done: lbuf may take the X hi reload
-            if (hh == 0 && q == 0 && lane == 0) {
-                tc::fence_proxy_async();
-                tc::mbar_arrive_expect_tx(&bar_xr[t], sh.xhalf);
-                tc::bulk_g2s(lbuf, xtiles + tile * xtile_bytes, sh.xhalf, &bar_xr[t]);
             }
             release();
             // ---- backward epilogues
@@ -625,16 +642,27 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
 #ifdef NVOL_TIMELINE
                 if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * (++epi_n), gtime());
 #endif
+                if (j == NH - 1 && hh == 0 && q == 0 && lane == 0) {
+                    // the dW_out / dW_{NH-1} MMAs that read lbuf (h_NH) are done: reload X hi for dW_0
+                    tc::mbar_arrive_expect_tx(&bar_xr[t], sh.xhalf);
+                    tc::bulk_g2s(lbuf, xtiles + tile * xtile_bytes, sh.xhalf, &bar_xr[t]);
+                }
                 if (j > 0) {
                     const uint8_t *hj = smem + sh.o_h[t][j];
-                    for (int c = cn0; c < cn0 + cnn; c += 16) {
-                        float v[16], hv[16];
-                        tc::tmem_ld16(tacc + c, v);
-                        load_row_f16(hj, s, c, NN, hv);
-                        tc::tmem_wait_ld();
+                    float v[2][16];
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) v[e] = hv[e] > 0.0f ? v[e] : 0.0f;
-                        store_row_f16(dbuf, s, c, NN, v, false);
+                    for (int ch = 0; ch < 2; ++ch)
+                        if (ch * 16 < cnn) tc::tmem_ld16(tacc + cn0 + ch * 16, v[ch]);
+#pragma unroll
+                    for (int ch = 0; ch < 2; ++ch) {
+                        if (ch * 16 >= cnn) continue;
+                        const int c = cn0 + ch * 16;
+                        float hv[16];
+                        load_row_f16(hj, s, c, NN, hv);
+                        if (ch == 0) tc::tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[ch][e] = hv[e] > 0.0f ? v[ch][e] : 0.0f;
+                        store_row_f16(dbuf, s, c, NN, v[ch], false);
                     }
                 } else {
                     // the slot's smem buffers are free once dW_0 / dX_0 completed: next X tile
@@ -657,34 +685,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                 release();
             }
         }
-        // ---- dW_out and the loss: warp-reduce the per-thread partials into shared
-        // memory; one RED per column and one loss atomic per CTA after the barrier
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                float v = dwo[ch * 16 + e];
-                for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o2);
-                dwo[ch * 16 + e] = v;
-            }
-        }
+        // ---- the loss: warp-reduce, one double atomic per CTA after the barrier
         for (int o2 = 16; o2 > 0; o2 >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o2);
-        if (lane == 0) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) s_red[warp * 33 + e] = dwo[e];
-            s_loss[warp] = hh == 0 ? lsum : 0.0;
-        }
+        if (lane == 0) s_loss[warp] = hh == 0 ? lsum : 0.0;
     }
     __syncthreads();
-    if (tid < NN) {
-        // column c belongs to half c / (NN/2) (NN >= 32) or half 0 (NN = 16); sum its 8 warps in fixed order
-        const int half = NN >= 32 ? tid / (NN / 2) : 0;
-        const int e = tid - half * (NN >= 32 ? NN / 2 : 0);
-        float acc = 0.0f;
-        for (int w = 0; w < PP_EPI_WARPS; ++w)
-            if (((w >> 2) & 1) == half) acc += s_red[w * 33 + e];
-        atomicAdd(dw_grads + sh.w_floats - NN + tid, acc * (1.0f / tc::kActScale));
-    }
     if (tid == PP_THREADS - 32) {
         double l = 0.0;
         for (int w = 0; w < PP_EPI_WARPS; ++w) l += s_loss[w];
@@ -727,6 +732,12 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                 }
             }
             base += (int64_t)NN * win;
+        }
+        if (grp == 0 && q * 32 < NN) {  // dW_out^T: lane o = hidden unit, column 0
+            float v[16];
+            tc::tmem_ld16(tmem + lane_base + sh.t_dwout, v);  // columns 0..15 (8 allocated + neighbours; only 0 used)
+            tc::tmem_wait_ld();
+            if (o < NN) atomicAdd(dw_grads + base + o, v[0] * unscale);
         }
     }
     tc::fence_before();

@@ -38,6 +38,55 @@ def shard_u32_offset(u32_base: int, step: int, batch_size: int, row0: int) -> in
     return int(u32_base) + 3 * int(batch_size) * int(step) + 3 * int(row0)
 
 
+def split_range(n: int, rank: int, world: int):
+    """(start, count) of rank's contiguous share of n units (z-slabs / image rows);
+    the first n % world ranks take one extra unit."""
+    if world < 1 or not 0 <= rank < world:
+        raise ConfigError(f"bad rank {rank} of world {world}")
+    q, r = divmod(int(n), world)
+    start = rank * q + min(rank, r)
+    return start, q + (1 if rank < r else 0)
+
+
+def decode_shard(model, dims=None, rank: int = 0, world: int = 1, mode: str | None = None):
+    """This rank's brick of a full-grid decode (trainer.py:98-106 sharded): the
+    z-slabs [z0, z0+nz) of the volume, decoded on this rank's GPU -> (z0, slab).
+    Voxels are independent, so the slabs of all ranks are bit-identical to the
+    single-GPU decode; the output stays distributed (no exchange)."""
+    from .trainer import decode_brick
+    dims = tuple(dims if dims is not None else model.dims)
+    dx, dy, dz = dims
+    z0, nz = split_range(dz, rank, world)
+    slab = torch.empty((nz, dy, dx), dtype=torch.float32, device=model.flat_params.device)
+    if nz:
+        decode_brick(model, dims, z0, nz, slab, mode=mode)
+    return z0, slab
+
+
+def render_tile(phi, tf, cam, cfg, grid=None, rank: int = 0, world: int = 1, architecture: str = "wavefront",
+                eval_mode: str | None = None):
+    """This rank's image tile (rows [row0, row0+nrows)) of one ray-marched frame
+    -> (row0, tile (nrows, W, 3) device tensor, FrameStats).  Rays are
+    independent, so the tiles assemble bit-identically to the full frame."""
+    from .render import render_frame_device
+    row0, nrows = split_range(cam.height, rank, world)
+    img, st = render_frame_device(phi, tf, cam, cfg, grid, architecture, eval_mode, rows=(row0, max(nrows, 1)))
+    return row0, img[:nrows], st
+
+
+def gather_rows(tile: torch.Tensor, total: int, group=None) -> torch.Tensor:
+    """All-gather per-rank row blocks (split_range layout) into the full (total, ...) tensor."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return tile
+    world = dist.get_world_size(group)
+    q = -(-total // world)
+    pad = torch.zeros((q,) + tuple(tile.shape[1:]), dtype=tile.dtype, device=tile.device)
+    pad[:tile.shape[0]] = tile
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([parts[r][:split_range(total, r, world)[1]] for r in range(world)])
+
+
 def allreduce_grads(flat_grads: torch.Tensor, loss_acc: torch.Tensor | None = None, group=None) -> None:
     """Sum the flat gradient buffer (and the loss accumulator) over ranks."""
     if not dist.is_initialized() or dist.get_world_size(group) == 1:

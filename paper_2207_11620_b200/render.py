@@ -197,8 +197,15 @@ def _workspace(npix: int, k: int) -> torch.Tensor:
 
 
 def render_frame_device(phi, tf: TransferFunction, cam: Camera, cfg: RenderConfig, grid: MacroCellGrid | None,
-                        architecture: str = "wavefront", eval_mode: str | None = None):
-    """One frame on the device -> (image (H,W,3) float32 device tensor, FrameStats)."""
+                        architecture: str = "wavefront", eval_mode: str | None = None, rows=None):
+    """One frame on the device -> (image (H,W,3) float32 device tensor, FrameStats).
+
+    rows=(row0, nrows) renders only that image tile (an (nrows,W,3) image):
+    rays are independent, so tiles of a frame assemble bit-identically
+    (the multi-GPU split, distributed.render_tile)."""
+    row0, nrows = (0, cam.height) if rows is None else (int(rows[0]), int(rows[1]))
+    if row0 < 0 or nrows < 1 or row0 + nrows > cam.height:
+        raise ConfigError(f"bad image tile rows {rows} for height {cam.height}")
     if cfg.mode == "pathtrace":
         raise ConfigError("pathtrace mode is outside the B200 hot path (ray marching only)")
     if architecture not in ("wavefront", "reference"):
@@ -243,9 +250,9 @@ def render_frame_device(phi, tf: TransferFunction, cam: Camera, cfg: RenderConfi
                    float(np.float32(cfg.ambient)), float(np.float32(tf.density_scale)), ng,
                    float(np.float32(-ld[0])), float(np.float32(-ld[1])), float(np.float32(-ld[2])),
                    *[float(np.float32(b)) for b in cfg.background], *[float(d) for d in dims]], dtype=np.float64)
-    cp = cam.device_params()
-    npix = cam.width * cam.height
-    img = torch.empty((cam.height, cam.width, 3), dtype=torch.float32, device=dev)
+    cp = cam.device_params(row0, nrows)
+    npix = cam.width * nrows
+    img = torch.empty((nrows, cam.width, 3), dtype=torch.float32, device=dev)
     ws = _workspace(npix, cfg.k_batch)
     stats = (ctypes_i64 := np.zeros(2, dtype=np.int64))
     hist = np.zeros(4096, dtype=np.int32)

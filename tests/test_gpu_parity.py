@@ -308,6 +308,22 @@ def test_decode_invariants(nv):
     np.testing.assert_array_equal(a.data.cpu().numpy(), want)
 
 
+def test_decode_shards_assemble_bit_identically(nv):
+    """distributed.decode_shard: z-slab bricks of 3 (virtual) ranks == the single decode."""
+    from paper_2207_11620_b200 import trainer
+    from paper_2207_11620_b200.distributed import decode_shard
+    from paper_2207_11620_b200.model import build_model
+    z = golden("encode_cfg2.npz")
+    model = build_model(golden_config(z), dims=(20, 16, 13), seed=0)
+    r = np.random.default_rng(5)
+    model.encoder.params.copy_(torch.from_numpy(r.normal(0, 0.3, model.encoder.params.shape).astype(np.float32)))
+    for mode in ("exact", "tensor"):
+        model.infer_mode = mode
+        full = trainer.decode(model, dims=(20, 16, 13)).data
+        parts = [decode_shard(model, (20, 16, 13), rank=k, world=3)[1] for k in range(3)]
+        assert torch.equal(torch.cat(parts), full)
+
+
 def test_save_load_roundtrip(nv, tmp_path):
     from paper_2207_11620_b200 import trainer
     from paper_2207_11620_b200.model import build_model

@@ -185,3 +185,21 @@ def test_online_macrocells_fused_into_training(nv):
         trainer.train(model, InCoreSampler(fld, seed=3), steps=5, tap=macrocell.OnlineMacrocells(grid))
         np.testing.assert_array_equal(grid.value_lo.cpu().numpy(), z["lo"])
         np.testing.assert_array_equal(grid.value_hi.cpu().numpy(), z["hi"])
+
+
+def test_render_tiles_assemble_bit_identically(scene):
+    """distributed.render_tile: image tiles of 3 (virtual) ranks == the full frame, bitwise,
+    and their evaluation counts add up (rays are independent)."""
+    from paper_2207_11620_b200.distributed import render_tile
+    from paper_2207_11620_b200.render import RenderConfig, render_frame_device
+    z, dims, model, grid, tf, cam = scene
+    cfg = RenderConfig(mode="raymarch", use_macrocells=True, k_batch=8)
+    for emode in ("exact", "tensor"):
+        full, st = render_frame_device(model, tf, cam, cfg, grid, "wavefront", emode)
+        parts, evals = [], 0
+        for r in range(3):
+            row0, tile, s = render_tile(model, tf, cam, cfg, grid, rank=r, world=3, eval_mode=emode)
+            parts.append(tile)
+            evals += s.evals
+        assert torch.equal(torch.cat(parts), full)
+        assert evals == st.evals
