@@ -267,7 +267,7 @@ int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const 
 
 int infer_tc_launch(const float *coords, int64_t b, const float *params, const GridTables &tab, const float *wflat,
                     uint8_t *wimg, int nn, int nh, int relu_out, int decode, int64_t dx, int64_t dy, int64_t dz,
-                    int64_t z0, double lo, double scale, float *out, cudaStream_t s) {
+                    int64_t z0, double lo, double scale, float *out, cudaStream_t s, bool pack = true) {
     InferShape sh;
     if (!build_infer_shape(sh, tab.n_levels, tab.n_feat, nn, nh, relu_out)) {
         set_error("MLP shape not supported by the tcgen05 inference path");
@@ -276,8 +276,10 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
     for (int l = 0; l < tab.n_levels; ++l)
         NVOL_REQUIRE(tab.entries[l] < (1ll << 31), "level too large for the tcgen05 inference path");
     NVOL_REQUIRE(wimg, "tcgen05 inference needs an mlp_image scratch buffer (nvol_mlp_image_bytes)");
-    int st = pack_mlp_image(wflat, sh.nin, sh.ninp, nn, nh, sh.o_w, sh.o_wout, wimg, s, sh.o_wlo);
-    if (st) return st;
+    if (pack) {  // callers that launch repeatedly on unchanged weights (the render loop) pack once
+        int st = pack_mlp_image(wflat, sh.nin, sh.ninp, nn, nh, sh.o_w, sh.o_wout, wimg, s, sh.o_wlo);
+        if (st) return st;
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

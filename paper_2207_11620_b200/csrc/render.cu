@@ -454,6 +454,32 @@ __global__ void rm_coord_kernel(RayState *__restrict__ rays, int64_t n, const Rm
 }
 
 // _render_kernels.py:543-563 rm_shade
+// phi_eval_staged (_render_kernels.py:518-540) evaluates only the staged
+// samples: the [n][K] staging (holes past counts[r]) is compacted with the
+// exclusive scan offs, evaluated densely, and scattered back.
+__global__ void compact_staged_kernel(const float *__restrict__ sxyz, const int32_t *__restrict__ counts,
+                                      const int32_t *__restrict__ offs, int64_t n, int K, float *__restrict__ dxyz,
+                                      int32_t *__restrict__ total) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int c = counts[r], o = offs[r];
+    for (int j = 0; j < c; ++j) {
+        const int64_t i = r * K + j;
+        dxyz[3 * (int64_t)(o + j)] = sxyz[3 * i];
+        dxyz[3 * (int64_t)(o + j) + 1] = sxyz[3 * i + 1];
+        dxyz[3 * (int64_t)(o + j) + 2] = sxyz[3 * i + 2];
+    }
+    if (r == n - 1) *total = o + c;
+}
+
+__global__ void scatter_staged_kernel(const float *__restrict__ dvals, const int32_t *__restrict__ counts,
+                                      const int32_t *__restrict__ offs, int64_t n, int K, float *__restrict__ values) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int c = counts[r], o = offs[r];
+    for (int j = 0; j < c; ++j) values[r * K + j] = dvals[o + j];
+}
+
 __global__ void rm_shade_kernel(RayState *__restrict__ rays, int64_t n, const RmScene S,
                                 const float *__restrict__ values, const float *__restrict__ sts,
                                 const float *__restrict__ ssbar, const int32_t *__restrict__ counts,
@@ -616,8 +642,8 @@ static void fill_cam(CamParams &C, const double *cp) {
 struct RenderWs {
     RayState *rays[2];
     uint8_t *flags;
-    float *sxyz, *sts, *ssbar, *values;
-    int32_t *counts;
+    float *sxyz, *sts, *ssbar, *values, *dxyz, *dvals;
+    int32_t *counts, *offs, *dtotal;
     uint8_t *mdone;
     unsigned long long *evals;
     int64_t *nsel;
@@ -645,12 +671,18 @@ static RenderWs carve(void *base, int64_t npix, int k) {
     w.ssbar = (float *)take(npix * k * 4);
     w.values = (float *)take(npix * k * 4);
     w.counts = (int32_t *)take(npix * 4);
+    w.offs = (int32_t *)take(npix * 4);
+    w.dxyz = (float *)take(npix * k * 12);
+    w.dvals = (float *)take(npix * k * 4);
+    w.dtotal = (int32_t *)take(8);
     w.mdone = (uint8_t *)take(npix);
     w.evals = (unsigned long long *)take(8);
     w.nsel = (int64_t *)take(8);
-    size_t cb = 0;
+    size_t cb = 0, cs = 0;
     cub::DeviceSelect::Flagged(nullptr, cb, (RayState *)nullptr, (uint8_t *)nullptr, (RayState *)nullptr,
                                (int64_t *)nullptr, (int64_t)npix);
+    cub::DeviceScan::ExclusiveSum(nullptr, cs, (int32_t *)nullptr, (int32_t *)nullptr, (int)npix);
+    cb = cb > cs ? cb : cs;
     w.cub_bytes = cb;
     w.cub_tmp = take((int64_t)cb);
     w.total = off;
@@ -663,7 +695,9 @@ int field_exact_launch(const float *coords, int64_t b, const float *params, cons
                        cudaStream_t s);
 int infer_tc_launch(const float *coords, int64_t b, const float *params, const GridTables &tab, const float *wflat,
                     uint8_t *wimg, int nn, int nh, int relu_out, int decode, int64_t dx, int64_t dy, int64_t dz,
-                    int64_t z0, double lo, double scale, float *out, cudaStream_t s);
+                    int64_t z0, double lo, double scale, float *out, cudaStream_t s, bool pack);
+int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const uint32_t *o_w, uint32_t o_wout,
+                   uint8_t *image, cudaStream_t s, const uint32_t *o_wlo);
 
 }  // namespace nvol
 
@@ -761,20 +795,29 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
                                                               w.evals);
             st = check_launch("rm_coord");
             if (st) return st;
-            const int64_t ns = n * K;
-            if (use_grid) {
-                extern int nvol_trilinear(const float *, int64_t, int64_t, int64_t, const float *, int64_t, float *,
-                                          void *);
-                st = nvol_trilinear(norm, ndx, ndy, ndz, w.sxyz, ns, w.values, stream);
-            } else if (eval_mode == 1) {
-                int nnv = widths[1];
-                st = infer_tc_launch(w.sxyz, ns, params, tab, weights, (uint8_t *)mlp_image, nnv, n_layers - 1,
-                                     relu_out, 0, 0, 0, 0, 0, 0.0, 1.0, w.values, s);
-            } else {
-                st = field_exact_launch(w.sxyz, ns, params, tab, weights, widths, n_layers, relu_out, 0, 0, 0, 0, 0,
-                                        0.0, 1.0, w.values, s);
+            // dense evaluation of the staged samples (holes dropped)
+            cub::DeviceScan::ExclusiveSum(w.cub_tmp, w.cub_bytes, w.counts, w.offs, (int)n, s);
+            compact_staged_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.sxyz, w.counts, w.offs, n, K, w.dxyz, w.dtotal);
+            int32_t ns32 = 0;
+            cudaMemcpyAsync(&ns32, w.dtotal, 4, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            const int64_t ns = ns32;
+            if (ns > 0) {
+                if (use_grid) {
+                    extern int nvol_trilinear(const float *, int64_t, int64_t, int64_t, const float *, int64_t, float *,
+                                              void *);
+                    st = nvol_trilinear(norm, ndx, ndy, ndz, w.dxyz, ns, w.dvals, stream);
+                } else if (eval_mode == 1) {
+                    int nnv = widths[1];
+                    st = infer_tc_launch(w.dxyz, ns, params, tab, weights, (uint8_t *)mlp_image, nnv, n_layers - 1,
+                                         relu_out, 0, 0, 0, 0, 0, 0.0, 1.0, w.dvals, s, /*pack=*/iters == 1);
+                } else {
+                    st = field_exact_launch(w.dxyz, ns, params, tab, weights, widths, n_layers, relu_out, 0, 0, 0, 0,
+                                            0, 0.0, 1.0, w.dvals, s);
+                }
+                if (st) return st;
+                scatter_staged_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.dvals, w.counts, w.offs, n, K, w.values);
             }
-            if (st) return st;
             rm_shade_kernel<<<grid_for(n, 128), 128, 0, s>>>(rs, n, S, w.values, w.sts, w.ssbar, w.counts, w.mdone,
                                                               img, w.flags);
             st = check_launch("rm_shade");
