@@ -102,6 +102,15 @@ __device__ __forceinline__ T corner_weight(const Cell<T> &c, int corner) {
     return w;
 }
 
+// Flat parameter layout (include/nvol.h): the buffer may start 4*pad bytes past
+// a 16-byte boundary (pad = (address / 4) % 4, chosen by the host so that the
+// hashed levels' entry pairs are 16-byte aligned); W_0 starts at the first
+// 16-byte-aligned float at or after the end of the encoder table.
+inline int64_t flat_weight_offset(const float *flat, int64_t enc_floats) {
+    const int64_t pad = (int64_t)((reinterpret_cast<uintptr_t>(flat) >> 2) & 3);
+    return ((pad + enc_floats + 3) & ~(int64_t)3) - pad;
+}
+
 // ----------------------------------------------------------------------------- L2 residency hints
 // The flat gradient (48.7 MB at cfg2) is kept L2-resident across a training
 // step: Adam zeroes it with evict_last stores and the encoder-backward REDs

@@ -207,10 +207,14 @@ __global__ void __launch_bounds__(256) adam_flat_kernel(
     int64_t t = *step_counter;
     if (t >= sched_len) t = sched_len - 1;
     const float lr = sched[3 * t], c1 = sched[3 * t + 1], c2 = sched[3 * t + 2];
-    const int64_t n4 = n >> 2;
+    // the flat buffers may start 4/8/12 bytes past a 16-byte boundary (nvol.h flat layout):
+    // scalar head, float4 body, scalar tail
+    // scalar head up to the next 128-byte boundary: each warp's float4 accesses then cover whole lines
+    const int64_t head = min(n, (int64_t)(((128 - (reinterpret_cast<uintptr_t>(p) & 127)) & 127) >> 2));
+    const int64_t n4 = (n - head) >> 2;
     bool bad = false;
-    float4 *p4 = reinterpret_cast<float4 *>(p), *g4 = reinterpret_cast<float4 *>(g);
-    float4 *m4 = reinterpret_cast<float4 *>(m), *v4 = reinterpret_cast<float4 *>(v);
+    float4 *p4 = reinterpret_cast<float4 *>(p + head), *g4 = reinterpret_cast<float4 *>(g + head);
+    float4 *m4 = reinterpret_cast<float4 *>(m + head), *v4 = reinterpret_cast<float4 *>(v + head);
 #ifndef NVOL_ADAM_P_KEEP
 #define NVOL_ADAM_P_KEEP 0
 #endif
@@ -236,15 +240,16 @@ __global__ void __launch_bounds__(256) adam_flat_kernel(
         __stcs(m4 + j, M);
         __stcs(v4 + j, V);
     }
-    for (int64_t j = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < head + (n - head - 4 * n4);
          j += (int64_t)gridDim.x * blockDim.x) {
-        float P = p[j], G = g[j], M = m[j], V = v[j];
+        const int64_t q = j < head ? j : head + 4 * n4 + (j - head);  // head then tail elements
+        float P = p[q], G = g[q], M = m[q], V = v[q];
         bad |= isnan(G);
         adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-        p[j] = P;
-        g[j] = G;
-        m[j] = M;
-        v[j] = V;
+        p[q] = P;
+        g[q] = G;
+        m[q] = M;
+        v[q] = V;
     }
     if (nan_flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan_flag, 1u);
 }
@@ -266,10 +271,12 @@ __global__ void __launch_bounds__(256, NVOL_ADAM_MINB) adam_step_kernel(
     const int64_t tc = *step_counter;
     const int64_t t = tc >= sched_len ? sched_len - 1 : tc;
     const float lr = sched[3 * t], c1 = sched[3 * t + 1], c2 = sched[3 * t + 2];
-    const int64_t n4 = n >> 2;
+    // scalar head up to the next 128-byte boundary: each warp's float4 accesses then cover whole lines
+    const int64_t head = min(n, (int64_t)(((128 - (reinterpret_cast<uintptr_t>(p) & 127)) & 127) >> 2));
+    const int64_t n4 = (n - head) >> 2;
     bool bad = false;
-    float4 *p4 = reinterpret_cast<float4 *>(p), *g4 = reinterpret_cast<float4 *>(g);
-    float4 *m4 = reinterpret_cast<float4 *>(m), *v4 = reinterpret_cast<float4 *>(v);
+    float4 *p4 = reinterpret_cast<float4 *>(p + head), *g4 = reinterpret_cast<float4 *>(g + head);
+    float4 *m4 = reinterpret_cast<float4 *>(m + head), *v4 = reinterpret_cast<float4 *>(v + head);
     const uint64_t keep = l2_evict_last();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     auto upd = [&](float4 &P, float4 &G, float4 &M, float4 &V) {
@@ -307,7 +314,8 @@ __global__ void __launch_bounds__(256, NVOL_ADAM_MINB) adam_step_kernel(
         __stcs(m4 + j, M);
         __stcs(v4 + j, V);
     }
-    for (int64_t q = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < head + (n - head - 4 * n4); jj += stride) {
+        const int64_t q = jj < head ? jj : head + 4 * n4 + (jj - head);  // head then tail elements
         float P = p[q], G = g[q], M = m[q], V = v[q];
         bad |= isnan(G);
         adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
@@ -575,14 +583,15 @@ int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, cons
                          float one_minus_beta2, float eps, float l2, uint32_t *nan_flag, double *loss_acc,
                          double *losses, int64_t t0, int64_t cap, double inv_b, uint32_t *ticket, void *stream) {
     NVOL_REQUIRE(p && g && m && v && sched && step_counter && ticket && sched_len >= 1, "null pointer");
-    NVOL_REQUIRE((((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) == 0,
-                 "flat Adam buffers must be 16-byte aligned");
+    NVOL_REQUIRE(((uintptr_t)p & 127) == ((uintptr_t)g & 127) && ((uintptr_t)p & 127) == ((uintptr_t)m & 127) &&
+                     ((uintptr_t)p & 127) == ((uintptr_t)v & 127) && ((uintptr_t)p & 3) == 0,
+                 "flat Adam buffers must share their alignment modulo 128 bytes");
     static int use_tma = -1;
     if (use_tma < 0) {
         const char *e = getenv("NVOL_ADAM_TMA");
         use_tma = e ? atoi(e) : 0;  // measured slower than the grid-stride kernel on B200 (84 vs 67 us)
     }
-    if (use_tma) {
+    if (use_tma && ((uintptr_t)p & 15) == 0) {
         const size_t smem = (size_t)(AT_ST * 4 + 2 * 3 + 1) * AT_CH * 4;
         static bool attr = false;
         if (!attr) {
@@ -635,8 +644,9 @@ int nvol_adam_flat_dev(float *p, float *g, float *m, float *v, int64_t n, const 
                        int64_t *step_counter, float beta1, float one_minus_beta1, float beta2,
                        float one_minus_beta2, float eps, float l2, uint32_t *nan_flag, void *stream) {
     NVOL_REQUIRE(p && g && m && v && sched && step_counter && sched_len >= 1, "null pointer");
-    NVOL_REQUIRE((((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) == 0,
-                 "flat Adam buffers must be 16-byte aligned");
+    NVOL_REQUIRE(((uintptr_t)p & 127) == ((uintptr_t)g & 127) && ((uintptr_t)p & 127) == ((uintptr_t)m & 127) &&
+                     ((uintptr_t)p & 127) == ((uintptr_t)v & 127) && ((uintptr_t)p & 3) == 0,
+                 "flat Adam buffers must share their alignment modulo 128 bytes");
     cudaStream_t s = as_stream(stream);
     adam_flat_kernel<<<stream_grid((n + 3) / 4), 256, 0, s>>>(p, g, m, v, n, sched, sched_len, step_counter, beta1,
                                                               one_minus_beta1, beta2, one_minus_beta2, eps, l2,

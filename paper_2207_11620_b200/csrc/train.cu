@@ -100,7 +100,7 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
     void *gptr[12];
     int64_t off = 0;
     for (int l = 0; l < m; ++l) off = max(off, tab.offset[l] + tab.entries[l] * n);
-    off = (off + 3) & ~(int64_t)3;  // W_0 starts 16-byte aligned (see nvol.h, flat layout)
+    off = flat_weight_offset(params, off);  // W_0 starts 16-byte aligned (see nvol.h, flat layout)
     for (int i = 0; i < nl; ++i) {
         wptr[i] = params + off;
         gptr[i] = grads + off;

@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
         // (a pair {e, e+1} is 16-byte aligned iff the level offset + 2e is a
         // multiple of 4 floats; odd-sized dense levels shift later offsets)
         float2 v[8];
-        const uint32_t par = (uint32_t)(tab.offset[l] >> 1) & 1u;
+        // entry pair {lo, lo+1} is 16-byte aligned iff (address of entry 0) / 8 + lo is even
+        const uint32_t par = (uint32_t)((reinterpret_cast<uintptr_t>(tb) >> 3) & 1u);
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
             const uint32_t lo = min(sl[k], sl[k + 1]);
@@ -802,7 +803,8 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
             if constexpr (NF == 2) {
                 // x-adjacent corner pairs in one aligned 16-byte entry pair go
                 // out as a single float4 RED
-                const uint32_t par = (uint32_t)(tab.offset[l] >> 1) & 1u;
+                // entry pair {lo, lo+1} is 16-byte aligned iff (address of entry 0) / 8 + lo is even
+                const uint32_t par = (uint32_t)((reinterpret_cast<uintptr_t>(gl) >> 3) & 1u);
 #pragma unroll
                 for (int k = 0; k < 8; k += 2) {
                     const uint32_t yo = (k >> 1) & 1, zo = (k >> 2) & 1;
@@ -840,15 +842,17 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
         }
     }
     __syncthreads();
-    // coarse levels: one vector RED per 4 entries per CTA (coarse_floats is a
-    // multiple of 4 or the tail goes out as scalars; grads is 16-byte aligned)
-    const int n4 = coarse_floats >> 2;
+    // coarse levels: one vector RED per 16-byte-aligned float quad per CTA (the flat
+    // buffer may start 4/8/12 bytes past a 16-byte boundary: scalar head and tail)
+    const int head = min(coarse_floats, (int)(((16 - (reinterpret_cast<uintptr_t>(grads) & 15)) & 15) >> 2));
+    const int n4 = (coarse_floats - head) >> 2;
     for (int q = threadIdx.x; q < n4; q += SC_THREADS) {
-        const float4 v = reinterpret_cast<const float4 *>(acc_s)[q];
-        if (v.x != 0.0f || v.y != 0.0f || v.z != 0.0f || v.w != 0.0f)
-            red_add4(grads + 4 * q, v, keep);
+        const float *a = acc_s + head + 4 * q;
+        const float4 v = make_float4(a[0], a[1], a[2], a[3]);
+        if (v.x != 0.0f || v.y != 0.0f || v.z != 0.0f || v.w != 0.0f) red_add4(grads + head + 4 * q, v, keep);
     }
-    for (int q = 4 * n4 + threadIdx.x; q < coarse_floats; q += SC_THREADS) red_add(grads + q, acc_s[q], keep);
+    for (int q = threadIdx.x; q < head; q += SC_THREADS) red_add(grads + q, acc_s[q], keep);
+    for (int q = head + 4 * n4 + threadIdx.x; q < coarse_floats; q += SC_THREADS) red_add(grads + q, acc_s[q], keep);
 }
 
 // ============================================================================ host side
@@ -959,7 +963,7 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
     float *dfeat = reinterpret_cast<float *>(ws + p.off_dfeat);
     int64_t enc = 0;
     for (int l = 0; l < tab.n_levels; ++l) enc = max(enc, tab.offset[l] + tab.entries[l] * tab.n_feat);
-    const int64_t woff = (enc + 3) & ~(int64_t)3;
+    const int64_t woff = flat_weight_offset(params, enc);
     int st = NVOL_OK;
     cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh.smem_bytes);
     const size_t csm = (size_t)p.coarse_floats * 4;

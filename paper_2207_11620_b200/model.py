@@ -14,6 +14,8 @@ flat buffers (one Adam launch, one all-reduce for data parallelism).
 """
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 from typing import Optional
 
@@ -135,14 +137,26 @@ class NeuralModel:
         dev = self.encoder.params.device
         k = self.encoder.n_params
         self.enc_size = k
-        self.w_offset = (k + 3) & ~3                   # 16-byte aligned weights (tcgen05 staging)
+        # front pad (floats) so that the hashed levels' entry pairs {2j, 2j+1} are 16-byte
+        # aligned (one float4 gather / RED per x-adjacent corner pair); every flat buffer is
+        # a view `lead` floats into a 16-byte-aligned allocation (nvol.h flat layout)
+        enc = self.encoder
+        hashed = [int(o) for o, d in zip(getattr(enc, "level_offsets", []), getattr(enc, "_dense", [])) if not d]
+        lead = (-hashed[0]) % 4 if (hashed and dt == torch.float32) else 0
+        if os.environ.get("NVOL_FLAT_LEAD") is not None:   # layout experiments
+            lead = int(os.environ["NVOL_FLAT_LEAD"]) % 4
+        self.flat_lead = lead
+        self.w_offset = ((lead + k + 3) & ~3) - lead   # 16-byte aligned weights (tcgen05 staging)
         self.w_shapes = [tuple(w.shape) for w in self.mlp.weights]
         total = self.w_offset + sum(int(np.prod(s)) for s in self.w_shapes)
-        self.flat_size = (total + 3) & ~3
-        self.flat_params = torch.zeros(self.flat_size, dtype=dt, device=dev)
-        self.flat_grads = torch.zeros_like(self.flat_params)
-        self.flat_m = torch.zeros_like(self.flat_params)
-        self.flat_v = torch.zeros_like(self.flat_params)
+        self.flat_size = ((lead + total + 3) & ~3) - lead
+
+        def alloc():
+            return torch.zeros(lead + self.flat_size, dtype=dt, device=dev)[lead:]
+        self.flat_params = alloc()
+        self.flat_grads = alloc()
+        self.flat_m = alloc()
+        self.flat_v = alloc()
         self.flat_params[:k].copy_(self.encoder.params)
         pos = self.w_offset
         for w in self.mlp.weights:
