@@ -44,10 +44,13 @@ static int build_infer_shape(InferShape &s, int m, int n, int nn, int nh, int re
         off += (bytes + 127) & ~127u;
         return r;
     };
-    // [0, o_x): the packed weight image (hi tiles, fp32 output row, lo tiles)
-    for (int i = 0; i < nh; ++i) s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+    // [0, o_x): the packed weight image; each layer's lo tile directly follows its hi
+    // tile, so [W_hi; W_lo] is one N = 2*nn B operand (hi*W_hi and hi*W_lo in one MMA)
+    for (int i = 0; i < nh; ++i) {
+        s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+        s.o_wlo[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+    }
     s.o_wout = take(4u * nn);
-    for (int i = 0; i < nh; ++i) s.o_wlo[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
     s.o_x = take(2u * IT_TILE * s.ninp);
     s.o_xlo = take(2u * IT_TILE * s.ninp);
     // one activation buffer (+ lo): a layer's epilogue overwrites the operand
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
     uint32_t phase = 0;
     const float *s_wout = reinterpret_cast<const float *>(smem + sh.o_wout);
     float *s_part = reinterpret_cast<float *>(smem + sh.o_part);
-    const uint32_t idesc = tc::make_idesc(128, NN, 0, 0);
+    const uint32_t idesc = tc::make_idesc(128, NN, 0, 0), idesc2 = tc::make_idesc(128, 2 * NN, 0, 0);
     const int mh = (M + 1) / 2, l_lo = h * mh, l_hi = min(M, (h + 1) * mh);
     const int64_t ntiles = (b + IT_TILE - 1) / IT_TILE;
     const int c0 = NN >= 32 ? h * (NN >> 1) : 0, nc = NN >= 32 ? (NN >> 1) : (h == 0 ? NN : 0);
@@ -204,15 +207,17 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
                 tc::fence_after();
                 const uint32_t ah = tc::smem_u32(smem + (li == 0 ? sh.o_x : sh.o_h));
                 const uint32_t al = tc::smem_u32(smem + (li == 0 ? sh.o_xlo : sh.o_hlo));
-                const uint32_t bh = tc::smem_u32(smem + sh.o_w[li]), bl = tc::smem_u32(smem + sh.o_wlo[li]);
+                const uint32_t bh = tc::smem_u32(smem + sh.o_w[li]);  // [W_hi; W_lo] rows 0..2NN-1
                 const uint32_t sbo = (win / 8) * 128;
                 for (int k = 0; k < win / 16; ++k) {
                     const uint64_t adh = tc::make_desc(ah + k * 256, 128, sbo), adl = tc::make_desc(al + k * 256, 128, sbo);
-                    const uint64_t bdh = tc::make_desc(bh + k * 256, 128, sbo), bdl = tc::make_desc(bl + k * 256, 128, sbo);
-                    tc::mma_f16(tmem, adh, bdh, idesc, k > 0);
+                    const uint64_t bdh = tc::make_desc(bh + k * 256, 128, sbo);
                     if (split) {
-                        tc::mma_f16(tlo, adl, bdh, idesc, k > 0);
-                        tc::mma_f16(tlo, adh, bdl, idesc, 1);
+                        // [hi*W_hi | hi*W_lo] -> [tmem | tlo] in one N = 2*NN MMA, then lo*W_hi -> tlo
+                        tc::mma_f16(tmem, adh, bdh, idesc2, k > 0);
+                        tc::mma_f16(tlo, adl, bdh, idesc, 1);
+                    } else {
+                        tc::mma_f16(tmem, adh, bdh, idesc, k > 0);
                     }
                 }
                 tc::mma_commit(&mbar);

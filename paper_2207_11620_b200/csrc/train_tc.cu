@@ -39,9 +39,6 @@ constexpr int MAX_NH = 8;
 // epilogue warps (2 per TMEM lane quarter, one column half each), plus one
 // MMA-issuer warp that round-robins the slots' layer phases.
 constexpr int PP_EPI_WARPS = 16;
-#ifndef NVOL_FWD_WLO
-#define NVOL_FWD_WLO 1  // split forward includes the hi(act) x lo(weight) product
-#endif
 constexpr int PP_THREADS = (PP_EPI_WARPS + 1) * 32;
 constexpr int SC_THREADS = 1024;
 constexpr int SC_LG = 4;  // levels per scatter item
@@ -81,9 +78,13 @@ static int build_shape(TcShape &s, int m, int n, int nn, int nh, int relu_out, i
         off += (bytes + 127) & ~127u;
         return r;
     };
-    for (int i = 0; i < nh; ++i) s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+    // each layer's lo tile directly follows its hi tile: [W_hi; W_lo] is one N = 2*nn
+    // B operand (the forward's hi*W_hi and hi*W_lo products in one MMA)
+    for (int i = 0; i < nh; ++i) {
+        s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+        s.o_wlo[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+    }
     s.o_wout = take(4u * nn);
-    for (int i = 0; i < nh; ++i) s.o_wlo[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
     for (int t = 0; t < 2; ++t) {
         s.o_d[t] = take(2u * TILE * s.wbuf);
         s.o_hlo[t] = take(2u * TILE * s.wbuf);
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
             uint32_t par_x = 0, par_xr = 0, par_op = 0, dw_started = 0, started = 0;
             int64_t kt0 = 0, kt1 = 1;
             int ph0 = 0, ph1 = 0;
-            const uint32_t idesc_fwd = tc::make_idesc(128, NN, 0, 0);
+            const uint32_t idesc_fwd = tc::make_idesc(128, NN, 0, 0), idesc_fwd2 = tc::make_idesc(128, 2 * NN, 0, 0);
 #ifdef NVOL_TIMELINE
             int mma_n = 0;
             TL(4000, gtime());
@@ -457,14 +458,12 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                         const uint32_t ah = (i == 0) ? dbuf : tc::smem_u32(smem + sh.o_h[t][i]);
                         const uint64_t adh = tc::make_desc(ah, 128, sbo), adl = tc::make_desc(lbuf, 128, sbo);
                         const uint64_t bdh = tc::make_desc(tc::smem_u32(smem + sh.o_w[i]), 128, sbo);
-                        const uint64_t bdl = tc::make_desc(tc::smem_u32(smem + sh.o_wlo[i]), 128, sbo);
                         for (int k = 0; k < win / 16; ++k) {
                             const uint64_t dk = (uint64_t)(k * 16);  // +256 bytes per K step
-                            tc::mma_f16(acc, adh + dk, bdh + dk, idesc_fwd, k > 0);
-                            tc::mma_f16(acc + NN, adl + dk, bdh + dk, idesc_fwd, k > 0);
-#if NVOL_FWD_WLO
-                            tc::mma_f16(acc + NN, adh + dk, bdl + dk, idesc_fwd, 1);
-#endif
+                            // [hi*W_hi | hi*W_lo] -> [acc | acc + NN] in one N = 2*NN MMA (B = [W_hi; W_lo]),
+                            // then lo*W_hi -> acc + NN
+                            tc::mma_f16(acc, adh + dk, bdh + dk, idesc_fwd2, k > 0);
+                            tc::mma_f16(acc + NN, adl + dk, bdh + dk, idesc_fwd, 1);
                         }
                     } else {
                         // backward layer j: dW_j += delta^T H_j (both slots accumulate), dX = delta W_j
