@@ -245,6 +245,12 @@ int nvol_set_stage_events(void *const *events, int32_t n);
  * Device-wide setting.  No reference counterpart (GPU residency control). */
 int64_t nvol_l2_persist(int64_t bytes);
 
+/* Diagnostic: L2 peaks for the L2-bound kernels' rooflines.  out[0] = streaming
+ * read GB/s of an L2-resident 48 MB buffer, out[1] = random 8-byte gathers G/s,
+ * out[2] = random float2 REDs G/s.  Synchronous; allocates 48 MB transiently.
+ * No reference counterpart (measurement). */
+int nvol_l2_probe(double *out);
+
 /* Workspace bytes nvol_train_fwd_bwd needs for batch b. */
 int64_t nvol_train_workspace_bytes(int64_t b, int32_t n_levels, int32_t n_feat, int32_t n_neurons,
                                    int32_t n_hidden, int32_t mode);

@@ -56,6 +56,7 @@ _SIGS = {
     "nvol_render_workspace_bytes": [I64, I32],
     "nvol_set_stage_events": [P, I32],
     "nvol_l2_persist": [I64],
+    "nvol_l2_probe": [P],
     "nvol_render": [P, P, P, P, I32, P, P, I32, P, I64, I64, I64, I32, P, I64, I64, I64, P, P, P, P, P, I32, I32,
                     P, P, I32, I32, I32, I32, P, P, P, I64, P, P, I32, P],
     "nvol_macrocell_ranges": [P, I64, I64, I64, I64, I32, P, P, P],
