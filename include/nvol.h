@@ -54,6 +54,12 @@ const char *nvol_last_error(void);
 /* 1 when the tcgen05 tensor-core MLP is compiled in and usable on `device`. */
 int nvol_has_tcgen05(int device);
 
+/* Ordered-reduction mode (SPEC bitwise-repeatability criterion): on != 0 makes
+ * every reduction of the fp32 SIMT training engine (nvol_train_fwd_bwd mode 0:
+ * split-K dW GEMMs, the loss sum, the encoder scatter) run in a fixed order,
+ * so training is bitwise repeatable run to run.  Library-wide; default off. */
+int nvol_set_deterministic(int32_t on);
+
 /* ------------------------------------------------------------------ encoder */
 
 /* _kernels.py:31-79 grid_encode_fwd (called from model.py:136-150).

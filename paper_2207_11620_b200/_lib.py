@@ -26,6 +26,7 @@ _SIGS = {
     "nvol_abi_version": [],
     "nvol_last_error": [],
     "nvol_has_tcgen05": [I32],
+    "nvol_set_deterministic": [I32],
     "nvol_grid_encode_fwd": [P, I64, P, P, P, P, P, I32, I32, P, P, P, I32, P],
     "nvol_grid_encode_bwd": [P, P, P, I64, I32, I32, P, I32, P],
     "nvol_grid_encode_bwd_coords": [P, P, I64, P, P, P, P, I32, I32, P, I32, I32, P],

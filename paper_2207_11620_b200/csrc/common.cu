@@ -10,6 +10,10 @@ static thread_local char g_buf[512];
 
 void set_error(const char *msg) { g_last_error = msg; }
 
+// Ordered-reduction mode (nvol_set_deterministic): every reduction of the
+// SIMT training path runs in a fixed order, so a run is bitwise repeatable.
+int g_deterministic = 0;
+
 int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -47,6 +51,11 @@ int pack_tables(GridTables &t, const int64_t *level_off, const int64_t *level_re
 }  // namespace nvol
 
 extern "C" {
+
+int nvol_set_deterministic(int32_t on) {
+    nvol::g_deterministic = on ? 1 : 0;
+    return NVOL_OK;
+}
 
 int nvol_abi_version(void) { return 2; }  // 2: nvol_render camera params carry an image tile (row0, nrows)
 

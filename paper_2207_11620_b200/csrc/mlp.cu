@@ -17,7 +17,8 @@ namespace nvol {
 template <typename T, bool TA, bool TB>
 __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t K, const T *__restrict__ A,
                                                    int64_t lda, const T *__restrict__ B, int64_t ldb,
-                                                   T *__restrict__ C, int64_t ldc, int accumulate, int relu) {
+                                                   T *__restrict__ C, int64_t ldc, int accumulate, int relu,
+                                                   T *__restrict__ partials) {
     __shared__ T As[16][64 + 1];
     __shared__ T Bs[16][64 + 1];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -67,7 +68,9 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
             if (gn >= N) continue;
             T v = acc[r][c];
             T *dst = C + gm * ldc + gn;
-            if (gridDim.z > 1) {
+            if (partials) {  // ordered split-K: this K chunk's partial, summed later in z order
+                partials[((int64_t)blockIdx.z * M + gm) * N + gn] = v;
+            } else if (gridDim.z > 1) {
                 atomicAdd(dst, v);
             } else {
                 if (accumulate) v += *dst;
@@ -76,6 +79,17 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
             }
         }
     }
+}
+
+template <typename T>
+__global__ void splitk_reduce_kernel(const T *__restrict__ part, int nz, int64_t M, int64_t N, T *__restrict__ C,
+                                     int64_t ldc) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M * N) return;
+    T acc = (T)0;
+    for (int z = 0; z < nz; ++z) acc += part[(int64_t)z * M * N + i];
+    const int64_t r = i / N, c = i - r * N;
+    C[r * ldc + c] += acc;
 }
 
 template <typename T, bool TA, bool TB>
@@ -88,7 +102,17 @@ static int gemm(int64_t M, int64_t N, int64_t K, const T *A, int64_t lda, const 
         split = min(split, (K + 1023) / 1024);
         grid.z = (unsigned)split;
     }
-    gemm_kernel<T, TA, TB><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, relu);
+    if (grid.z > 1 && g_deterministic) {
+        // ordered split-K: partials [split][M][N], then C += sum_z in z order
+        T *part = nullptr;
+        if (cudaMallocAsync((void **)&part, sizeof(T) * grid.z * M * N, s) != cudaSuccess)
+            return check_launch("gemm partials alloc");
+        gemm_kernel<T, TA, TB><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, relu, part);
+        splitk_reduce_kernel<T><<<grid_for(M * N, 256), 256, 0, s>>>(part, (int)grid.z, M, N, C, ldc);
+        cudaFreeAsync(part, s);
+        return check_launch("gemm (ordered split-K)");
+    }
+    gemm_kernel<T, TA, TB><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, relu, (T *)nullptr);
     return check_launch("gemm");
 }
 
@@ -140,7 +164,8 @@ static int mlp_backward_t(int64_t b, int nl, const int32_t *widths, const void *
 
 template <typename T>
 __global__ void loss_kernel(const T *__restrict__ pred, const T *__restrict__ target, int64_t b, int kind,
-                            double denom, T *__restrict__ grad, double *__restrict__ loss_sum) {
+                            double denom, T *__restrict__ grad, double *__restrict__ loss_sum,
+                            double *__restrict__ block_sums) {
     __shared__ double red[32];
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double s = 0.0;
@@ -163,7 +188,20 @@ __global__ void loss_kernel(const T *__restrict__ pred, const T *__restrict__ ta
     if (threadIdx.x < 32) {
         s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) atomicAdd(loss_sum, s);
+        if (threadIdx.x == 0) {
+            if (block_sums)
+                block_sums[blockIdx.x] = s;  // ordered mode: summed in block order by loss_fold_kernel
+            else
+                atomicAdd(loss_sum, s);
+        }
+    }
+}
+
+__global__ void loss_fold_kernel(const double *__restrict__ block_sums, int n, double *__restrict__ loss_sum) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += block_sums[i];
+        *loss_sum += acc;
     }
 }
 
@@ -564,12 +602,20 @@ int nvol_loss_and_grad_scaled(const void *pred, const void *target, int64_t b, i
     NVOL_REQUIRE(b >= 1, "empty batch");
     NVOL_REQUIRE(pred && target && loss_sum, "null pointer");
     cudaStream_t s = as_stream(stream);
+    const unsigned nb = grid_for(b, 256);
+    double *bs = nullptr;
+    if (g_deterministic && cudaMallocAsync((void **)&bs, sizeof(double) * nb, s) != cudaSuccess)
+        return check_launch("loss partials alloc");
     if (dtype_bytes == 4)
-        loss_kernel<float><<<grid_for(b, 256), 256, 0, s>>>((const float *)pred, (const float *)target, b, kind,
-                                                            (double)b_global, (float *)grad, loss_sum);
+        loss_kernel<float><<<nb, 256, 0, s>>>((const float *)pred, (const float *)target, b, kind, (double)b_global,
+                                              (float *)grad, loss_sum, bs);
     else
-        loss_kernel<double><<<grid_for(b, 256), 256, 0, s>>>((const double *)pred, (const double *)target, b,
-                                                             kind, (double)b_global, (double *)grad, loss_sum);
+        loss_kernel<double><<<nb, 256, 0, s>>>((const double *)pred, (const double *)target, b, kind,
+                                               (double)b_global, (double *)grad, loss_sum, bs);
+    if (bs) {
+        loss_fold_kernel<<<1, 32, 0, s>>>(bs, (int)nb, loss_sum);
+        cudaFreeAsync(bs, s);
+    }
     return check_launch("loss_and_grad");
 }
 

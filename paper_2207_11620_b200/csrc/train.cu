@@ -117,7 +117,7 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
                            stream);
     if (st) return st;
     st = nvol_grid_encode_bwd_coords(coords, dfeat, b, level_off, level_res, level_entries, level_dense, m, n,
-                                     grads, 4, 0, stream);
+                                     grads, 4, g_deterministic, stream);
     (void)s;
     return st;
 }

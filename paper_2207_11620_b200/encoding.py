@@ -32,11 +32,14 @@ _deterministic = False
 
 
 def set_deterministic(flag: bool) -> None:
-    """Route encoder backward scatters through the order-preserving kernel
-    (bit-identical to the reference's serial scatter, run-to-run
-    reproducible) instead of float atomics."""
+    """Bitwise run-to-run repeatability (the reference's SPEC.md:197,286,785):
+    encoder backward scatters go through the order-preserving kernel
+    (bit-identical to the reference's serial scatter) instead of float atomics,
+    and training runs on the fp32 SIMT engine with every reduction ordered
+    (nvol_set_deterministic: split-K dW GEMMs, loss sum)."""
     global _deterministic
     _deterministic = bool(flag)
+    _lib.load().nvol_set_deterministic(int(_deterministic))
 
 
 def deterministic() -> bool:

@@ -230,7 +230,7 @@ class NeuralModel:
         c = self.encoder.config
         need = int(_lib.load().nvol_train_workspace_bytes(b, c.n_levels, c.n_features_per_level,
                                                            self.mlp.config.n_neurons,
-                                                           self.mlp.config.n_hidden_layers, self.train_mode))
+                                                           self.mlp.config.n_hidden_layers, self._engine()))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.flat_params.device)
         return self._ws
@@ -246,7 +246,13 @@ class NeuralModel:
                   _lib.ptr(self.flat_params), _lib.ptr(self.flat_grads), off, res, ent, dense, c.n_levels,
                   c.n_features_per_level, self.mlp.config.n_neurons, self.mlp.config.n_hidden_layers,
                   int(self.mlp.config.output_activation == "relu"), 0 if self.loss_kind == "L1" else 1,
-                  _lib.ptr(loss_sum), _lib.ptr(ws), ws.numel(), self.train_mode, _lib.stream())
+                  _lib.ptr(loss_sum), _lib.ptr(ws), ws.numel(), self._engine(), _lib.stream())
+
+    def _engine(self) -> int:
+        """Training engine for nvol_train_fwd_bwd: the fp32 SIMT engine (ordered
+        reductions) when bitwise repeatability is requested, else train_mode."""
+        from .encoding import deterministic
+        return MODE_SIMT if deterministic() else self.train_mode
 
     def adam_device(self, nan_flag: Optional[torch.Tensor] = None) -> None:
         """One flat Adam step (network.py:160-183) with host-cast scalars; advances opt.t."""

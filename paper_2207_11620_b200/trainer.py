@@ -89,7 +89,7 @@ class StepPipeline:
         B = model.batch_size
         row0, b = shard_rows(B, rank, world)
         self.model, self.sampler = model, sampler
-        self.train_mode = model.train_mode
+        self.train_mode = model._engine()
         self.B, self.b, self.row0 = B, b, row0
         self.world, self.group = world, group
         dev = model.flat_params.device
@@ -213,7 +213,7 @@ class StepPipeline:
 
     def launches_per_step(self) -> int:
         """Kernels of one step from this library (for the bench's gpu_launches)."""
-        if self.model.train_mode == 0:
+        if self.train_mode == 0:
             return 1 + 5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 + 1
         # sample (next step's, overlapped), nchunks x (encode, MLP, scatter), Adam step
         # (chunk plan of train_tc.cu make_plan: NVOL_TRAIN_CHUNKS, default 1)
@@ -273,7 +273,7 @@ def _cached_pipeline(model: NeuralModel, sampler, steps: int, mc_grid=None) -> "
     if p is not None:
         ok = (p.sampler is sampler and p.mc_grid is mc_grid and p.t0 + p.done == model.opt.t
               and p.done + steps <= p.capacity
-              and p.train_mode == model.train_mode and p.B == model.batch_size
+              and p.train_mode == model._engine() and p.B == model.batch_size
               and (p.host_feed or sampler.rng.u32 == p.u32_base + 3 * p.B * p.done))
         if ok:
             return p
