@@ -145,6 +145,17 @@ int nvol_sample_incore(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, ui
  * u32 offset = u32_base + (*step_counter - counter0) * 3 * b_global + 3 * row0
  * (rows [row0, row0+b) of a global batch of b_global: the data-parallel shard
  * of one rank reproduces exactly those rows of the single-process batch). */
+/* sampler.py:224-253 BlockBuffer.sample (out-of-core, SURVEY 8 f item 2): the
+ * caller draws slots (int32 [b], rng.integers(0, R)), voxel fractions u and raw
+ * jitter (f32 [b,3] each, rng.random(float32)) with the reference's generator;
+ * coordinates and the payload-local trilinear (nearest != 0: nearest) targets
+ * are computed here, bit-exact.  origins / interiors int64 [R,3], payloads f32
+ * [R][pz][py][px] with a one-voxel ghost border; all device pointers. */
+int nvol_sample_outofcore(const int32_t *slots, const float *u, const float *jitter, int64_t b,
+                          const int64_t *origins, const int64_t *interiors, const float *payloads, int64_t px,
+                          int64_t py, int64_t pz, int64_t dx, int64_t dy, int64_t dz, int32_t nearest,
+                          float *coords, float *targets, void *stream);
+
 int nvol_sample_incore_dev(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                            uint64_t u32_base, const int64_t *step_counter, int64_t counter0, int64_t b_global,
                            int64_t row0, int64_t b,

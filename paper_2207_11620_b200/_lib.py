@@ -42,6 +42,7 @@ _SIGS = {
     "nvol_sample_incore_dev_mc": [U64, U64, U64, U64, U64, P, I64, I64, I64, I64, P, I64, I64, I64, P, P, P, P,
                                   I64, I64, I64, I64, P],
     "nvol_macrocell_update_online": [P, P, I64, I64, I64, I64, P, P, I64, I64, I64, I64, P],
+    "nvol_sample_outofcore": [P, P, P, I64, P, P, P, I64, I64, I64, I64, I64, I64, I32, P, P, P],
     "nvol_trilinear": [P, I64, I64, I64, P, I64, P, P],
     "nvol_rasterize": [I32, I64, I64, I64, I64, I64, P, I32, P],
     "nvol_sq_err_sum": [P, P, I64, P, P],

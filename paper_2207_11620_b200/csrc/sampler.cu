@@ -140,6 +140,64 @@ static const PcgJump &jump_for(U128 inc) {
     return cached;
 }
 
+// sampler.py:224-253 BlockBuffer.sample on the device: the batch's slot /
+// voxel / jitter draws come from the caller's numpy generator (so the stream is
+// the reference's), the coordinate arithmetic and the payload-local trilinear
+// (or nearest) gather run here, float32 in the reference's operation order.
+// Payloads [R][pz][py][px] carry a one-voxel ghost border (index 0 = origin-1).
+__global__ void sample_outofcore_kernel(const int32_t *__restrict__ slots, const float *__restrict__ u,
+                                        const float *__restrict__ jit, int64_t b, const int64_t *__restrict__ origins,
+                                        const int64_t *__restrict__ interiors, const float *__restrict__ payloads,
+                                        int64_t px, int64_t py, int64_t pz, int64_t dx, int64_t dy, int64_t dz,
+                                        int nearest, float *__restrict__ coords, float *__restrict__ targets) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b) return;
+    const int64_t sl = slots[i];
+    const float *pl = payloads + sl * pz * py * px;
+    const int64_t dims[3] = {dx, dy, dz};
+    const float one_below_1 = __int_as_float(0x3f7fffff);
+    int64_t vox[3], org[3];
+    float c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        org[a] = origins[3 * sl + a];
+        const int64_t in = interiors[3 * sl + a];
+        vox[a] = min((int64_t)xmul(u[3 * i + a], (float)in), in - 1);          // (u * interior).astype(int64)
+        const float center = xadd(xadd((float)org[a], (float)vox[a]), 0.5f);   // origin + voxel + 0.5
+        const float j = xsub(jit[3 * i + a], 0.5f);                             // rng.random - 0.5
+        c[a] = fminf(fmaxf(xdiv(xadd(center, j), (float)dims[a]), 0.0f), one_below_1);
+        coords[3 * i + a] = c[a];
+    }
+    float t;
+    if (nearest) {
+        t = pl[((vox[2] + 1) * py + (vox[1] + 1)) * px + (vox[0] + 1)];
+    } else {
+        int64_t i0[3];
+        float fr[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float sa = xsub(xmul(c[a], (float)dims[a]), 0.5f);
+            i0[a] = (int64_t)floorf(sa);
+            fr[a] = xsub(sa, (float)i0[a]);
+        }
+        t = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            int64_t l[3];
+            float w = 1.0f;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int off = (k >> a) & 1;
+                const int64_t g = min(max(i0[a] + off, (int64_t)0), dims[a] - 1);
+                l[a] = g - (org[a] - 1);
+                w = xmul(w, off ? fr[a] : xsub(1.0f, fr[a]));
+            }
+            t = xadd(t, xmul(w, pl[(l[2] * py + l[1]) * px + l[0]]));
+        }
+    }
+    targets[i] = fminf(fmaxf(t, 0.0f), 1.0f);
+}
+
 __global__ void trilinear_kernel(const float *__restrict__ vol, int64_t dx, int64_t dy, int64_t dz,
                                  const float *__restrict__ pts, int64_t n, float *__restrict__ out) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -269,6 +327,18 @@ int nvol_macrocell_update_online(const float *coords, const float *targets, int6
     mc_update_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(coords, targets, n, dx, dy, dz,
                                                                       McGrid{lo, hi, gx, gy, gz, n_g});
     return check_launch("macrocell_update_online");
+}
+
+int nvol_sample_outofcore(const int32_t *slots, const float *u, const float *jitter, int64_t b,
+                          const int64_t *origins, const int64_t *interiors, const float *payloads, int64_t px,
+                          int64_t py, int64_t pz, int64_t dx, int64_t dy, int64_t dz, int32_t nearest, float *coords,
+                          float *targets, void *stream) {
+    if (b == 0) return NVOL_OK;
+    NVOL_REQUIRE(slots && u && jitter && origins && interiors && payloads && coords && targets, "null pointer");
+    NVOL_REQUIRE(px >= 1 && py >= 1 && pz >= 1 && dx >= 1 && dy >= 1 && dz >= 1, "bad dims");
+    sample_outofcore_kernel<<<grid_for(b, 256), 256, 0, as_stream(stream)>>>(
+        slots, u, jitter, b, origins, interiors, payloads, px, py, pz, dx, dy, dz, nearest, coords, targets);
+    return check_launch("sample_outofcore");
 }
 
 int nvol_trilinear(const float *volume, int64_t dx, int64_t dy, int64_t dz, const float *pts, int64_t n, float *out,
