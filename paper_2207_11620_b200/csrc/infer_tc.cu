@@ -83,7 +83,7 @@ template <int NF>
 __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
     const float *__restrict__ coords, int64_t b, const float *__restrict__ params, const GridTables tab,
     const InferShape sh, const uint8_t *__restrict__ wimg, int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
-    double lo, double scale, float *__restrict__ out, int split) {
+    double lo, double scale, float *__restrict__ out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_sh;
@@ -212,13 +212,9 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
                 for (int k = 0; k < win / 16; ++k) {
                     const uint64_t adh = tc::make_desc(ah + k * 256, 128, sbo), adl = tc::make_desc(al + k * 256, 128, sbo);
                     const uint64_t bdh = tc::make_desc(bh + k * 256, 128, sbo);
-                    if (split) {
-                        // [hi*W_hi | hi*W_lo] -> [tmem | tlo] in one N = 2*NN MMA, then lo*W_hi -> tlo
-                        tc::mma_f16(tmem, adh, bdh, idesc2, k > 0);
-                        tc::mma_f16(tlo, adl, bdh, idesc, 1);
-                    } else {
-                        tc::mma_f16(tmem, adh, bdh, idesc, k > 0);
-                    }
+                    // [hi*W_hi | hi*W_lo] -> [tmem | tlo] in one N = 2*NN MMA, then lo*W_hi -> tlo
+                    tc::mma_f16(tmem, adh, bdh, idesc2, k > 0);
+                    tc::mma_f16(tlo, adl, bdh, idesc, 1);
                 }
                 tc::mma_commit(&mbar);
             }
@@ -229,16 +225,10 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
             for (int c = c0; c < c0 + nc; c += 16) {   // values carry kActScale (see tc.cuh)
                 float v[16], vl[16];
                 tc::tmem_ld16(tmem + lane_base + c, v);
-                if (split) {
-                    tc::tmem_ld16(tlo + lane_base + c, vl);
-                    tc::tmem_wait_ld();
+                tc::tmem_ld16(tlo + lane_base + c, vl);
+                tc::tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
-                } else {
-                    tc::tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e], 0.0f);
-                }
+                for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
                 if (li < NH - 1) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) vl[e] = (v[e] - __half2float(__float2half_rn(v[e]))) * tc::kLoScale;
@@ -288,11 +278,6 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static int split = -1;
-    if (split < 0) {
-        const char *e = getenv("NVOL_INFER_SPLIT");
-        split = e ? atoi(e) : 1;
-    }
     int64_t ntiles = (b + IT_TILE - 1) / IT_TILE;
     int64_t cap = (int64_t)sms * 2;
     int grid = (int)(ntiles < cap ? ntiles : cap);
@@ -302,7 +287,7 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
     case NFV:                                                                                                  \
         cudaFuncSetAttribute(infer_tc_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes); \
         infer_tc_kernel<NFV><<<grid, IT_THREADS, sh.smem_bytes, s>>>(coords, b, params, tab, sh, wimg, decode, dx, dy, \
-                                                                    dz, z0, lo, scale, out, split);            \
+                                                                    dz, z0, lo, scale, out);                   \
         break;
         LAUNCH_IT(1)
         LAUNCH_IT(2)

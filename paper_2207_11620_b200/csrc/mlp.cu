@@ -253,27 +253,16 @@ __global__ void __launch_bounds__(256) adam_flat_kernel(
     bool bad = false;
     float4 *p4 = reinterpret_cast<float4 *>(p + head), *g4 = reinterpret_cast<float4 *>(g + head);
     float4 *m4 = reinterpret_cast<float4 *>(m + head), *v4 = reinterpret_cast<float4 *>(v + head);
-#ifndef NVOL_ADAM_P_KEEP
-#define NVOL_ADAM_P_KEEP 0
-#endif
     const uint64_t keep = l2_evict_last();
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
-#if NVOL_ADAM_P_KEEP
-        float4 P = ld4_hint(p4 + j, keep);
-#else
         float4 P = __ldcs(p4 + j);
-#endif
         float4 G = ld4_hint(g4 + j, keep), M = __ldcs(m4 + j), V = __ldcs(v4 + j);
         bad |= isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w);
         adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
         adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
         adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
         adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-#if NVOL_ADAM_P_KEEP
-        st4_hint(p4 + j, P, keep);
-#else
         __stcs(p4 + j, P);
-#endif
         st4_hint(g4 + j, G, keep);  // the zeroed gradient stays in L2 for the next scatter
         __stcs(m4 + j, M);
         __stcs(v4 + j, V);
@@ -292,16 +281,10 @@ __global__ void __launch_bounds__(256) adam_flat_kernel(
     if (nan_flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan_flag, 1u);
 }
 
-#ifndef NVOL_ADAM_UNROLL2
-#define NVOL_ADAM_UNROLL2 0
-#endif
 // Training-pipeline Adam step: adam_flat_kernel's update plus the step's bookkeeping in the last block to
 // finish (ticket): losses[t - t0] = loss_sum / B, loss_sum = 0, t += 1.  Every
 // block reads t before taking its ticket, so the advance cannot race a reader.
-#ifndef NVOL_ADAM_MINB
-#define NVOL_ADAM_MINB 1
-#endif
-__global__ void __launch_bounds__(256, NVOL_ADAM_MINB) adam_step_kernel(
+__global__ void __launch_bounds__(256) adam_step_kernel(
     float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v, int64_t n,
     const float *__restrict__ sched, int64_t sched_len, int64_t *__restrict__ step_counter, float b1, float omb1,
     float b2, float omb2, float eps, float l2, uint32_t *__restrict__ nan_flag, double *__restrict__ loss_acc,
@@ -325,25 +308,6 @@ __global__ void __launch_bounds__(256, NVOL_ADAM_MINB) adam_step_kernel(
         adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
     };
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-#if NVOL_ADAM_UNROLL2
-    for (; j + stride < n4; j += 2 * stride) {
-        const int64_t k = j + stride;
-        float4 P0 = __ldcs(p4 + j), P1 = __ldcs(p4 + k);
-        float4 G0 = ld4_hint(g4 + j, keep), G1 = ld4_hint(g4 + k, keep);
-        float4 M0 = __ldcs(m4 + j), M1 = __ldcs(m4 + k);
-        float4 V0 = __ldcs(v4 + j), V1 = __ldcs(v4 + k);
-        upd(P0, G0, M0, V0);
-        upd(P1, G1, M1, V1);
-        __stcs(p4 + j, P0);
-        __stcs(p4 + k, P1);
-        st4_hint(g4 + j, G0, keep);
-        st4_hint(g4 + k, G1, keep);
-        __stcs(m4 + j, M0);
-        __stcs(m4 + k, M1);
-        __stcs(v4 + j, V0);
-        __stcs(v4 + k, V1);
-    }
-#endif
     for (; j < n4; j += stride) {
         float4 P = __ldcs(p4 + j), G = ld4_hint(g4 + j, keep), M = __ldcs(m4 + j), V = __ldcs(v4 + j);
         upd(P, G, M, V);
@@ -370,167 +334,6 @@ __global__ void __launch_bounds__(256, NVOL_ADAM_MINB) adam_step_kernel(
             __threadfence();
             const int64_t k = tc - t0;
             if (losses && k >= 0 && k < cap) losses[k] = *reinterpret_cast<volatile double *>(loss_acc) * inv_b;
-            if (loss_acc) *loss_acc = 0.0;
-            *step_counter = tc + 1;
-            *ticket = 0u;
-        }
-    }
-}
-
-// ---------------------------------------------------------------- TMA-streamed Adam step
-// The same update as adam_step_kernel, but each persistent CTA streams
-// contiguous 8 KB chunks of p, g, m, v through a 3-stage shared-memory ring with
-// bulk TMA copies (cp.async.bulk, mbarrier completion) and writes p, m, v (and
-// the zeroed g) back with bulk stores: ~100 KB in flight per SM with a handful
-// of instructions per chunk, and long sequential DRAM streams (a 4-array
-// grid-stride loop with more warps measured slower on B200).
-constexpr int AT_CH = 2048;      // floats per array per chunk
-constexpr int AT_ST = 3;         // ring stages
-constexpr int AT_THREADS = 256;  // 8 floats per thread per chunk
-
-__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-            "r"((uint32_t)__cvta_generic_to_shared(dst)),
-        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar)), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_store(void *dst, const void *src, uint32_t bytes, uint64_t pol) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
-                 "r"((uint32_t)__cvta_generic_to_shared(src)), "r"(bytes), "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ uint64_t l2_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void at_mbar_init(uint64_t *bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
-}
-__device__ __forceinline__ void at_expect(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void at_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\tW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@!P1 bra W_%=;\n\t}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
-        "r"(parity), "r"(1000000u)
-        : "memory");
-}
-
-__global__ void __launch_bounds__(AT_THREADS, 1) adam_tma_kernel(
-    float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v, int64_t n,
-    const float *__restrict__ sched, int64_t sched_len, int64_t *__restrict__ step_counter, float b1, float omb1,
-    float b2, float omb2, float eps, float l2, uint32_t *__restrict__ nan_flag, double *__restrict__ loss_acc,
-    double *__restrict__ losses, int64_t t0, int64_t cap, double inv_b, uint32_t *__restrict__ ticket) {
-    extern __shared__ __align__(128) float at_smem[];
-    float *in = at_smem;                              // [AT_ST][4][AT_CH]: p, g, m, v
-    float *out = in + AT_ST * 4 * AT_CH;              // [2][3][AT_CH]: p, m, v
-    float *zeros = out + 2 * 3 * AT_CH;               // [AT_CH]
-    __shared__ uint64_t full[AT_ST];
-    const int tid = threadIdx.x;
-    const int64_t tc = *step_counter;
-    const int64_t ts = tc >= sched_len ? sched_len - 1 : tc;
-    const float lr = sched[3 * ts], c1 = sched[3 * ts + 1], c2 = sched[3 * ts + 2];
-    const int64_t nv = n & ~(int64_t)3;  // bulk-streamed prefix (16-byte multiple); tail below
-    const int64_t nchunks = (nv + AT_CH - 1) / AT_CH;
-    const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
-    float *arr[4] = {p, g, m, v};
-    for (int q = tid; q < AT_CH; q += AT_THREADS) zeros[q] = 0.0f;
-    if (tid == 0) {
-        for (int st = 0; st < AT_ST; ++st) at_mbar_init(&full[st]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto issue = [&](int64_t c, int st) {  // thread 0: the 4 loads of chunk c into stage st
-        const int64_t off = c * AT_CH;
-        const uint32_t bytes = (uint32_t)(min((int64_t)AT_CH, nv - off) * 4);
-        at_expect(&full[st], 4 * bytes);
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-            bulk_load(in + (st * 4 + a) * AT_CH, arr[a] + off, bytes, &full[st], a == 1 ? keep : stream);
-    };
-    if (tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int k = 0; k < AT_ST; ++k) {
-            const int64_t c = blockIdx.x + (int64_t)k * gridDim.x;
-            if (c < nchunks) issue(c, k);
-        }
-    }
-    bool bad = false;
-    uint32_t par = 0;
-    int k = 0;
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++k) {
-        const int st = k % AT_ST, ob = k & 1;
-        at_wait(&full[st], (par >> st) & 1u);
-        par ^= 1u << st;
-        const int64_t off = c * AT_CH;
-        const int cnt = (int)min((int64_t)AT_CH, nv - off);
-        if (tid == 0) bulk_wait_read<1>();  // the stores issued from out[ob] two chunks ago have read it
-        __syncthreads();
-        const float *ip = in + st * 4 * AT_CH;
-        float *op = out + ob * 3 * AT_CH;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = (tid * 2 + h) * 4;
-            if (e < cnt) {
-                float4 P = *reinterpret_cast<const float4 *>(ip + e);
-                float4 G = *reinterpret_cast<const float4 *>(ip + AT_CH + e);
-                float4 M = *reinterpret_cast<const float4 *>(ip + 2 * AT_CH + e);
-                float4 V = *reinterpret_cast<const float4 *>(ip + 3 * AT_CH + e);
-                bad |= isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w);
-                adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-                adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-                adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-                adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-                *reinterpret_cast<float4 *>(op + e) = P;
-                *reinterpret_cast<float4 *>(op + AT_CH + e) = M;
-                *reinterpret_cast<float4 *>(op + 2 * AT_CH + e) = V;
-            }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();  // outputs written, stage st fully read
-        if (tid == 0) {
-            const uint32_t bytes = (uint32_t)cnt * 4;
-            bulk_store(p + off, op, bytes, stream);
-            bulk_store(m + off, op + AT_CH, bytes, stream);
-            bulk_store(v + off, op + 2 * AT_CH, bytes, stream);
-            bulk_store(g + off, zeros, bytes, keep);  // the zeroed gradient stays in L2 for the scatter
-            bulk_commit();
-            const int64_t cn = c + (int64_t)AT_ST * gridDim.x;
-            if (cn < nchunks) issue(cn, st);
-        }
-    }
-    if (tid == 0) bulk_wait_all();
-    // scalar tail (n % 4 floats)
-    for (int64_t q = nv + (int64_t)blockIdx.x * AT_THREADS + tid; q < n; q += (int64_t)gridDim.x * AT_THREADS) {
-        float P = p[q], G = g[q], M = m[q], V = v[q];
-        bad |= isnan(G);
-        adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-        p[q] = P;
-        g[q] = G;
-        m[q] = M;
-        v[q] = V;
-    }
-    if (nan_flag && __any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicOr(nan_flag, 1u);
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
-            __threadfence();
-            const int64_t kk = tc - t0;
-            if (losses && kk >= 0 && kk < cap) losses[kk] = *reinterpret_cast<volatile double *>(loss_acc) * inv_b;
             if (loss_acc) *loss_acc = 0.0;
             *step_counter = tc + 1;
             *ticket = 0u;
@@ -632,28 +435,6 @@ int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, cons
     NVOL_REQUIRE(((uintptr_t)p & 127) == ((uintptr_t)g & 127) && ((uintptr_t)p & 127) == ((uintptr_t)m & 127) &&
                      ((uintptr_t)p & 127) == ((uintptr_t)v & 127) && ((uintptr_t)p & 3) == 0,
                  "flat Adam buffers must share their alignment modulo 128 bytes");
-    static int use_tma = -1;
-    if (use_tma < 0) {
-        const char *e = getenv("NVOL_ADAM_TMA");
-        use_tma = e ? atoi(e) : 0;  // measured slower than the grid-stride kernel on B200 (84 vs 67 us)
-    }
-    if (use_tma && ((uintptr_t)p & 15) == 0) {
-        const size_t smem = (size_t)(AT_ST * 4 + 2 * 3 + 1) * AT_CH * 4;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(adam_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t nch = ((n & ~(int64_t)3) + AT_CH - 1) / AT_CH;
-        const int grid = (int)max((int64_t)1, min((int64_t)sms, nch));
-        adam_tma_kernel<<<grid, AT_THREADS, smem, as_stream(stream)>>>(
-            p, g, m, v, n, sched, sched_len, step_counter, beta1, one_minus_beta1, beta2, one_minus_beta2, eps, l2,
-            nan_flag, loss_acc, losses, t0, cap, inv_b, ticket);
-        return check_launch("adam_train_step");
-    }
     adam_step_kernel<<<stream_grid((n + 3) / 4), 256, 0, as_stream(stream)>>>(
         p, g, m, v, n, sched, sched_len, step_counter, beta1, one_minus_beta1, beta2, one_minus_beta2, eps, l2,
         nan_flag, loss_acc, losses, t0, cap, inv_b, ticket);

@@ -1,4 +1,4 @@
-"""Accuracy + speed of the tcgen05 evaluator (NVOL_INFER_SPLIT=0/1) vs the exact one."""
+"""Accuracy + speed of the tcgen05 (split-fp16) evaluator vs the exact one."""
 import sys
 import time
 from pathlib import Path
