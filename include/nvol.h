@@ -47,7 +47,7 @@ extern "C" {
 /* ------------------------------------------------------------------ library */
 
 /* ABI version (bumped on any signature change; 2: the nvol_render camera parameter array gained
- * the image tile rows row0, nrows). */
+ * the image tile rows row0, nrows; 3: nvol_render path tracing block + 3 stats). */
 int nvol_abi_version(void);
 /* Static string describing the last non-zero status (thread-local). */
 const char *nvol_last_error(void);
@@ -306,14 +306,17 @@ int64_t nvol_render_workspace_bytes(int64_t n_pixels, int32_t k_batch);
  * up[3] (camera.py:44-56 basis, float64), tan_half, aspect, width, height,
  * row0, nrows (the image tile rendered: rows [row0, row0+nrows) of the frame;
  * multi-GPU renders give each rank a tile);
- * [host] render_params[20] = mode_shadow, use_mc, skip_empty, k_batch, s1,
+ * [host] render_params[29] = mode_shadow, use_mc, skip_empty, k_batch, s1,
  * s2, pexp, termination, ambient, density_scale, n_g, -light[3],
- * background[3], Dx, Dy, Dz.  TF tables as TransferFunction.tables
+ * background[3], Dx, Dy, Dz, then path tracing (mode "pathtrace",
+ * _render_kernels.py:566-878: delta tracking, NEE, Russian roulette):
+ * pathtrace, seed low 32 bits, seed high 32 bits, frame, rr_depth,
+ * light radiance[3], global majorant (f32-rounded).  TF tables as TransferFunction.tables
  * (transfer.py:43-47) [host].  mu: device macro-cell majorants (gz,gy,gx)
  * (a 1x1x1 dummy without macro-cells).  Field: a dense normalised grid
  * (use_grid) or the hash-grid model (tables [host], params/weights device).
  * img: device (nrows*W*3) float32.  stats_out [host]: {field evaluations,
- * iterations}; alive_hist [host]: rays alive per iteration (up to max_hist). */
+ * iterations, majorant violations}; alive_hist [host]: rays alive per iteration (up to max_hist). */
 int nvol_render(const double *cam_params, const double *render_params, const float *tf_cv,
                 const float *tf_crgb, int32_t ncv, const float *tf_ov, const float *tf_oa,
                 int32_t nov, const float *mu, int64_t gx, int64_t gy, int64_t gz, int32_t use_grid,

@@ -57,7 +57,7 @@ int nvol_set_deterministic(int32_t on) {
     return NVOL_OK;
 }
 
-int nvol_abi_version(void) { return 2; }  // 2: nvol_render camera params carry an image tile (row0, nrows)
+int nvol_abi_version(void) { return 3; }  // 3: nvol_render path tracing (render_params[29], stats_out[3])
 
 const char *nvol_last_error(void) { return nvol::g_last_error; }
 

@@ -40,11 +40,16 @@ struct RmScene {
     float sd[3], bg[3];
     double hx, hy, hz;
     TfTables tf;
+    // path tracing (render.py mode "pathtrace", _render_kernels.py:566-878)
+    int pathtrace, rr_depth;
+    uint64_t seed, frame;
+    float light[3];
+    double mu_glob;
 };
 
 struct RayState {
     float T, r, g, b, clock, sbar, best_w, best_t, Tsh, o[3], d[3], muc;
-    double cell_exit, march_end, tm[3], td[3];
+    double cell_exit, march_end, tm[3], td[3], t0;  // t0: float64 slab entry (path tracing starts there)
     int32_t pixel, phase, in_cell, pad0;
     int64_t c[3], st[3];
 };
@@ -346,6 +351,7 @@ __global__ void raygen_kernel(const CamParams cam, const RmScene S, RayState *__
     hit[p] = h_ ? 1 : 0;
     R.T = 1.0f;
     R.clock = (float)t0;
+    R.t0 = t0;
     R.Tsh = 1.0f;
     R.march_end = t1;
     R.pixel = (int32_t)p;
@@ -588,7 +594,7 @@ static int fill_scene(RmScene &S, const double *rp, const float *tf_cv, const fl
                       const float *tf_ov, const float *tf_oa, int nov, int64_t gx, int64_t gy, int64_t gz) {
     NVOL_REQUIRE(ncv >= 1 && ncv <= MAX_TF && nov >= 1 && nov <= MAX_TF, "transfer function has too many points");
     // rp: mode_shadow, use_mc, skip_empty, k_batch, s1, s2, pexp, term, ka, ds, ng,
-    //     sd[3], bg[3], hx, hy, hz
+    //     sd[3], bg[3], hx, hy, hz, then the path-tracing block below
     S.mode_shadow = (int)rp[0];
     S.use_mc = (int)rp[1];
     S.skip_empty = (int)rp[2];
@@ -607,6 +613,13 @@ static int fill_scene(RmScene &S, const double *rp, const float *tf_cv, const fl
     S.hx = rp[17];
     S.hy = rp[18];
     S.hz = rp[19];
+    // rp[20..28]: pathtrace, seed (low 32 bits, high 32 bits), frame, rr_depth, light radiance[3], mu_glob
+    S.pathtrace = (int)rp[20];
+    S.seed = (uint64_t)rp[21] | ((uint64_t)rp[22] << 32);
+    S.frame = (uint64_t)rp[23];
+    S.rr_depth = (int)rp[24];
+    for (int a = 0; a < 3; ++a) S.light[a] = (float)rp[25 + a];
+    S.mu_glob = rp[28];
     S.gx = gx;
     S.gy = gy;
     S.gz = gz;
@@ -621,6 +634,335 @@ static int fill_scene(RmScene &S, const double *rp, const float *tf_cv, const fl
         S.tf.oa[i] = tf_oa[i];
     }
     return NVOL_OK;
+}
+
+// ============================================================================ path tracing
+// _render_kernels.py:566-878 (delta / Woodcock tracking with macro-cell
+// majorants, next-event estimation toward a directional light, isotropic
+// scattering with TF-colour albedo, Russian roulette) + rng.py's counter RNG.
+// One tentative collision per ray per wavefront iteration, as pt_coord /
+// pt_shade; the mega-kernel runs the same helpers to completion per ray.
+struct PtState {
+    float thr[3], rad[3], o[3], d[3], cp[3], alb[3], mu_s;         // PTF
+    double t, t1, tau, cell_exit, tm[3], td[3];                      // PTD
+    int64_t pixel, event, role, bounces, tau_pending, in_cell, c[3], st[3];  // PTI
+};
+
+// rng.py / _render_kernels.py:26-49: SplitMix64-style key hash -> float32 in [0,1)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ float u01(uint64_t seed, uint64_t frame, int64_t pixel, int64_t event) {
+    uint64_t h = mix64(seed + 0x9E3779B97F4A7C15ull);
+    h = mix64(h + frame * 0xD1B54A32D192ED03ull);
+    h = mix64(h + (uint64_t)pixel * 0x8CB92BA72F3D8DD7ull);
+    h = mix64(h + (uint64_t)event * 0x9E3779B97F4A7C15ull);
+    return __fmul_rn((float)(h >> 40), 1.0f / 16777216.0f);
+}
+
+// _render_kernels.py:92-138 _dda_enter for the PT state
+__device__ void pt_dda_enter(const RmScene &S, PtState &P) {
+    const double t0 = P.t, ng = S.ng;
+    const int64_t gd[3] = {S.gx, S.gy, S.gz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double o = (double)P.o[a], d = (double)P.d[a];
+        const double p = o + t0 * d;
+        const int64_t c = clampl((int64_t)floor(p / ng), 0, gd[a] - 1);
+        P.c[a] = c;
+        if (d > 0.0) {
+            P.st[a] = 1;
+            P.tm[a] = t0 + ((double)(c + 1) * ng - p) / d;
+            P.td[a] = ng / d;
+        } else if (d < 0.0) {
+            P.st[a] = -1;
+            P.tm[a] = t0 + ((double)c * ng - p) / d;
+            P.td[a] = -ng / d;
+        } else {
+            P.st[a] = 0;
+            P.tm[a] = INFINITY;
+            P.td[a] = INFINITY;
+        }
+    }
+}
+
+__device__ __forceinline__ double pt_cell_exit(const PtState &P) {
+    double se = P.tm[0];
+    if (P.tm[1] < se) se = P.tm[1];
+    if (P.tm[2] < se) se = P.tm[2];
+    if (se > P.t1) se = P.t1;
+    return se;
+}
+
+// _render_kernels.py:582-628 _pt_after_nee (true = ray done)
+__device__ bool pt_after_nee(const RmScene &S, PtState &P) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) P.thr[c] = P.thr[c] * P.alb[c];
+    const float u1 = u01(S.seed, S.frame, P.pixel, P.event++);
+    const float u2 = u01(S.seed, S.frame, P.pixel, P.event++);
+    const double zz = 1.0 - 2.0 * (double)u1;
+    const double rr = sqrt(fmax(0.0, 1.0 - zz * zz));
+    const double ph = (2.0 * 3.141592653589793) * (double)u2;
+    P.d[0] = (float)(rr * cos(ph));
+    P.d[1] = (float)(rr * sin(ph));
+    P.d[2] = (float)zz;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) P.o[a] = P.cp[a];
+    double t0, t1;
+    if (!isect(P.o[0], P.o[1], P.o[2], P.d[0], P.d[1], P.d[2], S.hx, S.hy, S.hz, t0, t1)) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) P.rad[c] = P.rad[c] + P.thr[c] * S.bg[c];
+        P.role = 2;
+        return true;
+    }
+    P.t = t0;
+    P.t1 = t1;
+    P.tau_pending = 0;
+    P.in_cell = 0;
+    if (P.bounces > S.rr_depth) {
+        float q = P.thr[0];
+        if (P.thr[1] > q) q = P.thr[1];
+        if (P.thr[2] > q) q = P.thr[2];
+        if (q > 1.0f) q = 1.0f;
+        const float u = u01(S.seed, S.frame, P.pixel, P.event++);
+        if (u >= q) {
+            P.role = 2;
+            return true;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) P.thr[c] = P.thr[c] / q;
+    }
+    P.role = 0;
+    return false;
+}
+
+// _render_kernels.py:631-716 _pt_next: track until a tentative collision needs a
+// field value (1, P.t set) or the ray resolves (-1)
+__device__ float pt_next(const RmScene &S, const float *__restrict__ mu, PtState &P) {
+    for (;;) {
+        if (P.role == 2) return -1.0f;
+        if (P.tau_pending == 0) {
+            const float zeta = u01(S.seed, S.frame, P.pixel, P.event++);
+            P.tau = -log1p(-(double)zeta);
+            P.tau_pending = 1;
+        }
+        bool escape = false;
+        if (S.use_mc) {
+            if (P.in_cell == 0) {
+                pt_dda_enter(S, P);
+                P.cell_exit = pt_cell_exit(P);
+                P.in_cell = 1;
+            }
+            const float muc = mu_read(S, mu, P.c[0], P.c[1], P.c[2]);
+            if (muc > 0.0f) {
+                const double seg = P.cell_exit - P.t;
+                const double tauc = (double)muc * seg;
+                if (P.tau <= tauc) {
+                    P.t = P.t + P.tau / (double)muc;
+                    P.mu_s = muc;
+                    return 1.0f;
+                }
+                P.tau -= tauc;
+            }
+            if (P.cell_exit >= P.t1) {
+                escape = true;
+            } else {
+                P.t = P.cell_exit;
+                if (P.tm[0] <= P.tm[1] && P.tm[0] <= P.tm[2]) {
+                    P.c[0] += P.st[0];
+                    P.tm[0] = P.tm[0] + P.td[0];
+                } else if (P.tm[1] <= P.tm[2]) {
+                    P.c[1] += P.st[1];
+                    P.tm[1] = P.tm[1] + P.td[1];
+                } else {
+                    P.c[2] += P.st[2];
+                    P.tm[2] = P.tm[2] + P.td[2];
+                }
+                P.cell_exit = pt_cell_exit(P);
+            }
+        } else {
+            if (S.mu_glob > 0.0) {
+                const double seg = P.t1 - P.t;
+                const double tauc = S.mu_glob * seg;
+                if (P.tau <= tauc) {
+                    P.t = P.t + P.tau / S.mu_glob;
+                    P.mu_s = (float)S.mu_glob;
+                    return 1.0f;
+                }
+            }
+            escape = true;
+        }
+        if (escape) {
+            if (P.role == 0) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) P.rad[c] = P.rad[c] + P.thr[c] * S.bg[c];
+                P.role = 2;
+                return -1.0f;
+            }
+            // shadow ray reached the light: T_sh = 1, take the NEE contribution
+#pragma unroll
+            for (int c = 0; c < 3; ++c) P.rad[c] = P.rad[c] + P.thr[c] * P.alb[c] * S.light[c];
+            if (pt_after_nee(S, P)) return -1.0f;
+        }
+    }
+}
+
+// _render_kernels.py:719-736 _pt_stage_coord
+__device__ void pt_stage_coord(const RmScene &S, const PtState &P, float &x, float &y, float &z) {
+    const float one_below = __int_as_float(0x3f7fffff);
+    const double h[3] = {S.hx, S.hy, S.hz};
+    float v[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float c = (float)(((double)P.o[a] + P.t * (double)P.d[a]) / h[a]);
+        if (c < 0.0f) c = 0.0f;
+        if (c >= 1.0f) c = one_below;
+        v[a] = c;
+    }
+    x = v[0];
+    y = v[1];
+    z = v[2];
+}
+
+// _render_kernels.py:739-780 _pt_consume: accept / reject the tentative collision (true = done)
+__device__ bool pt_consume(const RmScene &S, PtState &P, float v, unsigned long long *violations) {
+    const float mu = P.mu_s;
+    float sig = tf_alpha(S.tf, v) * S.ds;
+    if (sig > mu * 1.0001f) {
+        atomicAdd(violations, 1ull);
+        sig = mu;
+    }
+    const float xi = u01(S.seed, S.frame, P.pixel, P.event++);
+    if (!((double)xi < (double)sig / (double)mu)) {
+        P.tau_pending = 0;  // null collision: fresh tau from here
+        return false;
+    }
+    if (P.role == 0) {
+        P.bounces += 1;
+        const double tc = P.t;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) P.cp[a] = (float)((double)P.o[a] + tc * (double)P.d[a]);
+        tf_rgb(S.tf, v, P.alb[0], P.alb[1], P.alb[2]);  // the collision's value doubles as albedo
+        double t0, t1;
+        if (!isect(P.cp[0], P.cp[1], P.cp[2], S.sd[0], S.sd[1], S.sd[2], S.hx, S.hy, S.hz, t0, t1)) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) P.rad[c] = P.rad[c] + P.thr[c] * P.alb[c] * S.light[c];
+            return pt_after_nee(S, P);
+        }
+        P.role = 1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            P.o[a] = P.cp[a];
+            P.d[a] = S.sd[a];
+        }
+        P.t = t0;
+        P.t1 = t1;
+        P.tau_pending = 0;
+        P.in_cell = 0;
+        return false;
+    }
+    return pt_after_nee(S, P);  // shadow ray hit something: occluded, no NEE contribution
+}
+
+__device__ __forceinline__ void pt_write(const PtState &P, float *__restrict__ img) {
+    img[3 * P.pixel] = P.rad[0];
+    img[3 * P.pixel + 1] = P.rad[1];
+    img[3 * P.pixel + 2] = P.rad[2];
+}
+
+// render.py:322-333 pt_state from the raygen / slab-test output
+__global__ void pt_init_kernel(const RayState *__restrict__ rays, int64_t n, PtState *__restrict__ pts) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const RayState R = rays[r];
+    PtState P;
+    memset(&P, 0, sizeof(P));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        P.thr[a] = 1.0f;
+        P.o[a] = R.o[a];
+        P.d[a] = R.d[a];
+    }
+    P.t = R.t0;
+    P.t1 = R.march_end;
+    P.pixel = R.pixel;
+    pts[r] = P;
+}
+
+// pt_coord (_render_kernels.py:830-852): one tentative collision per ray
+__global__ void pt_coord_kernel(PtState *__restrict__ pts, int64_t n, const RmScene S, const float *__restrict__ mu,
+                                float *__restrict__ sxyz, int32_t *__restrict__ counts, uint8_t *__restrict__ alive,
+                                float *__restrict__ img) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    PtState P = pts[r];
+    if (pt_next(S, mu, P) < 0.0f) {
+        pt_write(P, img);
+        counts[r] = 0;
+        alive[r] = 0;
+    } else {
+        pt_stage_coord(S, P, sxyz[3 * r], sxyz[3 * r + 1], sxyz[3 * r + 2]);
+        counts[r] = 1;
+        alive[r] = 1;
+    }
+    pts[r] = P;
+}
+
+// pt_shade (_render_kernels.py:855-878)
+__global__ void pt_shade_kernel(PtState *__restrict__ pts, int64_t n, const RmScene S,
+                                const float *__restrict__ values, const int32_t *__restrict__ counts,
+                                uint8_t *__restrict__ alive, float *__restrict__ img,
+                                unsigned long long *__restrict__ violations) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n || counts[r] == 0) return;
+    PtState P = pts[r];
+    if (pt_consume(S, P, values[r], violations)) {
+        pt_write(P, img);
+        alive[r] = 0;
+    }
+    pts[r] = P;
+}
+
+// pt_reference (_render_kernels.py:783-827): the mega-kernel path tracer
+template <int NN>
+__global__ void __launch_bounds__(FE_THREADS) pt_mega_kernel(PtState *__restrict__ pts, int64_t n, const RmScene S,
+                                                             const float *__restrict__ mu, const FieldDesc F,
+                                                             const GridTables tab, const MlpShape sh, int maxw,
+                                                             float *__restrict__ img,
+                                                             unsigned long long *__restrict__ evals,
+                                                             unsigned long long *__restrict__ violations) {
+    extern __shared__ float4 smem4[];
+    float *smem = reinterpret_cast<float *>(smem4);
+    float *wt = smem;
+    int wsz = F.use_grid ? 0 : stage_weights_t(F.weights, sh, wt);
+    float *h0 = wt + wsz, *h1 = h0 + maxw * FE_THREADS;
+    __syncthreads();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    PtState P = pts[r];
+    unsigned long long ev = 0;
+    float *col0 = h0 + threadIdx.x, *col1 = h1 + threadIdx.x;
+    for (;;) {
+        if (pt_next(S, mu, P) < 0.0f) break;
+        float x, y, z;
+        pt_stage_coord(S, P, x, y, z);
+        float v;
+        if (F.use_grid) {
+            v = trilinear_at(F.norm, F.ndx, F.ndy, F.ndz, x, y, z);
+        } else {
+            encode_exact(x, y, z, F.params, tab, col0);
+            if constexpr (NN > 0)
+                v = mlp_exact_reg<NN>(col0, tab.n_levels * tab.n_feat, wt, sh);
+            else
+                v = mlp_exact_smem(col0, col1, wt, sh);
+        }
+        ++ev;
+        if (pt_consume(S, P, v, violations)) break;
+    }
+    pt_write(P, img);
+    atomicAdd(evals, ev);
 }
 
 static void fill_cam(CamParams &C, const double *cp) {
@@ -699,6 +1041,103 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
 int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const uint32_t *o_w, uint32_t o_wout,
                    uint8_t *image, cudaStream_t s, const uint32_t *o_wlo);
 
+// pt_coord staging has exactly one sample per alive ray: count it for the frame stats
+__global__ void count_staged_kernel(const int32_t *__restrict__ counts, int64_t n,
+                                    unsigned long long *__restrict__ evals) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long c = (r < n) ? (unsigned long long)counts[r] : 0ull;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(evals, c);
+}
+
+// render.py:355-368 (pt_reference) and 396-423 (pathtrace branch of render_wavefront)
+static int render_pathtrace(const RmScene &S, const RenderWs &w, RayState *hits, int64_t n, const float *mu,
+                            const FieldDesc &F, const GridTables &tab, const MlpShape &sh, int maxw,
+                            const int32_t *widths, int32_t n_layers, int32_t relu_out, int32_t architecture,
+                            int32_t eval_mode, void *mlp_image, float *img, int32_t *alive_hist, int32_t max_hist,
+                            unsigned long long *violations, int &iters, cudaStream_t s) {
+    iters = 0;
+    if (n == 0) return NVOL_OK;
+    PtState *pts[2] = {nullptr, nullptr};
+    size_t sel_bytes = 0;
+    cub::DeviceSelect::Flagged(nullptr, sel_bytes, (PtState *)nullptr, (uint8_t *)nullptr, (PtState *)nullptr,
+                               (int64_t *)nullptr, n);
+    void *sel_tmp = nullptr;
+    if (cudaMallocAsync((void **)&pts[0], sizeof(PtState) * (size_t)n, s) != cudaSuccess ||
+        cudaMallocAsync((void **)&pts[1], sizeof(PtState) * (size_t)n, s) != cudaSuccess ||
+        cudaMallocAsync(&sel_tmp, sel_bytes, s) != cudaSuccess)
+        return check_launch("pathtrace state alloc");
+    pt_init_kernel<<<grid_for(n, 256), 256, 0, s>>>(hits, n, pts[0]);
+    int st = check_launch("pt_init");
+    int cur = 0;
+    if (st == NVOL_OK && architecture == 1) {
+        int wtot = 0;
+        for (int i = 0; i < (F.use_grid ? 0 : n_layers); ++i) wtot += widths[i] * widths[i + 1];
+        size_t smem = sizeof(float) * (((wtot + 3) & ~3) + 2 * (size_t)maxw * FE_THREADS);
+        int nn = (!F.use_grid && n_layers >= 2) ? widths[1] : 0;
+        bool uniform = !F.use_grid && n_layers >= 2;
+        for (int i = 1; i < n_layers && uniform; ++i) uniform &= widths[i] == nn;
+        unsigned grid = grid_for(n, FE_THREADS);
+#define LAUNCH_PT(NNV)                                                                                        \
+    do {                                                                                                      \
+        cudaFuncSetAttribute(pt_mega_kernel<NNV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+        pt_mega_kernel<NNV><<<grid, FE_THREADS, smem, s>>>(pts[0], n, S, mu, F, tab, sh, maxw, img, w.evals,  \
+                                                           violations);                                       \
+    } while (0)
+        if (uniform && nn == 16)
+            LAUNCH_PT(16);
+        else if (uniform && nn == 32)
+            LAUNCH_PT(32);
+        else if (uniform && nn == 64)
+            LAUNCH_PT(64);
+        else
+            LAUNCH_PT(0);
+#undef LAUNCH_PT
+        st = check_launch("pt_mega_kernel");
+        if (max_hist > 0) alive_hist[0] = (int32_t)n;
+        iters = 1;
+    } else {
+        while (st == NVOL_OK && n > 0) {
+            if (iters < max_hist) alive_hist[iters] = (int32_t)n;
+            ++iters;
+            PtState *ps = pts[cur];
+            pt_coord_kernel<<<grid_for(n, 128), 128, 0, s>>>(ps, n, S, mu, w.sxyz, w.counts, w.flags, img);
+            count_staged_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.counts, n, w.evals);
+            // dense evaluation of the staged collisions (rays that resolved stage none)
+            size_t cb = w.cub_bytes;
+            cub::DeviceScan::ExclusiveSum(w.cub_tmp, cb, w.counts, w.offs, (int)n, s);
+            compact_staged_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.sxyz, w.counts, w.offs, n, 1, w.dxyz, w.dtotal);
+            int32_t ns32 = 0;
+            cudaMemcpyAsync(&ns32, w.dtotal, 4, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            if (ns32 > 0) {
+                if (F.use_grid) {
+                    st = ::nvol_trilinear(F.norm, F.ndx, F.ndy, F.ndz, w.dxyz, ns32, w.dvals, s);
+                } else if (eval_mode == 1) {
+                    st = infer_tc_launch(w.dxyz, ns32, F.params, tab, F.weights, (uint8_t *)mlp_image, widths[1],
+                                         n_layers - 1, relu_out, 0, 0, 0, 0, 0, 0.0, 1.0, w.dvals, s, iters == 1);
+                } else {
+                    st = field_exact_launch(w.dxyz, ns32, F.params, tab, F.weights, widths, n_layers, relu_out, 0,
+                                            0, 0, 0, 0, 0.0, 1.0, w.dvals, s);
+                }
+                if (st) break;
+                scatter_staged_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.dvals, w.counts, w.offs, n, 1, w.values);
+            }
+            pt_shade_kernel<<<grid_for(n, 128), 128, 0, s>>>(ps, n, S, w.values, w.counts, w.flags, img, violations);
+            st = check_launch("pt_shade");
+            if (st) break;
+            cub::DeviceSelect::Flagged(sel_tmp, sel_bytes, ps, w.flags, pts[cur ^ 1], w.nsel, n, s);
+            cudaMemcpyAsync(&n, w.nsel, 8, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            cur ^= 1;
+        }
+    }
+    cudaFreeAsync(pts[0], s);
+    cudaFreeAsync(pts[1], s);
+    cudaFreeAsync(sel_tmp, s);
+    return st;
+}
+
 }  // namespace nvol
 
 using namespace nvol;
@@ -757,6 +1196,23 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
     cudaMemcpyAsync(&n, w.nsel, 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     int cur = 1, iters = 0;
+    if (S.pathtrace) {
+        unsigned long long *viol = nullptr;
+        if (cudaMallocAsync((void **)&viol, 8, s) != cudaSuccess) return check_launch("pathtrace alloc");
+        cudaMemsetAsync(viol, 0, 8, s);
+        st = render_pathtrace(S, w, w.rays[cur], n, mu, F, tab, sh, maxw, widths, n_layers, relu_out, architecture,
+                              eval_mode, mlp_image, img, alive_hist, max_hist, viol, iters, s);
+        if (st) return st;
+        unsigned long long ev = 0, vi = 0;
+        cudaMemcpyAsync(&ev, w.evals, 8, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(&vi, viol, 8, cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(viol, s);
+        cudaStreamSynchronize(s);
+        stats_out[0] = (int64_t)ev;
+        stats_out[1] = iters;
+        stats_out[2] = (int64_t)vi;
+        return check_launch("render (pathtrace)");
+    }
     if (architecture == 1) {
         // in-shader: one thread per ray to completion
         if (n > 0) {
@@ -833,8 +1289,11 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
     cudaStreamSynchronize(s);
     stats_out[0] = (int64_t)ev;
     stats_out[1] = iters;
+    stats_out[2] = 0;
     return check_launch("render");
 }
+
+
 
 int nvol_macrocell_ranges(const float *vals, int64_t dx, int64_t dy, int64_t dz, int64_t ng, int32_t clip,
                           float *lo, float *hi, void *stream) {

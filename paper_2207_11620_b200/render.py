@@ -22,7 +22,7 @@ from .camera import Camera
 from .errors import ConfigError
 from .macrocell import MacroCellGrid, macrocell_build, macrocell_from_model, macrocell_set_tf
 from .model import NeuralModel
-from .transfer import TransferFunction
+from .transfer import TransferFunction, tf_max_opacity
 from .volume import ScalarField
 
 MODES = ("raymarch", "raymarch_shadow", "pathtrace")
@@ -197,7 +197,7 @@ def _workspace(npix: int, k: int) -> torch.Tensor:
 
 
 def render_frame_device(phi, tf: TransferFunction, cam: Camera, cfg: RenderConfig, grid: MacroCellGrid | None,
-                        architecture: str = "wavefront", eval_mode: str | None = None, rows=None):
+                        architecture: str = "wavefront", eval_mode: str | None = None, rows=None, frame: int = 0):
     """One frame on the device -> (image (H,W,3) float32 device tensor, FrameStats).
 
     rows=(row0, nrows) renders only that image tile (an (nrows,W,3) image):
@@ -206,8 +206,6 @@ def render_frame_device(phi, tf: TransferFunction, cam: Camera, cfg: RenderConfi
     row0, nrows = (0, cam.height) if rows is None else (int(rows[0]), int(rows[1]))
     if row0 < 0 or nrows < 1 or row0 + nrows > cam.height:
         raise ConfigError(f"bad image tile rows {rows} for height {cam.height}")
-    if cfg.mode == "pathtrace":
-        raise ConfigError("pathtrace mode is outside the B200 hot path (ray marching only)")
     if architecture not in ("wavefront", "reference"):
         raise ConfigError(f"unknown architecture {architecture!r}; expected one of ['reference', 'wavefront']")
     dev = _lib.device()
@@ -244,17 +242,23 @@ def render_frame_device(phi, tf: TransferFunction, cam: Camera, cfg: RenderConfi
     gz, gy, gx = mu.shape
     cv, crgb, ov, oa = tf.tables
     ld = cfg.light_direction
+    seed = int(cfg.seed) & 0xFFFFFFFFFFFFFFFF
     rp = np.array([float(cfg.mode == "raymarch_shadow"), float(cfg.use_macrocells), float(cfg.skip_empty),
                    float(cfg.k_batch), float(np.float32(cfg.step_size)), float(np.float32(cfg.max_step)),
                    float(np.float32(cfg.step_exponent)), float(np.float32(TERMINATION)),
                    float(np.float32(cfg.ambient)), float(np.float32(tf.density_scale)), ng,
                    float(np.float32(-ld[0])), float(np.float32(-ld[1])), float(np.float32(-ld[2])),
-                   *[float(np.float32(b)) for b in cfg.background], *[float(d) for d in dims]], dtype=np.float64)
+                   *[float(np.float32(b)) for b in cfg.background], *[float(d) for d in dims],
+                   # path tracing (render.py:291-304 _Scene): seed split in 32-bit halves (exact in f64),
+                   # frame, Russian-roulette depth, light radiance (f32), global majorant rounded through f32
+                   float(cfg.mode == "pathtrace"), float(seed & 0xFFFFFFFF), float(seed >> 32), float(frame),
+                   float(cfg.rr_depth), *[float(np.float32(c)) for c in cfg.light_radiance],
+                   float(np.float32(tf_max_opacity(tf, 0.0, 1.0) * tf.density_scale))], dtype=np.float64)
     cp = cam.device_params(row0, nrows)
     npix = cam.width * nrows
     img = torch.empty((nrows, cam.width, 3), dtype=torch.float32, device=dev)
     ws = _workspace(npix, cfg.k_batch)
-    stats = (ctypes_i64 := np.zeros(2, dtype=np.int64))
+    stats = (ctypes_i64 := np.zeros(3, dtype=np.int64))
     hist = np.zeros(4096, dtype=np.int32)
     mlp_img = phi.mlp_image() if (isinstance(phi, NeuralModel) and emode == 1) else None
     c64 = np.ctypeslib.as_ctypes
@@ -266,7 +270,8 @@ def render_frame_device(phi, tf: TransferFunction, cam: Camera, cfg: RenderConfi
     ms = (time.perf_counter() - t0) * 1e3
     del img_ptr_keep
     iters = int(stats[1])
-    return img, FrameStats(evals=int(stats[0]), violations=0, alive_per_iteration=hist[:min(iters, len(hist))].tolist(),
+    return img, FrameStats(evals=int(stats[0]), violations=int(stats[2]),
+                           alive_per_iteration=hist[:min(iters, len(hist))].tolist(),
                            ms=ms)
 
 
@@ -274,7 +279,7 @@ def _one(architecture):
     def run(phi, tf, cam, cfg, grid=None, frame: int = 0, stats_out: list | None = None):
         if cfg.use_macrocells and grid is None:
             grid = ensure_macrocells(phi, tf, cfg, None)
-        img, st = render_frame_device(phi, tf, cam, cfg, grid, architecture)
+        img, st = render_frame_device(phi, tf, cam, cfg, grid, architecture, frame=frame)
         if stats_out is not None:
             stats_out.append(st)
         return img.cpu().numpy()
@@ -294,8 +299,8 @@ def render(phi, tf: TransferFunction, cam: Camera, cfg: RenderConfig, architectu
         raise ConfigError(f"unknown architecture {architecture!r}; expected one of ['reference', 'wavefront']")
     grid = ensure_macrocells(phi, tf, cfg, grid)
     fb = Framebuffer(cam.width, cam.height)
-    for _ in range(cfg.frames):
-        img, st = render_frame_device(phi, tf, cam, cfg, grid, architecture)
+    for f in range(cfg.frames):
+        img, st = render_frame_device(phi, tf, cam, cfg, grid, architecture, frame=f)
         if stats_out is not None:
             stats_out.append(st)
         accumulate(fb, img)

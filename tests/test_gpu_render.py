@@ -203,3 +203,62 @@ def test_render_tiles_assemble_bit_identically(scene):
             evals += s.evals
         assert torch.equal(torch.cat(parts), full)
         assert evals == st.evals
+
+
+# ----------------------------------------------------------------------------- path tracing (SURVEY 8 f item 3)
+
+PT_CASES = {
+    "pt_mc": dict(mode="pathtrace", use_macrocells=True, seed=3),
+    "pt_nomc": dict(mode="pathtrace", use_macrocells=False, seed=3),
+    "pt_mc_f4": dict(mode="pathtrace", use_macrocells=True, frames=4, seed=5, rr_depth=1),
+}
+
+
+@pytest.mark.parametrize("name", sorted(PT_CASES))
+def test_pathtrace_matches_reference(scene, name):
+    """Wavefront path tracer (exact evaluator) vs the reference's renders
+    (oracle/gen_golden_pathtrace.py): the counter RNG, the tracking arithmetic
+    (float64 / float32 in the reference's order) and the f32 casts follow the
+    reference, and the images and per-frame field-evaluation counts come out
+    bit-identical on these scenes (the device's float64 log1p / cos / sin agree
+    with glibc's to the bit here; an ulp difference could flip a rare
+    Monte-Carlo decision, which would show up as a failure of this bar)."""
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    g = golden("render_pathtrace.npz")
+    cfg = RenderConfig(**PT_CASES[name])
+    stats = []
+    model.infer_mode = "exact"
+    img = render(model, tf, cam, cfg, "wavefront", grid=grid if cfg.use_macrocells else None, stats_out=stats)
+    np.testing.assert_array_equal(img, g[f"img_{name}"])
+    np.testing.assert_array_equal([s.evals for s in stats], g[f"evals_{name}"])
+    np.testing.assert_array_equal([s.violations for s in stats], g[f"viol_{name}"])
+
+
+def test_pathtrace_grid_field_matches_reference(scene):
+    from paper_2207_11620_b200 import fields, macrocell
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    g = golden("render_pathtrace.npz")
+    fld = fields.rasterize("blobs", dims, host=True)
+    gridf = macrocell.macrocell_build(fld, n_g=8)
+    macrocell.macrocell_set_tf(gridf, tf)
+    img = render(fld, tf, cam, RenderConfig(mode="pathtrace", use_macrocells=True, seed=7), "wavefront", grid=gridf)
+    np.testing.assert_array_equal(img, g["img_pt_grid_mc"])
+
+
+def test_pathtrace_wavefront_equals_megakernel(scene):
+    """render_wavefront == render_reference bitwise for the path tracer, as the
+    reference's own test (test_render.py:90-113): same per-ray state machine,
+    one collision per wavefront iteration."""
+    from paper_2207_11620_b200.render import RenderConfig, render_reference, render_wavefront
+    z, dims, model, grid, tf, cam = scene
+    model.infer_mode = "exact"
+    for mc in (True, False):
+        cfg = RenderConfig(mode="pathtrace", use_macrocells=mc, seed=11)
+        s1, s2 = [], []
+        a = render_wavefront(model, tf, cam, cfg, grid=grid if mc else None, stats_out=s1)
+        b = render_reference(model, tf, cam, cfg, grid=grid if mc else None, stats_out=s2)
+        np.testing.assert_array_equal(a, b)
+        assert s1[0].evals == s2[0].evals
+        assert s1[0].violations == s2[0].violations
