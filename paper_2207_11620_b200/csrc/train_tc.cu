@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
         auto release = [&]() {            // smem operands written / TMEM reads done -> MMA warp
 #ifdef NVOL_TIMELINE
             if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * epi_n + 1, gtime());
+            if (t == 0 && lane == 0 && epi_n < 12) TL(3100 + epi_n * 8 + (warp & 7), gtime());
 #endif
             tc::fence_before();
             tc::fence_proxy_async();
@@ -562,7 +563,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                 par_acc ^= 1u;
                 tc::fence_after();
 #ifdef NVOL_TIMELINE
-                if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * (++epi_n), gtime());
+                ++epi_n;
+                if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * epi_n, gtime());
 #endif
                 const bool last = i == NH - 1;
                 uint8_t *dst = last ? lbuf : smem + sh.o_h[t][i + 1];
@@ -640,7 +642,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                 par_acc ^= 1u;
                 tc::fence_after();
 #ifdef NVOL_TIMELINE
-                if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * (++epi_n), gtime());
+                ++epi_n;
+                if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * epi_n, gtime());
 #endif
                 if (j == NH - 1 && hh == 0 && q == 0 && lane == 0) {
                     // the dW_out / dW_{NH-1} MMAs that read lbuf (h_NH) are done: reload X hi for dW_0

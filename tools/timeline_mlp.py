@@ -39,3 +39,9 @@ for t in range(2):
         if w == 0:
             break
         print(f"slot {t} epi {k:2d}: acc-ready {(w - t0) / 1e3:7.2f}  release {(r - t0) / 1e3 if r else -1:7.2f}")
+print("per-warp release (slot 0), us after kernel start, phases 1..11:")
+for k in range(1, 12):
+    row = [int(a[3100 + k * 8 + w]) for w in range(8)]
+    if all(r == 0 for r in row):
+        break
+    print(f"  epi {k:2d}: " + " ".join(f"{(r - t0) / 1e3:6.2f}" for r in row))
