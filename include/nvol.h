@@ -239,7 +239,8 @@ int nvol_decode(const float *params, const int64_t *level_off, const int64_t *le
  * data-parallel caller can all-reduce `grads` in between.
  * coords/targets: [b] rows of this rank; grad_scale = 1/B_global (L1 sign
  * gradient, network.py:108).  loss_sum (f64) accumulates sum |pred-target|.
- * mode 0 = SIMT fp32, 1 = tcgen05 (fp16 operands, fp32 accumulate). */
+ * mode 0 = SIMT fp32, 1 = tcgen05 (fp16 operands, fp32 accumulate), optionally
+ * or-ed with NVOL_TRAIN_PREENCODED / NVOL_TRAIN_ENCODE_ONLY (below). */
 int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int64_t b_global,
                        const float *params, float *grads, const int64_t *level_off,
                        const int64_t *level_res, const int64_t *level_entries,
@@ -291,6 +292,29 @@ int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, cons
                          float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
                          double *loss_acc, double *losses, int64_t t0, int64_t cap, double inv_b,
                          uint32_t *ticket, void *stream);
+
+/* nvol_train_fwd_bwd mode flags (tcgen05 engine, mode 1 only). */
+#define NVOL_TRAIN_PREENCODED 16  /* the workspace's tile buffer already holds this batch's encoding */
+#define NVOL_TRAIN_ENCODE_ONLY 32 /* run the encoder forward into the tile buffer and stop */
+
+/* nvol_adam_train_step fused with the NEXT step's encoder forward: one
+ * persistent launch whose CTAs split into an Adam sweep over the flat buffers
+ * (table order) and the encoding of next_coords [b,3] into the tcgen05 tile
+ * buffer of `workspace` (the nvol_train_fwd_bwd mode-1 workspace for batch b);
+ * level l is encoded as soon as the sweep has updated level l's table.  The
+ * next nvol_train_fwd_bwd then runs with mode 1 | NVOL_TRAIN_PREENCODED.
+ * work: zero-initialised u32[2 + NVOL_MAX_LEVELS], re-armed by the kernel.
+ * Same results as nvol_adam_train_step followed by the encode of next_coords
+ * with the updated parameters (trainer.py:61-77, network.py:160-183,
+ * _kernels.py:31-79). */
+int nvol_adam_encode_step(float *p, float *g, float *m, float *v, int64_t n, const float *sched,
+                          int64_t sched_len, int64_t *step_counter, float beta1, float one_minus_beta1,
+                          float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
+                          double *loss_acc, double *losses, int64_t t0, int64_t cap, double inv_b,
+                          uint32_t *work, const float *next_coords, int64_t b, const int64_t *level_off,
+                          const int64_t *level_res, const int64_t *level_entries,
+                          const uint8_t *level_dense, int32_t n_levels, int32_t n_feat, int32_t n_neurons,
+                          int32_t n_hidden, void *workspace, int64_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------ rendering */
 

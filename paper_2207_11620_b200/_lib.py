@@ -55,6 +55,8 @@ _SIGS = {
     "nvol_adam_flat_dev": [P, P, P, P, I64, P, I64, P, F32, F32, F32, F32, F32, F32, P, P],
     "nvol_adam_train_step": [P, P, P, P, I64, P, I64, P, F32, F32, F32, F32, F32, F32, P, P, P, I64, I64, F64, P,
                              P],
+    "nvol_adam_encode_step": [P, P, P, P, I64, P, I64, P, F32, F32, F32, F32, F32, F32, P, P, P, I64, I64, F64, P,
+                              P, I64, P, P, P, P, I32, I32, I32, I32, P, I64, P],
     "nvol_render_workspace_bytes": [I64, I32],
     "nvol_set_stage_events": [P, I32],
     "nvol_l2_persist": [I64],

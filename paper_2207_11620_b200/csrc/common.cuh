@@ -44,6 +44,21 @@ __device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ double xsqrt(double a) { return __dsqrt_rn(a); }
 
+// Adam update of one parameter: network.py:172-182, operation for operation.
+template <typename T>
+__device__ __forceinline__ void adam_one(T &p, T &g, T &m, T &v, T lr, T b1, T omb1, T b2, T omb2, T c1,
+                                         T c2, T eps, T l2) {
+    T geff = xadd(g, xmul(l2, p));
+    T mj = xadd(xmul(m, b1), xmul(omb1, geff));
+    T vj = xadd(xmul(v, b2), xmul(omb2, xmul(geff, geff)));
+    T mhat = xdiv(mj, c1);
+    T vhat = xdiv(vj, c2);
+    p = xsub(p, xdiv(xmul(lr, mhat), xadd(xsqrt(vhat), eps)));
+    m = mj;
+    v = vj;
+    g = (T)0;
+}
+
 // ----------------------------------------------------------------------------- grid tables
 // GridEncoder.kernel_tables() (encoding.py:174-177) packed by value.
 struct GridTables {

@@ -205,21 +205,6 @@ __global__ void loss_fold_kernel(const double *__restrict__ block_sums, int n, d
     }
 }
 
-// network.py:172-182, operation for operation.
-template <typename T>
-__device__ __forceinline__ void adam_one(T &p, T &g, T &m, T &v, T lr, T b1, T omb1, T b2, T omb2, T c1,
-                                         T c2, T eps, T l2) {
-    T geff = xadd(g, xmul(l2, p));
-    T mj = xadd(xmul(m, b1), xmul(omb1, geff));
-    T vj = xadd(xmul(v, b2), xmul(omb2, xmul(geff, geff)));
-    T mhat = xdiv(mj, c1);
-    T vhat = xdiv(vj, c2);
-    p = xsub(p, xdiv(xmul(lr, mhat), xadd(xsqrt(vhat), eps)));
-    m = mj;
-    v = vj;
-    g = (T)0;
-}
-
 template <typename T>
 __global__ void adam_kernel(T *__restrict__ p, T *__restrict__ g, T *__restrict__ m, T *__restrict__ v,
                             int64_t n, T lr, T b1, T omb1, T b2, T omb2, T c1, T c2, T eps, T l2) {

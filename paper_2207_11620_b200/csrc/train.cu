@@ -38,7 +38,7 @@ static int64_t ws_simt(int64_t b, int m, int n, int nn, int nh) {
 
 int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_t b_global, const float *params,
                     float *grads, const GridTables &tab, int nn, int nh, int relu_out, int loss_kind,
-                    double *loss_sum, void *workspace, int64_t ws_bytes, cudaStream_t s);
+                    double *loss_sum, void *workspace, int64_t ws_bytes, int flags, cudaStream_t s);
 int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh);
 
 }  // namespace nvol
@@ -67,6 +67,9 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
     GridTables tab;
     int st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
     if (st) return st;
+    const int flags = mode & ~15;  // NVOL_TRAIN_PREENCODED / NVOL_TRAIN_ENCODE_ONLY (tcgen05 engine)
+    mode &= 15;
+    NVOL_REQUIRE(flags == 0 || mode == 1, "encode flags need the tcgen05 engine (mode 1)");
     NVOL_REQUIRE(b >= 1 && b_global >= b, "bad batch");
     NVOL_REQUIRE(n_hidden >= 1 && n_hidden <= 10, "n_hidden_layers out of range");
     NVOL_REQUIRE(loss_kind == 0 || loss_kind == 1, "loss kind must be L1 or L2");
@@ -76,7 +79,7 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
     cudaStream_t s = as_stream(stream);
     if (mode == 1)
         return train_tc_launch(coords, targets, b, b_global, params, grads, tab, n_neurons, n_hidden, relu_out,
-                               loss_kind, loss_sum, workspace, workspace_bytes, s);
+                               loss_kind, loss_sum, workspace, workspace_bytes, flags, s);
     const int m = n_levels, n = n_feat, nn = n_neurons, nh = n_hidden;
     const int nl = nh + 1;
     Ws w{(char *)workspace, 0};

@@ -145,17 +145,24 @@ __device__ __forceinline__ float cw32(const Cell32 &c, int k) {
 }
 
 // ============================================================================ 1. encode
-template <int NF>
-__global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restrict__ coords, int64_t b,
-                                                           const float *__restrict__ params, const GridTables tab,
-                                                           int ninp, uint8_t *__restrict__ xtiles) {
+// Table reads: the standalone kernel may use the read-only path; the fused
+// Adam + encode kernel reads parameters other CTAs of the same launch just
+// wrote, so it loads through L2 (ld.global.cg, coherent).
+template <bool COHERENT, typename V>
+__device__ __forceinline__ V tab_ld(const V *p) {
+    if constexpr (COHERENT)
+        return __ldcg(p);
+    else
+        return __ldg(p);
+}
+
+// One (sample i, level l) item of the encoder forward (_kernels.py:31-79), bit-exact
+// fp32, split into fp16 hi + lo and stored straight into the UMMA tile layout.
+template <int NF, bool COHERENT>
+__device__ __forceinline__ void encode_item(const float *__restrict__ coords, const float *__restrict__ params,
+                                            const GridTables &tab, int ninp, uint8_t *__restrict__ xtiles, int l,
+                                            int64_t i) {
     const int m = tab.n_levels;
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= b * m) return;
-    // level-major: a warp covers 32 consecutive samples of one level (uniform
-    // level constants, coalesced coordinates, L1 reuse on coarse levels)
-    const int l = (int)(t / b);
-    const int64_t i = t - (int64_t)l * b;
     const int32_t res = tab.res[l];
     const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
     const bool dense = tab.dense[l] != 0;
@@ -168,24 +175,22 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
 #pragma unroll
     for (int k = 0; k < 8; ++k) sl[k] = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask, dense);
     if constexpr (NF == 2) {
-        // x-adjacent corners (k, k+1) whose slots differ only in bit 0 share
-        // one aligned 16-byte entry pair: fetch it with a single float4 load
-        // (a pair {e, e+1} is 16-byte aligned iff the level offset + 2e is a
-        // multiple of 4 floats; odd-sized dense levels shift later offsets)
+        // x-adjacent corners (k, k+1) whose slots differ only in bit 0 share one
+        // aligned 16-byte entry pair: fetch it with a single float4 load; the pair
+        // {lo, lo+1} is 16-byte aligned iff (address of entry 0) / 8 + lo is even
         float2 v[8];
-        // entry pair {lo, lo+1} is 16-byte aligned iff (address of entry 0) / 8 + lo is even
         const uint32_t par = (uint32_t)((reinterpret_cast<uintptr_t>(tb) >> 3) & 1u);
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
             const uint32_t lo = min(sl[k], sl[k + 1]);
             if (max(sl[k], sl[k + 1]) == lo + 1 && ((lo + par) & 1u) == 0u) {
-                const float4 q = __ldg(reinterpret_cast<const float4 *>(tb + 2 * (size_t)lo));
+                const float4 q = tab_ld<COHERENT>(reinterpret_cast<const float4 *>(tb + 2 * (size_t)lo));
                 const bool lo_first = sl[k] == lo;
                 v[k] = lo_first ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
                 v[k + 1] = lo_first ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
             } else {
-                v[k] = __ldg(reinterpret_cast<const float2 *>(tb) + sl[k]);
-                v[k + 1] = __ldg(reinterpret_cast<const float2 *>(tb) + sl[k + 1]);
+                v[k] = tab_ld<COHERENT>(reinterpret_cast<const float2 *>(tb) + sl[k]);
+                v[k + 1] = tab_ld<COHERENT>(reinterpret_cast<const float2 *>(tb) + sl[k + 1]);
             }
         }
 #pragma unroll
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
         for (int k = 0; k < 8; ++k) {
             float w = cw32(c, k);
 #pragma unroll
-            for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, __ldg(tb + (size_t)sl[k] * NF + f)));
+            for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, tab_ld<COHERENT>(tb + (size_t)sl[k] * NF + f)));
         }
     }
     const int64_t tile = i >> 7;
@@ -225,6 +230,210 @@ __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restri
         for (int cidx = m * NF; cidx < ninp; ++cidx) {
             *reinterpret_cast<__half *>(base + tc::tile_off(s, cidx, ninp)) = __float2half_rn(0.0f);
             *reinterpret_cast<__half *>(base_lo + tc::tile_off(s, cidx, ninp)) = __float2half_rn(0.0f);
+        }
+    }
+}
+
+template <int NF>
+__global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restrict__ coords, int64_t b,
+                                                           const float *__restrict__ params, const GridTables tab,
+                                                           int ninp, uint8_t *__restrict__ xtiles) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= b * tab.n_levels) return;
+    // level-major: a warp covers 32 consecutive samples of one level (uniform
+    // level constants, coalesced coordinates, L1 reuse on coarse levels)
+    const int l = (int)(t / b);
+    encode_item<NF, false>(coords, params, tab, ninp, xtiles, l, t - (int64_t)l * b);
+}
+
+// ---------------------------------------------------------------------------- Adam(k) + encode(k+1)
+// The step tail fused with the next step's encoder forward.  Adam streams the
+// flat buffers in table order (network.py:160-183); the encoder forward of the
+// NEXT batch (_kernels.py:31-79, sampled ahead on the side stream) of level l
+// only needs level l's updated table, so it can run as soon as the Adam sweep
+// has passed that level instead of after a kernel boundary.  CTAs take a role
+// in arrival order: the first n_adam to start sweep the flat buffers in
+// grid-stride chunks (chunk c after chunk c - n_adam, so the sweep advances
+// through the levels in order) and count finished chunks per level; the rest
+// run the encoder items level-major, each waiting (acquire) until its level's
+// chunk count is complete.  Arrival-order roles make the wait deadlock-free:
+// every chunk an encoder CTA waits on belongs to a CTA that is already running
+// and never waits.  The last CTA out records the loss, advances the step
+// counter and re-arms the work words.
+struct AdamArgs {
+    float *p, *g, *m, *v;
+    int64_t n;
+    const float *sched;
+    int64_t sched_len;
+    int64_t *counter;
+    float b1, omb1, b2, omb2, eps, l2;
+    uint32_t *nan_flag;
+    double *loss_acc, *losses;
+    int64_t t0, cap;
+    double inv_b;
+};
+
+// CTA = 4 Adam warps + 12 encoder warps (warp-specialised, 3 CTAs per SM).
+// Adam warps dequeue warp chunks (32 lanes x 8 float4 of each of p, g, m, v)
+// from an atomic counter, so the sweep runs in table order; each lane streams
+// its float4s through a 3-deep cp.async ring in shared memory (the in-flight
+// bytes live in shared memory, not registers, so 4 warps per CTA keep enough
+// DRAM traffic in flight) and publishes each finished chunk with a fence and
+// one add per level the chunk overlaps.  Encoder warps take (level, 32
+// samples) items level-major and poll (acquire) their level's chunk count
+// before gathering.  Dynamic dequeue keeps this deadlock-free whatever the
+// residency: every chunk is claimed by a running Adam warp, which never waits.
+constexpr int AE_ADAM_WARPS = 4, AE_ENC_WARPS = 12;
+constexpr int AE_THREADS = 32 * (AE_ADAM_WARPS + AE_ENC_WARPS);
+#ifndef NVOL_AE_CHUNK_U
+#define NVOL_AE_CHUNK_U 32
+#endif
+constexpr int AE_CHUNK_U = NVOL_AE_CHUNK_U;       // float4 per lane per chunk
+constexpr int AE_WARP_F4 = 32 * AE_CHUNK_U;       // 4,096 floats per array per chunk
+constexpr int AE_D = 3;                           // cp.async ring depth
+
+// Per-level range of warp chunks covering the level's table (host-computed).
+struct LevelChunks {
+    int32_t lo[NVOL_MAX_LEVELS], hi[NVOL_MAX_LEVELS];
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void adam_scalar(const AdamArgs &a, int64_t q, float lr, float c1, float c2, bool &bad) {
+    float P = a.p[q], G = a.g[q], M = a.m[q], V = a.v[q];
+    bad |= isnan(G);
+    adam_one<float>(P, G, M, V, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+    a.p[q] = P;
+    a.g[q] = G;
+    a.m[q] = M;
+    a.v[q] = V;
+}
+
+// work words: [0] chunk queue, [1] exit ticket, [2 + l] finished warp chunks of level l
+template <int NF>
+__global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, int64_t head, int64_t n4,
+                                                                    int64_t nch, const LevelChunks lc,
+                                                                    const float *__restrict__ coords, int64_t b,
+                                                                    const GridTables tab, int ninp,
+                                                                    uint8_t *__restrict__ xtiles,
+                                                                    uint32_t *__restrict__ work) {
+    __shared__ float4 ring[AE_D][4][AE_ADAM_WARPS * 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t tc = *a.counter;
+    const int m = tab.n_levels;
+    if (warp < AE_ADAM_WARPS) {
+        const int64_t t = tc >= a.sched_len ? a.sched_len - 1 : tc;
+        const float lr = a.sched[3 * t], c1 = a.sched[3 * t + 1], c2 = a.sched[3 * t + 2];
+        float4 *p4 = reinterpret_cast<float4 *>(a.p + head), *g4 = reinterpret_cast<float4 *>(a.g + head);
+        float4 *m4 = reinterpret_cast<float4 *>(a.m + head), *v4 = reinterpret_cast<float4 *>(a.v + head);
+        const uint64_t keep = l2_evict_last();
+        const int64_t ntail = a.n - head - 4 * n4;
+        bool bad = false;
+        auto dequeue = [&]() -> int64_t {
+            uint32_t c = 0;
+            if (lane == 0) c = atomicAdd(work, 1u);
+            return (int64_t)__shfl_sync(0xffffffffu, c, 0);
+        };
+        // prefetch cursor (pc, pu) runs AE_D slots ahead of the compute cursor (cc, cu)
+        int64_t cc = dequeue(), pc = cc, nxt = -1;
+        int pu = 0, cu = 0;
+        auto issue = [&](int slot) {
+            if (pc < nch) {
+                const int64_t j = pc * AE_WARP_F4 + pu * 32 + lane;
+                if (j < n4) {
+                    cp_async16(&ring[slot][0][tid], p4 + j);
+                    cp_async16(&ring[slot][1][tid], g4 + j);
+                    cp_async16(&ring[slot][2][tid], m4 + j);
+                    cp_async16(&ring[slot][3][tid], v4 + j);
+                }
+                if (++pu == AE_CHUNK_U) {
+                    pu = 0;
+                    pc = nxt = dequeue();
+                }
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int d = 0; d < AE_D; ++d) issue(d);
+        int slot = 0;
+        while (cc < nch) {
+            cp_async_wait<AE_D - 1>();
+            const int64_t j = cc * AE_WARP_F4 + cu * 32 + lane;
+            if (j < n4) {
+                float4 P = ring[slot][0][tid], G = ring[slot][1][tid], M = ring[slot][2][tid], V = ring[slot][3][tid];
+                bad |= isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w);
+                adam_one<float>(P.x, G.x, M.x, V.x, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                adam_one<float>(P.y, G.y, M.y, V.y, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                adam_one<float>(P.z, G.z, M.z, V.z, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                adam_one<float>(P.w, G.w, M.w, V.w, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                p4[j] = P;                    // default policy: the encoder warps gather it next
+                st4_hint(g4 + j, G, keep);    // the zeroed gradient stays in L2 for the next scatter
+                __stcs(m4 + j, M);
+                __stcs(v4 + j, V);
+            }
+            issue(slot);  // this lane's slot is consumed: refill it AE_D slots ahead
+            slot = slot + 1 == AE_D ? 0 : slot + 1;
+            if (++cu == AE_CHUNK_U) {
+                // chunk done: scalar head (chunk 0) / tail (last chunk), then publish
+                if (cc == 0 && lane < head) adam_scalar(a, lane, lr, c1, c2, bad);
+                if (cc == nch - 1 && lane < ntail) adam_scalar(a, head + 4 * n4 + lane, lr, c1, c2, bad);
+                __threadfence();
+                __syncwarp();
+                if (lane < m && lc.lo[lane] <= cc && cc <= lc.hi[lane]) atomicAdd(work + 2 + lane, 1u);
+                cu = 0;
+                cc = nxt;
+            }
+        }
+        cp_async_wait<0>();
+        if (a.nan_flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nan_flag, 1u);
+    } else {
+        const int64_t nblk = (b + 31) >> 5;
+        const int64_t n_enc = (int64_t)gridDim.x * AE_ENC_WARPS;
+        int ready = -1;
+        for (int64_t it = (int64_t)blockIdx.x * AE_ENC_WARPS + (warp - AE_ADAM_WARPS); it < nblk * m; it += n_enc) {
+            const int l = (int)(it / nblk);
+            const int64_t i = (it - (int64_t)l * nblk) * 32 + lane;
+            if (l > ready) {
+                // lane 0 polls (acquire) with backoff; __syncwarp orders the lanes' gathers after it
+                if (lane == 0) {
+                    const uint32_t need = (uint32_t)(lc.hi[l] - lc.lo[l] + 1);
+                    uint32_t ns = 256;
+                    for (;;) {
+                        uint32_t got;
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(work + 2 + l) : "memory");
+                        if (got >= need) break;
+                        __nanosleep(ns);
+                        ns = ns < 2048 ? 2 * ns : ns;
+                    }
+                }
+                __syncwarp();
+                ready = l;
+            }
+            if (i < b) encode_item<NF, true>(coords, a.p, tab, ninp, xtiles, l, i);
+        }
+    }
+    // exit ticket: the last CTA records the loss, advances the counter, re-arms the work words
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+            __threadfence();
+            const int64_t k = tc - a.t0;
+            if (a.losses && k >= 0 && k < a.cap) a.losses[k] = *reinterpret_cast<volatile double *>(a.loss_acc) * a.inv_b;
+            if (a.loss_acc) *a.loss_acc = 0.0;
+            *a.counter = tc + 1;
+            for (int l = 0; l < m; ++l) work[2 + l] = 0u;
+            work[0] = 0u;
+            work[1] = 0u;
         }
     }
 }
@@ -340,7 +549,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
     const TcShape sh, const float *__restrict__ wflat, double *__restrict__ loss_sum, float *__restrict__ dfeat,
     int64_t stride, float *__restrict__ dw_grads) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar_x[2], bar_xr[2], bar_acc[2], bar_op[2], bar_w;
+    __shared__ uint64_t bar_x[2], bar_xr[2], bar_acc[2], bar_op[2], bar_w, bar_dwo;
     __shared__ uint32_t tmem_base_sh;
     __shared__ double s_loss[PP_EPI_WARPS];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -358,6 +567,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
             tc::mbar_init(&bar_op[t], 8);  // one arrive per epilogue warp of the slot
         }
         tc::mbar_init(&bar_w, 1);
+        tc::mbar_init(&bar_dwo, 1);
         tc::fence_mbar_init();
         const uint32_t wbytes = (uint32_t)sh.w_floats * 4u;  // multiple of 16 (nn in {16, 32, 64})
         tc::mbar_arrive_expect_tx(&bar_w, wbytes);
@@ -416,7 +626,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
     if (warp == PP_EPI_WARPS) {
         // ================================================================ MMA issuer
         if (lane == 0) {
-            uint32_t par_x = 0, par_xr = 0, par_op = 0, dw_started = 0, started = 0;
+            uint32_t par_x = 0, par_xr = 0, par_op = 0, dw_started = 0, started = 0, par_dwo = 0;
             int64_t kt0 = 0, kt1 = 1;
             int ph0 = 0, ph1 = 0;
             const uint32_t idesc_fwd = tc::make_idesc(128, NN, 0, 0), idesc_fwd2 = tc::make_idesc(128, 2 * NN, 0, 0);
@@ -440,7 +650,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                         tc::mbar_wait(&bar_x[t], (par_x >> t) & 1u);
                         par_x ^= 1u << t;
                     }
-                    if (ph == nph - 1) {  // dW_0 reads the reloaded X hi tile
+                    if (ph == nph - 1 && NH > 1) {  // dW_0 reads the reloaded X hi tile
                         tc::mbar_wait(&bar_xr[t], (par_xr >> t) & 1u);
                         par_xr ^= 1u << t;
                     }
@@ -480,6 +690,20 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                                 tc::mma_f16(tmem + sh.t_dwout, ad + (uint64_t)(k * 2 * (NN / 8) * 8),
                                             bd + (uint64_t)(k * 16), id, (first || k > 0) ? 1 : 0);
                             dw_started |= 1u << 31;
+                            if (NH == 1) {
+                                // one hidden layer: dW_out (reads h_1 in lbuf) and dW_0 (reads the X hi
+                                // reload into lbuf) share this phase, so the reload happens here, after
+                                // the dW_out MMAs completed, instead of in the epilogue
+                                tc::mma_commit(&bar_dwo);
+                                tc::mbar_wait(&bar_dwo, par_dwo);
+                                par_dwo ^= 1u;
+                                tc::mbar_arrive_expect_tx(&bar_xr[t], sh.xhalf);
+                                tc::bulk_g2s(smem + sh.o_hlo[t], xtiles + ((int64_t)blockIdx.x + kt * (int64_t)gridDim.x) * xtile_bytes,
+                                             sh.xhalf, &bar_xr[t]);
+                                tc::mbar_wait(&bar_xr[t], (par_xr >> t) & 1u);
+                                par_xr ^= 1u << t;
+                                tc::fence_after();
+                            }
                         }
                         {
                             const uint32_t id = tc::make_idesc(128, win, 1, 1);
@@ -645,7 +869,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                 ++epi_n;
                 if ((warp & 7) == 0 && lane == 0) TL(1024 + t * 1024 + 2 * epi_n, gtime());
 #endif
-                if (j == NH - 1 && hh == 0 && q == 0 && lane == 0) {
+                if (j == NH - 1 && NH > 1 && hh == 0 && q == 0 && lane == 0) {
                     // the dW_out / dW_{NH-1} MMAs that read lbuf (h_NH) are done: reload X hi for dW_0
                     tc::mbar_arrive_expect_tx(&bar_xr[t], sh.xhalf);
                     tc::bulk_g2s(lbuf, xtiles + tile * xtile_bytes, sh.xhalf, &bar_xr[t]);
@@ -953,7 +1177,7 @@ static SideStreams &side_streams() {
 
 int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_t b_global, const float *params,
                     float *grads, const GridTables &tab, int nn, int nh, int relu_out, int loss_kind,
-                    double *loss_sum, void *workspace, int64_t ws_bytes, cudaStream_t s) {
+                    double *loss_sum, void *workspace, int64_t ws_bytes, int flags, cudaStream_t s) {
     TcPlan p;
     if (!make_plan(p, b, tab, nn, nh, relu_out, loss_kind)) {
         set_error("MLP / grid shape not supported by the tcgen05 path");
@@ -979,7 +1203,10 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
     // profiling: one chunk, events at the stage boundaries on the caller's stream
     cudaEvent_t *pev = g_stage_events;
     const bool prof = g_stage_events_n >= 4;
-    const int nc = prof ? 1 : p.nchunks;
+    // flags: 16 = the tile buffer already holds this batch's encoding (written by
+    // nvol_adam_encode_step), 32 = encode only
+    const bool pre = (flags & 16) != 0, only = (flags & 32) != 0;
+    const int nc = (prof || flags) ? 1 : p.nchunks;
     if (prof) cudaEventRecord(pev[0], s);
     SideStreams &ss = side_streams();
     cudaStream_t se = nc > 1 ? ss.enc : s, sc = nc > 1 ? ss.sc : s;
@@ -997,16 +1224,19 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         const unsigned egrid = grid_for(nb * tab.n_levels, 256);
         uint8_t *xtc = xt + t0 * tile_bytes;
         const float *cc = coords + 3 * r0;
-        if (nb % TILE)  // rows past the batch must be zero (0 x garbage could be NaN in dW)
-            cudaMemsetAsync(xtc + (nb / TILE) * tile_bytes, 0, (size_t)tile_bytes, se);
-        switch (tab.n_feat) {
-            case 1: encode_tiles_kernel<1><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
-            case 2: encode_tiles_kernel<2><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
-            case 4: encode_tiles_kernel<4><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
-            default: encode_tiles_kernel<8><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+        if (!pre) {
+            if (nb % TILE)  // rows past the batch must be zero (0 x garbage could be NaN in dW)
+                cudaMemsetAsync(xtc + (nb / TILE) * tile_bytes, 0, (size_t)tile_bytes, se);
+            switch (tab.n_feat) {
+                case 1: encode_tiles_kernel<1><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+                case 2: encode_tiles_kernel<2><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+                case 4: encode_tiles_kernel<4><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+                default: encode_tiles_kernel<8><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+            }
+            st = check_launch("encode_tiles_kernel");
+            if (st) return st;
         }
-        st = check_launch("encode_tiles_kernel");
-        if (st) return st;
+        if (only) return NVOL_OK;
         if (nc > 1) {
             cudaEventRecord(ss.enc_done[c], se);
             cudaStreamWaitEvent(s, ss.enc_done[c], 0);
@@ -1088,4 +1318,67 @@ extern "C" int nvol_has_tcgen05(int device) {
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
     return major == 10 && minor == 0;
+}
+
+// Step tail fused with the next step's encoder forward (adam_encode_kernel):
+// nvol_adam_train_step's update + bookkeeping, and the encoding of next_coords
+// into the tcgen05 tile buffer of `workspace`, so the next
+// nvol_train_fwd_bwd(mode 1 | NVOL_TRAIN_PREENCODED) skips its encode kernel.
+extern "C" int nvol_adam_encode_step(float *p, float *g, float *m, float *v, int64_t n, const float *sched,
+                                     int64_t sched_len, int64_t *step_counter, float beta1, float one_minus_beta1,
+                                     float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
+                                     double *loss_acc, double *losses, int64_t t0, int64_t cap, double inv_b,
+                                     uint32_t *work, const float *next_coords, int64_t b, const int64_t *level_off,
+                                     const int64_t *level_res, const int64_t *level_entries,
+                                     const uint8_t *level_dense, int32_t n_levels, int32_t n_feat, int32_t n_neurons,
+                                     int32_t n_hidden, void *workspace, int64_t workspace_bytes, void *stream) {
+    using namespace nvol;
+    NVOL_REQUIRE(p && g && m && v && sched && step_counter && work && sched_len >= 1, "null pointer");
+    NVOL_REQUIRE(next_coords && workspace && b >= 1, "null pointer");
+    NVOL_REQUIRE(((uintptr_t)p & 127) == ((uintptr_t)g & 127) && ((uintptr_t)p & 127) == ((uintptr_t)m & 127) &&
+                     ((uintptr_t)p & 127) == ((uintptr_t)v & 127) && ((uintptr_t)p & 3) == 0,
+                 "flat Adam buffers must share their alignment modulo 128 bytes");
+    GridTables tab;
+    int st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
+    if (st) return st;
+    TcPlan pl;
+    if (!make_plan(pl, b, tab, n_neurons, n_hidden, 1, 0)) {
+        set_error("MLP / grid shape not supported by the tcgen05 path");
+        return NVOL_EINVAL;
+    }
+    NVOL_REQUIRE(workspace_bytes >= pl.total, "workspace too small for the tcgen05 pipeline");
+    for (int l = 0; l < n_levels; ++l)
+        NVOL_REQUIRE(level_off[l] >= 0 && level_off[l] + level_entries[l] * n_feat <= n, "table outside the flat buffer");
+    cudaStream_t s = as_stream(stream);
+    uint8_t *xt = reinterpret_cast<uint8_t *>(workspace) + pl.off_x;
+    const int64_t tile_bytes = 2 * TILE * pl.sh.ninp * 2;
+    if (b % TILE) cudaMemsetAsync(xt + (b / TILE) * tile_bytes, 0, (size_t)tile_bytes, s);
+    AdamArgs a{p,    g,    m,    v,        n,        sched,  sched_len, step_counter, beta1, one_minus_beta1,
+               beta2, one_minus_beta2, eps, l2, nan_flag, loss_acc, losses, t0, cap, inv_b};
+    // flat layout: scalar head up to the next 128-byte boundary, float4 body in warp chunks, scalar tail
+    const int64_t head = std::min(n, (int64_t)(((128 - ((uintptr_t)p & 127)) & 127) >> 2));
+    const int64_t n4 = (n - head) >> 2;
+    const int64_t nch = std::max((int64_t)1, (n4 + AE_WARP_F4 - 1) / AE_WARP_F4);
+    auto chunk_of = [&](int64_t idx) -> int64_t {
+        return idx < head ? 0 : std::min((idx - head) / (4 * AE_WARP_F4), nch - 1);
+    };
+    NVOL_REQUIRE(nch < (1ll << 31), "flat buffer too large");
+    LevelChunks lc;
+    for (int l = 0; l < n_levels; ++l) {
+        lc.lo[l] = (int32_t)chunk_of(level_off[l]);
+        lc.hi[l] = (int32_t)chunk_of(level_off[l] + level_entries[l] * n_feat - 1);
+    }
+    auto launch = [&](auto kern) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, AE_THREADS, 0);
+        if (per_sm < 1) per_sm = 1;
+        kern<<<per_sm * num_sms(), AE_THREADS, 0, s>>>(a, head, n4, nch, lc, next_coords, b, tab, pl.sh.ninp, xt, work);
+    };
+    switch (n_feat) {
+        case 1: launch(adam_encode_kernel<1>); break;
+        case 2: launch(adam_encode_kernel<2>); break;
+        case 4: launch(adam_encode_kernel<4>); break;
+        default: launch(adam_encode_kernel<8>); break;
+    }
+    return check_launch("adam_encode_kernel");
 }

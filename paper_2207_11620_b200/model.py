@@ -40,6 +40,8 @@ _ENCODER_KIND_TO_OTYPE = {v: k for k, v in _ENCODER_OTYPES.items()}
 # Training-step engines (nvol_train_fwd_bwd `mode`).
 MODE_SIMT = 0      # generic kernels, fp32 CUDA cores
 MODE_TCGEN05 = 1   # fused tile pipeline, tcgen05 fp16 operands / fp32 accumulate
+TRAIN_PREENCODED = 16   # mode flag, nvol.h NVOL_TRAIN_PREENCODED
+TRAIN_ENCODE_ONLY = 32  # mode flag, nvol.h NVOL_TRAIN_ENCODE_ONLY
 
 
 def encoder_config_from_json(obj: dict) -> EncoderConfig:
@@ -236,8 +238,10 @@ class NeuralModel:
         return self._ws
 
     def fwd_bwd_device(self, coords: torch.Tensor, targets: torch.Tensor, loss_sum: torch.Tensor,
-                       b_global: Optional[int] = None) -> None:
-        """Encode -> MLP -> loss -> backprop -> encoder scatter into flat_grads (no Adam)."""
+                       b_global: Optional[int] = None, flags: int = 0) -> None:
+        """Encode -> MLP -> loss -> backprop -> encoder scatter into flat_grads (no Adam).
+        flags (tcgen05 engine): TRAIN_PREENCODED skips the encode (the tile buffer was
+        filled by nvol_adam_encode_step), TRAIN_ENCODE_ONLY stops after it."""
         b = coords.shape[0]
         c = self.encoder.config
         ws = self._workspace(b)
@@ -246,7 +250,7 @@ class NeuralModel:
                   _lib.ptr(self.flat_params), _lib.ptr(self.flat_grads), off, res, ent, dense, c.n_levels,
                   c.n_features_per_level, self.mlp.config.n_neurons, self.mlp.config.n_hidden_layers,
                   int(self.mlp.config.output_activation == "relu"), 0 if self.loss_kind == "L1" else 1,
-                  _lib.ptr(loss_sum), _lib.ptr(ws), ws.numel(), self._engine(), _lib.stream())
+                  _lib.ptr(loss_sum), _lib.ptr(ws), ws.numel(), self._engine() | flags, _lib.stream())
 
     def _engine(self) -> int:
         """Training engine for nvol_train_fwd_bwd: the fp32 SIMT engine (ordered

@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from .errors import ConfigError, FormatError
-from .model import NeuralModel, build_model
+from .model import MODE_TCGEN05, TRAIN_ENCODE_ONLY, TRAIN_PREENCODED, NeuralModel, build_model
 from .network import adam_scalars, lr_at
 from .sampler import InCoreSampler
 from .volume import ScalarField, VolumeMeta
@@ -127,6 +127,14 @@ class StepPipeline:
         self.overlap = ((not self.host_feed) and mc_grid is None
                         and os.environ.get("NVOL_SAMPLE_OVERLAP", "1") != "0")
         self.side = torch.cuda.Stream(device=dev) if self.overlap else None
+        # fused step tail (opt-in, NVOL_FUSED_TAIL=1): Adam + the NEXT batch's encoder
+        # forward in one launch (nvol_adam_encode_step); the next step's fwd/bwd then
+        # skips its encode.  Off by default: measured on B200 at cfg2 the two halves
+        # share L2 throughput, so the fused launch (145 us) is slower than Adam +
+        # encode back to back (70 + 31 us) -- DESIGN.md "Step-tail fusion"
+        self.fused = (self.overlap and self.train_mode == MODE_TCGEN05
+                      and os.environ.get("NVOL_FUSED_TAIL", "0") == "1")
+        self.work = torch.zeros(2 + 32, dtype=torch.int32, device=dev)   # NVOL_MAX_LEVELS
         if self.host_feed:
             self.copy_stream = torch.cuda.Stream(device=dev)
             self.ready = [torch.cuda.Event(), torch.cuda.Event()]
@@ -200,12 +208,24 @@ class StepPipeline:
         else:
             self.sample_into(parity, 0)
         c, t = self.bufs[parity]
-        m.fwd_bwd_device(c, t, self.acc, b_global=self.B)
+        m.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_PREENCODED if self.fused else 0)
         if self.world > 1:
             from .distributed import allreduce_grads
             allreduce_grads(m.flat_grads, self.acc, self.group)
         if self.overlap:
             main.wait_stream(self.side)                 # join before the counter advances
+        if self.fused:
+            cfg = m.encoder.config
+            off, res, ent, dense = m.encoder.c_tables()
+            ws = m._workspace(self.b)
+            _lib.call("nvol_adam_encode_step", _lib.ptr(m.flat_params), _lib.ptr(m.flat_grads), _lib.ptr(m.flat_m),
+                      _lib.ptr(m.flat_v), m.flat_size, _lib.ptr(self.sched), self.sched.numel() // 3,
+                      _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag), _lib.ptr(self.acc),
+                      _lib.ptr(self.losses), self.t0, self.capacity, 1.0 / self.B, _lib.ptr(self.work),
+                      _lib.ptr(self.bufs[parity ^ 1][0]), self.b, off, res, ent, dense, cfg.n_levels,
+                      cfg.n_features_per_level, m.mlp.config.n_neurons, m.mlp.config.n_hidden_layers,
+                      _lib.ptr(ws), ws.numel(), _lib.stream())
+            return
         _lib.call("nvol_adam_train_step", _lib.ptr(m.flat_params), _lib.ptr(m.flat_grads), _lib.ptr(m.flat_m),
                   _lib.ptr(m.flat_v), m.flat_size, _lib.ptr(self.sched), self.sched.numel() // 3,
                   _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag), _lib.ptr(self.acc),
@@ -215,6 +235,8 @@ class StepPipeline:
         """Kernels of one step from this library (for the bench's gpu_launches)."""
         if self.train_mode == 0:
             return 1 + 5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 + 1
+        if self.fused:
+            return 4    # sample (next step's), MLP, scatter, Adam + next encode
         # sample (next step's, overlapped), nchunks x (encode, MLP, scatter), Adam step
         # (chunk plan of train_tc.cu make_plan: NVOL_TRAIN_CHUNKS, default 1)
         ntiles = (self.b + 127) // 128
@@ -227,13 +249,18 @@ class StepPipeline:
         """Enqueue n steps (no host synchronisation)."""
         if self.done + n > self.capacity:
             raise ConfigError(f"pipeline capacity {self.capacity} exceeded")
-        for _ in range(n):
+        for k in range(n):
             parity = self.done & 1
             if self.host_feed:
                 self._feed(parity)
+            if self.done == 0 and self.overlap:
+                self.sample_into(0, 0)                  # the first batch, on the main stream
+            if k == 0 and self.fused:
+                # this call's first batch: encode it with the current parameters (the
+                # previous call's look-ahead encode may predate a parameter change)
+                c, t = self.bufs[parity]
+                self.model.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_ENCODE_ONLY)
             if self.done == 0:
-                if self.overlap:
-                    self.sample_into(0, 0)              # the first batch, on the main stream
                 self._body(parity)                      # eager first step (warms up / lazily allocates)
             elif not self.use_graph:
                 self._body(parity)

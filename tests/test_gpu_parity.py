@@ -341,7 +341,7 @@ def test_save_load_roundtrip(nv, tmp_path):
     np.testing.assert_array_equal(model.eval_batch(c), m2.eval_batch(c))
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "odd"])
 def test_tcgen05_step_matches_oracle(nv, name):
     """Fused tcgen05 fwd/bwd (fp16 operands, fp32 accumulate) vs the oracle's
     fp32 step on the same params and batch: loss, MLP and encoder gradients
@@ -405,6 +405,43 @@ def test_tcgen05_training_converges(nv):
         res[mode] = float(np.mean(runs))
     assert res[MODE_TCGEN05] > 20.0
     assert abs(res[MODE_TCGEN05] - res[0]) < 1.5, res
+
+
+@pytest.mark.parametrize("name,batch", [("cfg2", 8192), ("odd", 4000), ("cfg1", 1000)])
+def test_fused_adam_encode_tail(nv, name, batch, monkeypatch):
+    """nvol_adam_encode_step (Adam of step k + encode of batch k+1 in one launch):
+    the tile buffer it leaves is bit-identical to a fresh encode of the
+    look-ahead batch with the updated parameters, across train() calls and for
+    ragged batches; losses track the unfused pipeline."""
+    from paper_2207_11620_b200 import _lib, fields, trainer
+    from paper_2207_11620_b200.model import MODE_TCGEN05, TRAIN_ENCODE_ONLY, build_model
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    if not _lib.load().nvol_has_tcgen05(0):
+        pytest.skip("no tcgen05 device")
+    cfg = dict(golden_config(golden(f"encode_{name}.npz")), batch_size=batch)
+    fld = fields.rasterize("mlobb", (32, 32, 32), host=True)
+    losses = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("NVOL_FUSED_TAIL", fused)
+        model = build_model(cfg, dims=(32, 32, 32), seed=0)
+        model.train_mode = MODE_TCGEN05
+        sampler = InCoreSampler(fld, seed=1)
+        h1 = trainer.train(model, sampler, steps=6)
+        h2 = trainer.train(model, sampler, steps=4)
+        losses[fused] = np.concatenate([h1.losses, h2.losses])
+        pipe = model._pipeline
+        assert pipe.fused == (fused == "1") and pipe.done == 10 and model.opt.t == 10
+        if fused == "1":
+            assert pipe.launches_per_step() == 4
+            torch.cuda.synchronize()
+            assert int(pipe.work.abs().sum().item()) == 0        # work words re-armed
+            before = model._ws.clone()
+            c, t = pipe.bufs[pipe.done & 1]                       # the look-ahead batch (step 10)
+            model.fwd_bwd_device(c, t, pipe.acc, b_global=pipe.B, flags=TRAIN_ENCODE_ONLY)
+            torch.cuda.synchronize()
+            assert torch.equal(before, model._ws)
+    assert losses["1"][0] == pytest.approx(losses["0"][0], rel=1e-6)
+    np.testing.assert_allclose(losses["1"], losses["0"], rtol=2e-2)
 
 
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "odd"])
