@@ -269,6 +269,11 @@ int64_t nvol_l2_persist(int64_t bytes);
  * No reference counterpart (measurement). */
 int nvol_l2_probe(double *out);
 
+/* 1 if the tcgen05 training engine (nvol_train_fwd_bwd mode 1) takes this
+ * grid / MLP shape (n_neurons in {16, 32, 64}, 1..8 hidden layers, encoder
+ * width <= 2 * n_neurons, shared-memory and TMEM budgets), else 0. */
+int nvol_train_tc_supported(int32_t n_levels, int32_t n_feat, int32_t n_neurons, int32_t n_hidden);
+
 /* Workspace bytes nvol_train_fwd_bwd needs for batch b. */
 int64_t nvol_train_workspace_bytes(int64_t b, int32_t n_levels, int32_t n_feat, int32_t n_neurons,
                                    int32_t n_hidden, int32_t mode);

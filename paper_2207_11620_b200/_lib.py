@@ -52,6 +52,7 @@ _SIGS = {
     "nvol_decode": [P, P, P, P, P, I32, I32, P, P, I32, I32, I64, I64, I64, I64, I64, F64, F64, P, I32, P, P],
     "nvol_train_fwd_bwd": [P, P, I64, I64, P, P, P, P, P, P, I32, I32, I32, I32, I32, I32, P, P, I64, I32, P],
     "nvol_train_workspace_bytes": [I64, I32, I32, I32, I32, I32],
+    "nvol_train_tc_supported": [I32, I32, I32, I32],
     "nvol_adam_flat_dev": [P, P, P, P, I64, P, I64, P, F32, F32, F32, F32, F32, F32, P, P],
     "nvol_adam_train_step": [P, P, P, P, I64, P, I64, P, F32, F32, F32, F32, F32, F32, P, P, P, I64, I64, F64, P,
                              P],

@@ -1313,6 +1313,11 @@ extern "C" int64_t nvol_l2_persist(int64_t bytes) {
     return (int64_t)got;
 }
 
+extern "C" int nvol_train_tc_supported(int32_t n_levels, int32_t n_feat, int32_t n_neurons, int32_t n_hidden) {
+    nvol::TcShape sh;
+    return nvol::build_shape(sh, n_levels, n_feat, n_neurons, n_hidden, 1, 0) ? 1 : 0;
+}
+
 extern "C" int nvol_has_tcgen05(int device) {
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);

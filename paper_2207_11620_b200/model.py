@@ -252,6 +252,12 @@ class NeuralModel:
                   int(self.mlp.config.output_activation == "relu"), 0 if self.loss_kind == "L1" else 1,
                   _lib.ptr(loss_sum), _lib.ptr(ws), ws.numel(), self._engine() | flags, _lib.stream())
 
+    def tcgen05_supported(self) -> bool:
+        """Whether the tcgen05 training engine (MODE_TCGEN05) takes this model's shape."""
+        c = self.encoder.config
+        return bool(self._use_kernels() and _lib.load().nvol_train_tc_supported(
+            c.n_levels, c.n_features_per_level, self.mlp.config.n_neurons, self.mlp.config.n_hidden_layers))
+
     def _engine(self) -> int:
         """Training engine for nvol_train_fwd_bwd: the fp32 SIMT engine (ordered
         reductions) when bitwise repeatability is requested, else train_mode."""

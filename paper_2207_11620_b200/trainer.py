@@ -13,11 +13,13 @@ The per-step losses are read back once at the end.
 from __future__ import annotations
 
 import csv
+import gc
 import json
 import logging
 import struct
 import os
 import time
+import weakref
 from dataclasses import dataclass, field
 from pathlib import Path
 
@@ -88,7 +90,11 @@ class StepPipeline:
         from .distributed import shard_rows
         B = model.batch_size
         row0, b = shard_rows(B, rank, world)
-        self.model, self.sampler = model, sampler
+        # weak: the model caches its pipeline (model._pipeline), and a strong cycle would
+        # leave the old pipeline's graphs / streams / events to the cyclic collector,
+        # which can run inside a later graph capture and invalidate it
+        self._model = weakref.ref(model)
+        self.sampler = sampler
         self.train_mode = model._engine()
         self.B, self.b, self.row0 = B, b, row0
         self.world, self.group = world, group
@@ -145,6 +151,13 @@ class StepPipeline:
         self.use_graph = use_graph
         self.graphs = [None, None]
         self.done = 0
+
+    @property
+    def model(self) -> NeuralModel:
+        m = self._model()
+        if m is None:
+            raise ConfigError("the pipeline's model was released")
+        return m
 
     def sample_into(self, parity: int, ahead: int) -> None:
         """Sample the batch of step (device counter + ahead) into buffer `parity`."""
@@ -267,8 +280,16 @@ class StepPipeline:
             else:
                 if self.graphs[parity] is None:
                     g = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(g):
-                        self._body(parity)
+                    # no cyclic collection mid-capture: a destructor's CUDA call (event /
+                    # stream / graph teardown) would invalidate the capture
+                    gc_was = gc.isenabled()
+                    gc.disable()
+                    try:
+                        with torch.cuda.graph(g):
+                            self._body(parity)
+                    finally:
+                        if gc_was:
+                            gc.enable()
                     self.graphs[parity] = g
                 self.graphs[parity].replay()
             if self.host_feed:

@@ -383,6 +383,44 @@ def test_tcgen05_step_matches_oracle(nv, name):
     assert rel_err(model.encoder.param_grads.cpu().numpy(), cap["enc_grads"]) < 1e-3
 
 
+_TC_SHAPES = [(16, 1, 4, 2), (16, 3, 4, 2), (16, 8, 6, 2), (32, 1, 6, 4), (32, 2, 16, 2), (32, 5, 8, 8),
+              (64, 1, 16, 2), (64, 2, 8, 8), (64, 4, 16, 2), (64, 8, 16, 4), (32, 3, 3, 1), (64, 3, 16, 8)]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("nn,nh,levels,feat", _TC_SHAPES)
+def test_tcgen05_step_shape_sweep(nv, nn, nh, levels, feat):
+    """Every MLP / grid shape the tcgen05 engine accepts (nn in {16,32,64}, 1..8 hidden
+    layers, input width up to 2*nn) runs to completion and matches the fp32 SIMT engine
+    on the same batch: loss and gradients within the half-precision bar."""
+    from paper_2207_11620_b200 import _lib
+    from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
+    if not _lib.load().nvol_has_tcgen05(0):
+        pytest.skip("no tcgen05 device")
+    cfg = {"encoding": {"otype": "HashGrid", "n_levels": levels, "n_features_per_level": feat,
+                        "log2_hashmap_size": 12, "base_resolution": 4},
+           "network": {"n_neurons": nn, "n_hidden_layers": nh}, "batch_size": 3000, "loss": {"otype": "L2"}}
+    g = torch.Generator().manual_seed(nn * 100 + nh)
+    c = torch.rand((3000, 3), generator=g).cuda()
+    t = torch.rand(3000, generator=g).cuda()
+    if not build_model(cfg, dims=(16, 16, 16), seed=0).tcgen05_supported():
+        pytest.skip("shape outside the tcgen05 engine's shared-memory / width budget")
+    out = {}
+    for mode in (0, MODE_TCGEN05):
+        model = build_model(cfg, dims=(16, 16, 16), seed=0)
+        model.train_mode = mode
+        acc = torch.zeros(1, dtype=torch.float64, device="cuda")
+        model.fwd_bwd_device(c, t, acc)
+        torch.cuda.synchronize()
+        out[mode] = (float(acc.item()) / 3000, model.encoder.param_grads.cpu().numpy().copy(),
+                     [w.cpu().numpy().copy() for w in model.mlp.grads])
+    (l0, e0, w0), (l1, e1, w1) = out[0], out[MODE_TCGEN05]
+    assert l1 == pytest.approx(l0, rel=1e-2)
+    assert rel_l2(e1, e0) < 2e-2
+    for i, (a, b) in enumerate(zip(w1, w0)):
+        assert rel_l2(a, b) < 2e-2, i
+
+
 def test_tcgen05_training_converges(nv):
     """cfg2-encoder training with the tcgen05 engine tracks the fp32 engine.
     Single trajectories are chaotic under float-atomic summation order
