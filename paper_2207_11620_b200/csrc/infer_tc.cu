@@ -83,7 +83,8 @@ template <int NF>
 __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
     const float *__restrict__ coords, int64_t b, const float *__restrict__ params, const GridTables tab,
     const InferShape sh, const uint8_t *__restrict__ wimg, int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
-    double lo, double scale, float *__restrict__ out) {
+    double lo, double scale, float *__restrict__ out, const int32_t *__restrict__ b_dev) {
+    if (b_dev) b = *b_dev;  // sample count produced on the device (render loop), b was its upper bound
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_sh;
@@ -262,7 +263,8 @@ int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const 
 
 int infer_tc_launch(const float *coords, int64_t b, const float *params, const GridTables &tab, const float *wflat,
                     uint8_t *wimg, int nn, int nh, int relu_out, int decode, int64_t dx, int64_t dy, int64_t dz,
-                    int64_t z0, double lo, double scale, float *out, cudaStream_t s, bool pack = true) {
+                    int64_t z0, double lo, double scale, float *out, cudaStream_t s, bool pack = true,
+                    const int32_t *b_dev = nullptr) {
     InferShape sh;
     if (!build_infer_shape(sh, tab.n_levels, tab.n_feat, nn, nh, relu_out)) {
         set_error("MLP shape not supported by the tcgen05 inference path");
@@ -287,7 +289,7 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
     case NFV:                                                                                                  \
         cudaFuncSetAttribute(infer_tc_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes); \
         infer_tc_kernel<NFV><<<grid, IT_THREADS, sh.smem_bytes, s>>>(coords, b, params, tab, sh, wimg, decode, dx, dy, \
-                                                                    dz, z0, lo, scale, out);                   \
+                                                                    dz, z0, lo, scale, out, b_dev);            \
         break;
         LAUNCH_IT(1)
         LAUNCH_IT(2)

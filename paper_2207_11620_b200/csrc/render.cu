@@ -20,6 +20,8 @@
 // rounding, not bitwise.
 #include <cub/cub.cuh>
 
+#include <cmath>
+
 #include "common.cuh"
 #include "field_exact.cuh"
 
@@ -39,6 +41,7 @@ struct RmScene {
     double ng;
     float sd[3], bg[3];
     double hx, hy, hz;
+    double ihx, ihy, ihz, ing;  // exact reciprocals of power-of-two extents / cell size, else 0
     TfTables tf;
     // path tracing (render.py mode "pathtrace", _render_kernels.py:566-878)
     int pathtrace, rr_depth;
@@ -47,14 +50,27 @@ struct RmScene {
     double mu_glob;
 };
 
-struct RayState {
+// 192 bytes, 16-byte aligned so a ray loads / stores as 12 vector accesses.
+// pend / mdone carry one wavefront iteration's staging (count, march-ended
+// flag) from the sampling half of rm_step_kernel to the next call's shading half.
+struct alignas(16) RayState {
     float T, r, g, b, clock, sbar, best_w, best_t, Tsh, o[3], d[3], muc;
     double cell_exit, march_end, tm[3], td[3], t0;  // t0: float64 slab entry (path tracing starts there)
-    int32_t pixel, phase, in_cell, pad0;
-    int64_t c[3], st[3];
+    int32_t pixel, phase, in_cell, pend;
+    int32_t c[3], st[3], mdone, pad0;
 };
 
-__device__ __forceinline__ float powd(float x, float y) { return (float)pow((double)x, (double)y); }
+// pow in float64, rounded.  x^1 = x, 1^y = 1 and x^2 = x*x (a float64 product of
+// two floats is exact) are the values every faithful pow returns: taken directly.
+__device__ __forceinline__ float powd(float x, float y) {
+    if (y == 1.0f) return x;
+    if (x == 1.0f) return 1.0f;
+    if (y == 2.0f) return (float)((double)x * (double)x);
+    return (float)pow((double)x, (double)y);
+}
+
+// x / h, as a multiply when h is a power of two (ih = 1 / h exactly, else 0): bit-identical
+__device__ __forceinline__ double div_h(double x, double h, double ih) { return ih != 0.0 ? x * ih : x / h; }
 
 __device__ __forceinline__ int64_t clampl(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
@@ -88,7 +104,7 @@ __device__ void cell_entry(const RmScene &S, const float *__restrict__ mu, RaySt
     for (int a = 0; a < 3; ++a) {
         double o = (double)R.o[a], d = (double)R.d[a];
         double p = o + t0 * d;
-        int64_t c = clampl((int64_t)floor(p / ng), 0, gd[a] - 1);
+        int64_t c = clampl((int64_t)floor(div_h(p, ng, S.ing)), 0, gd[a] - 1);
         R.c[a] = c;
         if (d > 0.0) {
             R.st[a] = 1;
@@ -280,11 +296,11 @@ __device__ void rm_final(const RmScene &S, const RayState &R, float *__restrict_
 // _render_kernels.py:435-452
 __device__ void coord_at(const RmScene &S, const RayState &R, float ts, float &x, float &y, float &z) {
     const float one_below = 0.99999994f;
-    const double h[3] = {S.hx, S.hy, S.hz};
+    const double h[3] = {S.hx, S.hy, S.hz}, ih[3] = {S.ihx, S.ihy, S.ihz};
     float c[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        float v = (float)(((double)R.o[a] + (double)ts * (double)R.d[a]) / h[a]);
+        float v = (float)div_h((double)R.o[a] + (double)ts * (double)R.d[a], h[a], ih[a]);
         if (v < 0.0f) v = 0.0f;
         if (v >= 1.0f) v = one_below;
         c[a] = v;
@@ -303,15 +319,9 @@ struct CamParams {
     int64_t row0, nrows;  // image tile: rows [row0, row0 + nrows) of the width x height frame
 };
 
-// camera.py:117-143 (float64, cast to float32) + render.py:225-243 slab test
-__global__ void raygen_kernel(const CamParams cam, const RmScene S, RayState *__restrict__ rays,
-                              uint8_t *__restrict__ hit, float *__restrict__ img) {
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel within the tile
-    const int64_t n = cam.width * cam.nrows;
-    if (p >= n) return;
-    img[3 * p] = S.bg[0];
-    img[3 * p + 1] = S.bg[1];
-    img[3 * p + 2] = S.bg[2];
+// camera.py:117-143 (float64, cast to float32) + render.py:225-243 slab test:
+// the ray of tile pixel p and whether it hits the volume box
+__device__ __forceinline__ bool make_ray(const CamParams &cam, const RmScene &S, int64_t p, RayState &R) {
     const int64_t pf = p + cam.row0 * cam.width;  // pixel index in the full frame (camera.py:117-125)
     double ii = (double)(pf % cam.width), jj = floor((double)pf / (double)cam.width);
     double nx = ((ii + 0.5) / (double)cam.width * 2.0 - 1.0) * (cam.tan_half * cam.aspect);
@@ -320,7 +330,6 @@ __global__ void raygen_kernel(const CamParams cam, const RmScene S, RayState *__
 #pragma unroll
     for (int a = 0; a < 3; ++a) d[a] = cam.fwd[a] + nx * cam.right[a] + ny * cam.up[a];
     double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    RayState R;
     memset(&R, 0, sizeof(R));
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -347,15 +356,51 @@ __global__ void raygen_kernel(const CamParams cam, const RmScene S, RayState *__
         up = fmin(up, u);
     }
     double t0 = fmax(lo, 0.0), t1 = up;
-    bool h_ = t1 > t0;
-    hit[p] = h_ ? 1 : 0;
     R.T = 1.0f;
     R.clock = (float)t0;
     R.t0 = t0;
     R.Tsh = 1.0f;
     R.march_end = t1;
     R.pixel = (int32_t)p;
-    rays[p] = R;
+    return t1 > t0;
+}
+
+// background into every pixel of the tile + the hit flags (the stable selection
+// of hit pixel ids then orders the rays as the reference's boolean gather does)
+__global__ void ray_hits_kernel(const CamParams cam, const RmScene S, uint8_t *__restrict__ hit,
+                                float *__restrict__ img) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel within the tile
+    const int64_t n = cam.width * cam.nrows;
+    if (p >= n) return;
+    img[3 * p] = S.bg[0];
+    img[3 * p + 1] = S.bg[1];
+    img[3 * p + 2] = S.bg[2];
+    RayState R;
+    hit[p] = make_ray(cam, S, p, R) ? 1 : 0;
+}
+
+__global__ void set_count_kernel(int64_t *__restrict__ c, int64_t v) { *c = v; }
+
+__global__ void iota_kernel(int32_t *__restrict__ ids, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) ids[i] = (int32_t)i;
+}
+
+// the initial state of hit ray i (pixel ids[i]), staged through shared memory so
+// the 192-byte records leave as coalesced 16-byte stores
+constexpr int RG_THREADS = 128;
+__global__ void __launch_bounds__(RG_THREADS) raygen_kernel(const CamParams cam, const RmScene S,
+                                                            const int32_t *__restrict__ ids, int64_t n,
+                                                            RayState *__restrict__ rays) {
+    __shared__ RayState st[RG_THREADS];
+    const int64_t i0 = (int64_t)blockIdx.x * RG_THREADS, i = i0 + threadIdx.x;
+    if (i < n) make_ray(cam, S, ids[i], st[threadIdx.x]);
+    __syncthreads();
+    const int64_t cnt = min((int64_t)RG_THREADS, n - i0);
+    const uint4 *src = reinterpret_cast<const uint4 *>(st);
+    uint4 *dst = reinterpret_cast<uint4 *>(rays + i0);
+    constexpr int Q = (int)(sizeof(RayState) / 16);
+    for (int64_t q = threadIdx.x; q < cnt * Q; q += RG_THREADS) dst[q] = src[q];
 }
 
 // ----------------------------------------------------------------------------- field for the in-shader marcher
@@ -419,50 +464,118 @@ __global__ void __launch_bounds__(FE_THREADS) rm_mega_kernel(RayState *__restric
 }
 
 // ----------------------------------------------------------------------------- wavefront stages
-// _render_kernels.py:491-515 rm_coord
-__global__ void rm_coord_kernel(RayState *__restrict__ rays, int64_t n, const RmScene S, const float *__restrict__ mu,
-                                float *__restrict__ sxyz, float *__restrict__ sts, float *__restrict__ ssbar,
-                                int32_t *__restrict__ counts, uint8_t *__restrict__ mdone,
-                                unsigned long long *__restrict__ evals) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    RayState R = rays[r];
-    const int K = S.k_batch;
-    int c = 0;
-    uint8_t done = 0;
-    while (c < K) {
-        float ts = rm_next(S, mu, R);
-        if (ts < 0.0f) {
-            done = 1;
-            break;
+// One wavefront iteration per alive ray (rays[ids[pos]]): the shading half of
+// the previous iteration (_render_kernels.py:543-563 rm_shade: composite the
+// evaluated staged samples, end the march / phase, write the pixel) followed by
+// the sampling half of this one (_render_kernels.py:491-515 rm_coord: stage up
+// to K samples).  Fusing the two halves touches each ray record once per
+// iteration.  Staging is addressed by ray (ray * K + c); counts / keep by
+// position for the compaction that follows.
+__global__ void __launch_bounds__(128) rm_step_kernel(const int32_t *__restrict__ ids, int64_t n,
+                                                      const int64_t *__restrict__ n_dev,
+                                                      RayState *__restrict__ rays, const RmScene S,
+                                                      const float *__restrict__ mu, int shade,
+                                                      const float *__restrict__ values, float *__restrict__ sxyz,
+                                                      float *__restrict__ sts, float *__restrict__ ssbar,
+                                                      int32_t *__restrict__ counts, uint8_t *__restrict__ keep,
+                                                      float *__restrict__ img, unsigned long long *__restrict__ evals,
+                                                      int32_t *__restrict__ coord_rays) {
+    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int c = 0, marched = 0;
+    // n_dev: the alive count produced on the device; n is then only its upper bound
+    // (launch size), and positions in [*n_dev, n) stage nothing and keep nothing
+    const int64_t nact = n_dev ? *n_dev : n;
+    if (pos < n && pos >= nact) {
+        counts[pos] = 0;
+        keep[pos] = 0;
+    } else if (pos < n) {
+        const int64_t ray = ids[pos];
+        RayState R = rays[ray];
+        const int K = S.k_batch;
+        bool alive = true;
+        if (shade) {
+            bool ended = false;
+            for (int q = 0; q < R.pend; ++q) {
+                const int64_t i = ray * K + q;
+                if (rm_consume(S, R, values[i], sts[i], ssbar[i])) {
+                    ended = true;
+                    break;
+                }
+            }
+            if (!ended && R.mdone) ended = true;
+            if (ended && rm_phase_end(S, R)) {
+                rm_final(S, R, img);
+                alive = false;
+            }
         }
-        float x, y, z;
-        coord_at(S, R, ts, x, y, z);
-        int64_t i = r * K + c;
-        sxyz[3 * i] = x;
-        sxyz[3 * i + 1] = y;
-        sxyz[3 * i + 2] = z;
-        sts[i] = ts;
-        ssbar[i] = R.sbar;
-        ++c;
+        if (alive) {
+            marched = 1;
+            int done = 0;
+            while (c < K) {
+                float ts = rm_next(S, mu, R);
+                if (ts < 0.0f) {
+                    done = 1;
+                    break;
+                }
+                float x, y, z;
+                coord_at(S, R, ts, x, y, z);
+                const int64_t i = ray * K + c;
+                sxyz[3 * i] = x;
+                sxyz[3 * i + 1] = y;
+                sxyz[3 * i + 2] = z;
+                sts[i] = ts;
+                ssbar[i] = R.sbar;
+                ++c;
+            }
+            R.pend = c;
+            R.mdone = done;
+            rays[ray] = R;
+        }
+        counts[pos] = c;
+        keep[pos] = alive ? 1 : 0;
     }
-    for (int q = c; q < K; ++q) {  // holes: a valid coordinate the batched evaluator may read
-        int64_t i = r * K + q;
-        sxyz[3 * i] = sxyz[3 * i + 1] = sxyz[3 * i + 2] = 0.0f;
-    }
-    counts[r] = c;
-    mdone[r] = done;
-    rays[r] = R;
     // phi_eval_staged evaluates exactly the staged samples (_render_kernels.py:518-540)
     unsigned long long tot = (unsigned long long)c;
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(__activemask(), tot, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(evals, tot);
+    int m = marched;
+    for (int o = 16; o > 0; o >>= 1) {
+        tot += __shfl_down_sync(0xffffffffu, tot, o);
+        m += __shfl_down_sync(0xffffffffu, m, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (tot) atomicAdd(evals, tot);
+        if (m) atomicAdd(coord_rays, m);
+    }
 }
 
-// _render_kernels.py:543-563 rm_shade
-// phi_eval_staged (_render_kernels.py:518-540) evaluates only the staged
-// samples: the [n][K] staging (holes past counts[r]) is compacted with the
-// exclusive scan offs, evaluated densely, and scattered back.
+// the staged samples of the alive rays, densely: dxyz[offs[pos] + j] = sxyz[ids[pos] * K + j]
+__global__ void compact_ids_kernel(const float *__restrict__ sxyz, const int32_t *__restrict__ ids,
+                                   const int32_t *__restrict__ counts, const int32_t *__restrict__ offs, int64_t n,
+                                   int K, float *__restrict__ dxyz, int32_t *__restrict__ total) {
+    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= n) return;
+    const int c = counts[pos], o = offs[pos];
+    const int64_t ray = ids[pos];
+    for (int j = 0; j < c; ++j) {
+        const int64_t i = ray * K + j;
+        dxyz[3 * (int64_t)(o + j)] = sxyz[3 * i];
+        dxyz[3 * (int64_t)(o + j) + 1] = sxyz[3 * i + 1];
+        dxyz[3 * (int64_t)(o + j) + 2] = sxyz[3 * i + 2];
+    }
+    if (pos == n - 1) *total = o + c;
+}
+
+__global__ void scatter_ids_kernel(const float *__restrict__ dvals, const int32_t *__restrict__ ids,
+                                   const int32_t *__restrict__ counts, const int32_t *__restrict__ offs, int64_t n,
+                                   int K, float *__restrict__ values) {
+    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= n) return;
+    const int c = counts[pos], o = offs[pos];
+    const int64_t ray = ids[pos];
+    for (int j = 0; j < c; ++j) values[ray * K + j] = dvals[o + j];
+}
+
+// Path tracing's position-indexed staging (one slot per ray): compacted with the
+// exclusive scan offs, evaluated densely, scattered back.
 __global__ void compact_staged_kernel(const float *__restrict__ sxyz, const int32_t *__restrict__ counts,
                                       const int32_t *__restrict__ offs, int64_t n, int K, float *__restrict__ dxyz,
                                       int32_t *__restrict__ total) {
@@ -484,33 +597,6 @@ __global__ void scatter_staged_kernel(const float *__restrict__ dvals, const int
     if (r >= n) return;
     const int c = counts[r], o = offs[r];
     for (int j = 0; j < c; ++j) values[r * K + j] = dvals[o + j];
-}
-
-__global__ void rm_shade_kernel(RayState *__restrict__ rays, int64_t n, const RmScene S,
-                                const float *__restrict__ values, const float *__restrict__ sts,
-                                const float *__restrict__ ssbar, const int32_t *__restrict__ counts,
-                                const uint8_t *__restrict__ mdone, float *__restrict__ img,
-                                uint8_t *__restrict__ alive) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    RayState R = rays[r];
-    const int K = S.k_batch;
-    bool ended = false;
-    for (int c = 0; c < counts[r]; ++c) {
-        int64_t i = r * K + c;
-        if (rm_consume(S, R, values[i], sts[i], ssbar[i])) {
-            ended = true;
-            break;
-        }
-    }
-    if (!ended && mdone[r]) ended = true;
-    bool al = true;
-    if (ended && rm_phase_end(S, R)) {
-        rm_final(S, R, img);
-        al = false;
-    }
-    alive[r] = al ? 1 : 0;
-    rays[r] = R;
 }
 
 // ----------------------------------------------------------------------------- macro-cells
@@ -613,6 +699,14 @@ static int fill_scene(RmScene &S, const double *rp, const float *tf_cv, const fl
     S.hx = rp[17];
     S.hy = rp[18];
     S.hz = rp[19];
+    auto exact_inv = [](double h) {
+        int e = 0;
+        return (h > 0.0 && std::frexp(h, &e) == 0.5) ? 1.0 / h : 0.0;
+    };
+    S.ihx = exact_inv(S.hx);
+    S.ihy = exact_inv(S.hy);
+    S.ihz = exact_inv(S.hz);
+    S.ing = exact_inv(S.ng);
     // rp[20..28]: pathtrace, seed (low 32 bits, high 32 bits), frame, rr_depth, light radiance[3], mu_glob
     S.pathtrace = (int)rp[20];
     S.seed = (uint64_t)rp[21] | ((uint64_t)rp[22] << 32);
@@ -670,7 +764,7 @@ __device__ void pt_dda_enter(const RmScene &S, PtState &P) {
     for (int a = 0; a < 3; ++a) {
         const double o = (double)P.o[a], d = (double)P.d[a];
         const double p = o + t0 * d;
-        const int64_t c = clampl((int64_t)floor(p / ng), 0, gd[a] - 1);
+        const int64_t c = clampl((int64_t)floor(div_h(p, ng, S.ing)), 0, gd[a] - 1);
         P.c[a] = c;
         if (d > 0.0) {
             P.st[a] = 1;
@@ -812,11 +906,11 @@ __device__ float pt_next(const RmScene &S, const float *__restrict__ mu, PtState
 // _render_kernels.py:719-736 _pt_stage_coord
 __device__ void pt_stage_coord(const RmScene &S, const PtState &P, float &x, float &y, float &z) {
     const float one_below = __int_as_float(0x3f7fffff);
-    const double h[3] = {S.hx, S.hy, S.hz};
+    const double h[3] = {S.hx, S.hy, S.hz}, ih[3] = {S.ihx, S.ihy, S.ihz};
     float v[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        float c = (float)(((double)P.o[a] + P.t * (double)P.d[a]) / h[a]);
+        float c = (float)div_h((double)P.o[a] + P.t * (double)P.d[a], h[a], ih[a]);
         if (c < 0.0f) c = 0.0f;
         if (c >= 1.0f) c = one_below;
         v[a] = c;
@@ -981,14 +1075,16 @@ static void fill_cam(CamParams &C, const double *cp) {
     C.nrows = (int64_t)cp[17];
 }
 
+constexpr int RM_HIST_CAP = 1 << 16;  // wavefront iterations recorded on the device per frame
+
 struct RenderWs {
-    RayState *rays[2];
+    RayState *rays;            // the hit rays, in pixel order (fixed for the frame)
+    int32_t *ids[2];           // alive ray indices (ping-pong), then hit pixel ids at setup
     uint8_t *flags;
     float *sxyz, *sts, *ssbar, *values, *dxyz, *dvals;
-    int32_t *counts, *offs, *dtotal;
-    uint8_t *mdone;
+    int32_t *counts, *offs, *dtotal, *coord_rays, *coord_hist;
     unsigned long long *evals;
-    int64_t *nsel;
+    int64_t *nsel, *nact;
     void *cub_tmp;
     size_t cub_bytes;
     int64_t total;
@@ -1005,8 +1101,9 @@ static RenderWs carve(void *base, int64_t npix, int k) {
         off += al256(bytes);
         return r;
     };
-    w.rays[0] = (RayState *)take(npix * (int64_t)sizeof(RayState));
-    w.rays[1] = (RayState *)take(npix * (int64_t)sizeof(RayState));
+    w.rays = (RayState *)take(npix * (int64_t)sizeof(RayState));
+    w.ids[0] = (int32_t *)take(npix * 4);
+    w.ids[1] = (int32_t *)take(npix * 4);
     w.flags = (uint8_t *)take(npix);
     w.sxyz = (float *)take(npix * k * 12);
     w.sts = (float *)take(npix * k * 4);
@@ -1017,11 +1114,13 @@ static RenderWs carve(void *base, int64_t npix, int k) {
     w.dxyz = (float *)take(npix * k * 12);
     w.dvals = (float *)take(npix * k * 4);
     w.dtotal = (int32_t *)take(8);
-    w.mdone = (uint8_t *)take(npix);
+    w.coord_rays = (int32_t *)take(8);
+    w.coord_hist = (int32_t *)take(4 * (int64_t)RM_HIST_CAP);
     w.evals = (unsigned long long *)take(8);
     w.nsel = (int64_t *)take(8);
+    w.nact = (int64_t *)take(8);
     size_t cb = 0, cs = 0;
-    cub::DeviceSelect::Flagged(nullptr, cb, (RayState *)nullptr, (uint8_t *)nullptr, (RayState *)nullptr,
+    cub::DeviceSelect::Flagged(nullptr, cb, (int32_t *)nullptr, (uint8_t *)nullptr, (int32_t *)nullptr,
                                (int64_t *)nullptr, (int64_t)npix);
     cub::DeviceScan::ExclusiveSum(nullptr, cs, (int32_t *)nullptr, (int32_t *)nullptr, (int)npix);
     cb = cb > cs ? cb : cs;
@@ -1037,7 +1136,8 @@ int field_exact_launch(const float *coords, int64_t b, const float *params, cons
                        cudaStream_t s);
 int infer_tc_launch(const float *coords, int64_t b, const float *params, const GridTables &tab, const float *wflat,
                     uint8_t *wimg, int nn, int nh, int relu_out, int decode, int64_t dx, int64_t dy, int64_t dz,
-                    int64_t z0, double lo, double scale, float *out, cudaStream_t s, bool pack);
+                    int64_t z0, double lo, double scale, float *out, cudaStream_t s, bool pack,
+                    const int32_t *b_dev = nullptr);
 int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const uint32_t *o_w, uint32_t o_wout,
                    uint8_t *image, cudaStream_t s, const uint32_t *o_wlo);
 
@@ -1188,19 +1288,25 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
         NVOL_REQUIRE(norm, "grid field without data");
     }
     cudaMemsetAsync(w.evals, 0, 8, s);
-    raygen_kernel<<<grid_for(npix, 256), 256, 0, s>>>(C, S, w.rays[0], w.flags, img);
-    st = check_launch("raygen");
+    ray_hits_kernel<<<grid_for(npix, 256), 256, 0, s>>>(C, S, w.flags, img);
+    iota_kernel<<<grid_for(npix, 256), 256, 0, s>>>(w.ids[0], npix);
+    st = check_launch("ray_hits");
     if (st) return st;
-    cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, w.rays[0], w.flags, w.rays[1], w.nsel, npix, s);
+    cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, w.ids[0], w.flags, w.ids[1], w.nsel, npix, s);
     int64_t n = 0;
     cudaMemcpyAsync(&n, w.nsel, 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    int cur = 1, iters = 0;
+    if (n > 0) {
+        raygen_kernel<<<(unsigned)((n + RG_THREADS - 1) / RG_THREADS), RG_THREADS, 0, s>>>(C, S, w.ids[1], n, w.rays);
+        st = check_launch("raygen");
+        if (st) return st;
+    }
+    int iters = 0;
     if (S.pathtrace) {
         unsigned long long *viol = nullptr;
         if (cudaMallocAsync((void **)&viol, 8, s) != cudaSuccess) return check_launch("pathtrace alloc");
         cudaMemsetAsync(viol, 0, 8, s);
-        st = render_pathtrace(S, w, w.rays[cur], n, mu, F, tab, sh, maxw, widths, n_layers, relu_out, architecture,
+        st = render_pathtrace(S, w, w.rays, n, mu, F, tab, sh, maxw, widths, n_layers, relu_out, architecture,
                               eval_mode, mlp_image, img, alive_hist, max_hist, viol, iters, s);
         if (st) return st;
         unsigned long long ev = 0, vi = 0;
@@ -1226,7 +1332,7 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
 #define LAUNCH_MK(NNV)                                                                                            \
     do {                                                                                                          \
         cudaFuncSetAttribute(rm_mega_kernel<NNV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-        rm_mega_kernel<NNV><<<grid, FE_THREADS, smem, s>>>(w.rays[cur], n, S, mu, F, tab, sh, maxw, img, w.evals); \
+        rm_mega_kernel<NNV><<<grid, FE_THREADS, smem, s>>>(w.rays, n, S, mu, F, tab, sh, maxw, img, w.evals); \
     } while (0)
             if (uniform && nn == 16)
                 LAUNCH_MK(16);
@@ -1243,21 +1349,94 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
         if (max_hist > 0) alive_hist[0] = (int32_t)n;
         iters = 1;
     } else {
-        while (n > 0) {
-            if (iters < max_hist) alive_hist[iters] = (int32_t)n;
-            ++iters;
-            RayState *rs = w.rays[cur];
-            rm_coord_kernel<<<grid_for(n, 128), 128, 0, s>>>(rs, n, S, mu, w.sxyz, w.sts, w.ssbar, w.counts, w.mdone,
-                                                              w.evals);
-            st = check_launch("rm_coord");
-            if (st) return st;
-            // dense evaluation of the staged samples (holes dropped)
-            cub::DeviceScan::ExclusiveSum(w.cub_tmp, w.cub_bytes, w.counts, w.offs, (int)n, s);
-            compact_staged_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.sxyz, w.counts, w.offs, n, K, w.dxyz, w.dtotal);
-            int32_t ns32 = 0;
-            cudaMemcpyAsync(&ns32, w.dtotal, 4, cudaMemcpyDeviceToHost, s);
+        // alive rays: initially every hit ray (ids = 0..n-1)
+        iota_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.ids[0], n);
+        if (eval_mode == 1 && !use_grid && n > 0) {
+            // Host-sync-free schedule (tcgen05 evaluator): every stage reads its live
+            // count from the device (alive rays: nact, staged samples: dtotal) and is
+            // launched on an upper bound, so iterations queue back to back; the host
+            // only reads each iteration's alive count one iteration late, to tighten
+            // the bound and to stop.  Per-iteration marcher counts land in coord_hist.
+            static int64_t *h_cnt = nullptr;
+            static cudaEvent_t ev_cnt[2];
+            if (!h_cnt) {
+                if (cudaHostAlloc((void **)&h_cnt, 2 * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
+                    return check_launch("render pinned counters");
+                cudaEventCreateWithFlags(&ev_cnt[0], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&ev_cnt[1], cudaEventDisableTiming);
+            }
+            set_count_kernel<<<1, 1, 0, s>>>(w.nact, n);
+            cudaMemsetAsync(w.coord_hist, 0, 4 * (size_t)RM_HIST_CAP, s);
+            int64_t bound = n;
+            int cur = 0, it = 0;
+            for (;;) {
+                const int slot = it < RM_HIST_CAP ? it : RM_HIST_CAP - 1;
+                rm_step_kernel<<<grid_for(bound, 128), 128, 0, s>>>(w.ids[cur], bound, w.nact, w.rays, S, mu,
+                                                                     it > 0 ? 1 : 0, w.values, w.sxyz, w.sts, w.ssbar,
+                                                                     w.counts, w.flags, img, w.evals,
+                                                                     w.coord_hist + slot);
+                cub::DeviceScan::ExclusiveSum(w.cub_tmp, w.cub_bytes, w.counts, w.offs, (int)bound, s);
+                compact_ids_kernel<<<grid_for(bound, 256), 256, 0, s>>>(w.sxyz, w.ids[cur], w.counts, w.offs, bound,
+                                                                         K, w.dxyz, w.dtotal);
+                cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, w.ids[cur], w.flags, w.ids[cur ^ 1], w.nact,
+                                           bound, s);
+                st = infer_tc_launch(w.dxyz, bound * K, params, tab, weights, (uint8_t *)mlp_image, widths[1],
+                                     n_layers - 1, relu_out, 0, 0, 0, 0, 0, 0.0, 1.0, w.dvals, s, it == 0, w.dtotal);
+                if (st) return st;
+                scatter_ids_kernel<<<grid_for(bound, 256), 256, 0, s>>>(w.dvals, w.ids[cur], w.counts, w.offs, bound,
+                                                                         K, w.values);
+                st = check_launch("render iteration");
+                if (st) return st;
+                cudaMemcpyAsync(&h_cnt[it & 1], w.nact, 8, cudaMemcpyDeviceToHost, s);
+                cudaEventRecord(ev_cnt[it & 1], s);
+                if (it >= 1) {
+                    cudaEventSynchronize(ev_cnt[(it - 1) & 1]);
+                    const int64_t alive = h_cnt[(it - 1) & 1];  // rays entering iteration `it`
+                    if (alive == 0) break;                      // iteration `it` had nothing to do
+                    bound = alive;                              // bounds every later iteration
+                }
+                cur ^= 1;
+                ++it;
+            }
+            const int nh = (it + 1) < RM_HIST_CAP ? it + 1 : RM_HIST_CAP;
+            int32_t *hist = (int32_t *)malloc(4 * (size_t)nh);
+            cudaMemcpyAsync(hist, w.coord_hist, 4 * (size_t)nh, cudaMemcpyDeviceToHost, s);
             cudaStreamSynchronize(s);
-            const int64_t ns = ns32;
+            for (int i = 0; i < nh && hist[i] > 0; ++i) {
+                if (iters < max_hist) alive_hist[iters] = hist[i];
+                ++iters;
+            }
+            free(hist);
+            n = 0;
+        }
+
+        int cur = 0;
+        bool shade = false;
+        while (n > 0) {
+            // shade the previous iteration's samples, stage this iteration's (one ray record pass)
+            cudaMemsetAsync(w.coord_rays, 0, 4, s);
+            rm_step_kernel<<<grid_for(n, 128), 128, 0, s>>>(w.ids[cur], n, nullptr, w.rays, S, mu, shade ? 1 : 0, w.values,
+                                                             w.sxyz, w.sts, w.ssbar, w.counts, w.flags, img, w.evals,
+                                                             w.coord_rays);
+            st = check_launch("rm_step");
+            if (st) return st;
+            shade = true;
+            // dense evaluation of the staged samples + the next alive list, one host sync
+            cub::DeviceScan::ExclusiveSum(w.cub_tmp, w.cub_bytes, w.counts, w.offs, (int)n, s);
+            compact_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.sxyz, w.ids[cur], w.counts, w.offs, n, K, w.dxyz,
+                                                                 w.dtotal);
+            cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, w.ids[cur], w.flags, w.ids[cur ^ 1], w.nsel, n, s);
+            int32_t hv[2] = {0, 0};
+            int64_t nn_next = 0;
+            cudaMemcpyAsync(&hv[0], w.dtotal, 4, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(&hv[1], w.coord_rays, 4, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(&nn_next, w.nsel, 8, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            const int64_t ns = hv[0];
+            if (hv[1] > 0) {
+                if (iters < max_hist) alive_hist[iters] = hv[1];
+                ++iters;
+            }
             if (ns > 0) {
                 if (use_grid) {
                     extern int nvol_trilinear(const float *, int64_t, int64_t, int64_t, const float *, int64_t, float *,
@@ -1272,15 +1451,10 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
                                             0, 0.0, 1.0, w.dvals, s);
                 }
                 if (st) return st;
-                scatter_staged_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.dvals, w.counts, w.offs, n, K, w.values);
+                scatter_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.dvals, w.ids[cur], w.counts, w.offs, n, K,
+                                                                     w.values);
             }
-            rm_shade_kernel<<<grid_for(n, 128), 128, 0, s>>>(rs, n, S, w.values, w.sts, w.ssbar, w.counts, w.mdone,
-                                                              img, w.flags);
-            st = check_launch("rm_shade");
-            if (st) return st;
-            cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, rs, w.flags, w.rays[cur ^ 1], w.nsel, n, s);
-            cudaMemcpyAsync(&n, w.nsel, 8, cudaMemcpyDeviceToHost, s);
-            cudaStreamSynchronize(s);
+            n = nn_next;
             cur ^= 1;
         }
     }

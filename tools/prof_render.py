@@ -26,7 +26,10 @@ macrocell_set_tf(grid, tf)
 cam = default_camera(DIMS, 1920, 1080)
 cfg = RenderConfig(mode="raymarch", use_macrocells=True, k_batch=8, step_size=1.0, max_step=64.0)
 mode = sys.argv[1] if len(sys.argv) > 1 else "tensor"
-for _ in range(2):
-    img, st = render_frame_device(m, tf, cam, cfg, grid, "wavefront", mode)
+img, st = render_frame_device(m, tf, cam, cfg, grid, "wavefront", mode)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()   # ncu --profile-from-start off: only this frame
+img, st = render_frame_device(m, tf, cam, cfg, grid, "wavefront", mode)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("evals", st.evals, "iters", len(st.alive_per_iteration), st.alive_per_iteration)
