@@ -79,7 +79,10 @@ __device__ __forceinline__ uint32_t slot32i(uint32_t vx, uint32_t vy, uint32_t v
     return (vx ^ (vy * 2654435761u) ^ (vz * 805459861u)) & mask;
 }
 
-template <int NF>
+// PAIR: fetch x-adjacent corner pairs with one 16-byte load where the slots allow
+// (arbitrary sample positions: render / field evaluation).  Voxel-centre decodes
+// skip most corners by zero weight instead, where the pair logic only costs issue slots.
+template <int NF, bool PAIR>
 __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
     const float *__restrict__ coords, int64_t b, const float *__restrict__ params, const GridTables tab,
     const InferShape sh, const uint8_t *__restrict__ wimg, int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
@@ -155,19 +158,50 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
                     // (bit-exact for finite tables).  Voxel-centre decodes hit this
                     // on every level finer than the output grid (fx = fy = fz = 0).
                     const bool zx = c.fx == 0.0f, zy = c.fy == 0.0f, zz = c.fz == 0.0f;
+                    if constexpr (NF == 2 && PAIR) {
+                        // x-adjacent corners (k, k+1) whose slots are an aligned pair {lo, lo+1}
+                        // (dense levels, and hashed levels at even x: the hash differs in bit 0)
+                        // share one 16-byte load; the pair is aligned iff address(entry 0) / 8 + lo is even
+                        const uint32_t par = (uint32_t)((reinterpret_cast<uintptr_t>(tb) >> 3) & 1u);
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const bool skip = ((k & 1) && zx) || ((k & 2) && zy) || ((k & 4) && zz);
-                        const uint32_t sl =
-                            slot32i(cx + (k & 1), cy + ((k >> 1) & 1), cz + ((k >> 2) & 1), r1, mask, dense);
-                        if constexpr (NF == 2) {
-                            const float2 v = skip ? make_float2(0.0f, 0.0f)
-                                                  : __ldg(reinterpret_cast<const float2 *>(tb) + sl);
-                            vals[u][k][0] = v.x;
-                            vals[u][k][1] = v.y;
-                        } else {
+                        for (int k = 0; k < 8; k += 2) {
+                            const bool s0 = ((k & 2) && zy) || ((k & 4) && zz), s1 = s0 || zx;
+                            const uint32_t sa = slot32i(cx, cy + ((k >> 1) & 1), cz + ((k >> 2) & 1), r1, mask, dense);
+                            const uint32_t sb =
+                                slot32i(cx + 1, cy + ((k >> 1) & 1), cz + ((k >> 2) & 1), r1, mask, dense);
+                            const uint32_t lo = min(sa, sb);
+                            // branch-free (predicated loads): every gather of the level batch stays in flight
+                            const bool pair = !s1 && max(sa, sb) == lo + 1 && ((lo + par) & 1u) == 0u;
+                            const float2 z2 = make_float2(0.0f, 0.0f);
+                            const float4 q = pair ? __ldg(reinterpret_cast<const float4 *>(tb + 2 * (size_t)lo))
+                                                  : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                            const float2 a2 = (!pair && !s0) ? __ldg(reinterpret_cast<const float2 *>(tb) + sa) : z2;
+                            const float2 b2 = (!pair && !s1) ? __ldg(reinterpret_cast<const float2 *>(tb) + sb) : z2;
+                            const bool a_first = sa == lo;
+                            const float2 qa = a_first ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
+                            const float2 qb = a_first ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
+                            const float2 va = pair ? qa : a2, vb = pair ? qb : b2;
+                            vals[u][k][0] = va.x;
+                            vals[u][k][1] = va.y;
+                            vals[u][k + 1][0] = vb.x;
+                            vals[u][k + 1][1] = vb.y;
+                        }
+                    } else {
 #pragma unroll
-                            for (int f = 0; f < NF; ++f) vals[u][k][f] = skip ? 0.0f : __ldg(tb + (size_t)sl * NF + f);
+                        for (int k = 0; k < 8; ++k) {
+                            const bool skip = ((k & 1) && zx) || ((k & 2) && zy) || ((k & 4) && zz);
+                            const uint32_t sl =
+                                slot32i(cx + (k & 1), cy + ((k >> 1) & 1), cz + ((k >> 2) & 1), r1, mask, dense);
+                            if constexpr (NF == 2) {
+                                const float2 v = skip ? make_float2(0.0f, 0.0f)
+                                                      : __ldg(reinterpret_cast<const float2 *>(tb) + sl);
+                                vals[u][k][0] = v.x;
+                                vals[u][k][1] = v.y;
+                            } else {
+#pragma unroll
+                                for (int f = 0; f < NF; ++f)
+                                    vals[u][k][f] = skip ? 0.0f : __ldg(tb + (size_t)sl * NF + f);
+                            }
                         }
                     }
                 }
@@ -284,18 +318,16 @@ int infer_tc_launch(const float *coords, int64_t b, const float *params, const G
     int64_t cap = (int64_t)sms * 2;
     int grid = (int)(ntiles < cap ? ntiles : cap);
     if (grid < 1) return NVOL_OK;
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes);
+        kern<<<grid, IT_THREADS, sh.smem_bytes, s>>>(coords, b, params, tab, sh, wimg, decode, dx, dy, dz, z0, lo,
+                                                     scale, out, b_dev);
+    };
     switch (tab.n_feat) {
-#define LAUNCH_IT(NFV)                                                                                         \
-    case NFV:                                                                                                  \
-        cudaFuncSetAttribute(infer_tc_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes); \
-        infer_tc_kernel<NFV><<<grid, IT_THREADS, sh.smem_bytes, s>>>(coords, b, params, tab, sh, wimg, decode, dx, dy, \
-                                                                    dz, z0, lo, scale, out, b_dev);            \
-        break;
-        LAUNCH_IT(1)
-        LAUNCH_IT(2)
-        LAUNCH_IT(4)
-        LAUNCH_IT(8)
-#undef LAUNCH_IT
+        case 1: decode ? go(infer_tc_kernel<1, false>) : go(infer_tc_kernel<1, true>); break;
+        case 2: decode ? go(infer_tc_kernel<2, false>) : go(infer_tc_kernel<2, true>); break;
+        case 4: decode ? go(infer_tc_kernel<4, false>) : go(infer_tc_kernel<4, true>); break;
+        default: decode ? go(infer_tc_kernel<8, false>) : go(infer_tc_kernel<8, true>); break;
     }
     return check_launch("infer_tc_kernel");
 }
