@@ -95,7 +95,10 @@ int field_exact_launch(const float *coords, int64_t b, const float *params, cons
     int nn = n_layers >= 2 ? widths[1] : 0;
     bool uniform = n_layers >= 2;
     for (int i = 1; i < n_layers; ++i) uniform &= widths[i] == nn;
-    size_t smem = sizeof(float) * (((wtotal + 3) & ~3) + 2 * (size_t)maxw * FE_THREADS);
+    // the register path (uniform NN) keeps only the feature columns in shared memory: 3 CTAs / SM at cfg2
+    // instead of 1 with the generic path's two maxw-wide ping-pong columns
+    const bool regpath = uniform && (nn == 16 || nn == 32 || nn == 64);
+    size_t smem = sizeof(float) * (((wtotal + 3) & ~3) + (regpath ? (size_t)widths[0] : 2 * (size_t)maxw) * FE_THREADS);
     NVOL_REQUIRE(smem <= 220 * 1024, "MLP too large for the exact evaluator");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

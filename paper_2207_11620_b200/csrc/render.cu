@@ -1173,10 +1173,12 @@ static int render_pathtrace(const RmScene &S, const RenderWs &w, RayState *hits,
     if (st == NVOL_OK && architecture == 1) {
         int wtot = 0;
         for (int i = 0; i < (F.use_grid ? 0 : n_layers); ++i) wtot += widths[i] * widths[i + 1];
-        size_t smem = sizeof(float) * (((wtot + 3) & ~3) + 2 * (size_t)maxw * FE_THREADS);
         int nn = (!F.use_grid && n_layers >= 2) ? widths[1] : 0;
         bool uniform = !F.use_grid && n_layers >= 2;
         for (int i = 1; i < n_layers && uniform; ++i) uniform &= widths[i] == nn;
+        const bool regpath = uniform && (nn == 16 || nn == 32 || nn == 64);  // feature columns only
+        size_t smem = sizeof(float) * (((wtot + 3) & ~3) +
+                                       (regpath ? (size_t)widths[0] : 2 * (size_t)maxw) * FE_THREADS);
         unsigned grid = grid_for(n, FE_THREADS);
 #define LAUNCH_PT(NNV)                                                                                        \
     do {                                                                                                      \
@@ -1324,10 +1326,12 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
         if (n > 0) {
             int wtot = 0;
             for (int i = 0; i < (use_grid ? 0 : n_layers); ++i) wtot += widths[i] * widths[i + 1];
-            size_t smem = sizeof(float) * (((wtot + 3) & ~3) + 2 * (size_t)maxw * FE_THREADS);
             int nn = (!use_grid && n_layers >= 2) ? widths[1] : 0;
             bool uniform = !use_grid && n_layers >= 2;
             for (int i = 1; i < n_layers && uniform; ++i) uniform &= widths[i] == nn;
+            const bool regpath = uniform && (nn == 16 || nn == 32 || nn == 64);  // feature columns only
+            size_t smem = sizeof(float) * (((wtot + 3) & ~3) +
+                                           (regpath ? (size_t)widths[0] : 2 * (size_t)maxw) * FE_THREADS);
             unsigned grid = grid_for(n, FE_THREADS);
 #define LAUNCH_MK(NNV)                                                                                            \
     do {                                                                                                          \
