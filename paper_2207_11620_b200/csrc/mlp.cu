@@ -266,6 +266,40 @@ __global__ void __launch_bounds__(256) adam_flat_kernel(
     if (nan_flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan_flag, 1u);
 }
 
+// Float32 Adam with host scalars (nvol_adam_step on float buffers that share
+// their 16-byte alignment, e.g. the flat model buffers): adam_flat_kernel's
+// float4 streaming without the device schedule table.
+__global__ void __launch_bounds__(256) adam_vec_kernel(float *__restrict__ p, float *__restrict__ g,
+                                                       float *__restrict__ m, float *__restrict__ v, int64_t n,
+                                                       float lr, float b1, float omb1, float b2, float omb2,
+                                                       float c1, float c2, float eps, float l2) {
+    const int64_t head = min(n, (int64_t)(((128 - (reinterpret_cast<uintptr_t>(p) & 127)) & 127) >> 2));
+    const int64_t n4 = (n - head) >> 2;
+    float4 *p4 = reinterpret_cast<float4 *>(p + head), *g4 = reinterpret_cast<float4 *>(g + head);
+    float4 *m4 = reinterpret_cast<float4 *>(m + head), *v4 = reinterpret_cast<float4 *>(v + head);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += stride) {
+        float4 P = __ldcs(p4 + j), G = __ldcs(g4 + j), M = __ldcs(m4 + j), V = __ldcs(v4 + j);
+        adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        __stcs(p4 + j, P);
+        __stcs(g4 + j, G);
+        __stcs(m4 + j, M);
+        __stcs(v4 + j, V);
+    }
+    for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < head + (n - head - 4 * n4); jj += stride) {
+        const int64_t q = jj < head ? jj : head + 4 * n4 + (jj - head);  // head then tail elements
+        float P = p[q], G = g[q], M = m[q], V = v[q];
+        adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        p[q] = P;
+        g[q] = G;
+        m[q] = M;
+        v[q] = V;
+    }
+}
+
 // Training-pipeline Adam step: adam_flat_kernel's update plus the step's bookkeeping in the last block to
 // finish (ticket): losses[t - t0] = loss_sum / B, loss_sum = 0, t += 1.  Every
 // block reads t before taking its ticket, so the advance cannot race a reader.
@@ -440,7 +474,14 @@ int nvol_adam_step(void *p, void *g, void *m, void *v, int64_t n, double lr, dou
     if (n == 0) return NVOL_OK;
     NVOL_REQUIRE(p && g && m && v, "null pointer");
     cudaStream_t s = as_stream(stream);
-    if (dtype_bytes == 4)
+    const uintptr_t al = (uintptr_t)p & 15;
+    if (dtype_bytes == 4 && n >= 1024 && al == ((uintptr_t)g & 15) && al == ((uintptr_t)m & 15) &&
+        al == ((uintptr_t)v & 15) && (al & 3) == 0)
+        adam_vec_kernel<<<stream_grid((n + 3) / 4), 256, 0, s>>>((float *)p, (float *)g, (float *)m, (float *)v, n,
+                                                                  (float)lr, (float)beta1, (float)one_minus_beta1,
+                                                                  (float)beta2, (float)one_minus_beta2, (float)c1,
+                                                                  (float)c2, (float)eps, (float)l2);
+    else if (dtype_bytes == 4)
         adam_kernel<float><<<stream_grid(n), 256, 0, s>>>((float *)p, (float *)g, (float *)m, (float *)v, n,
                                                           (float)lr, (float)beta1, (float)one_minus_beta1,
                                                           (float)beta2, (float)one_minus_beta2, (float)c1,
