@@ -293,6 +293,15 @@ def run_ours(args):
         roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tc_sus, "unit": "TFLOP/s",
                 "frac": ach / tc_sus, "traffic": None, "algorithmic_flops_per_launch": mlp_flops,
                 "launch_ms": kernels[dom], "peak_source": peak_kind}
+    # DRAM traffic of the dominant kernel per launch, from the committed ncu --set full capture
+    # (profiles/ncu_traffic.json, written from profiles/<round>_ncu_summary.md)
+    try:
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
+        if dom in tr:
+            roof["traffic"] = tr[dom]["traffic_bytes"]
+            roof["traffic_source"] = tr["_source"]
+    except (OSError, ValueError, KeyError):
+        pass
     step_bytes = adam_bytes + 3 * gather_bytes + B * 64
     roof["step_algorithmic_bytes"] = step_bytes
     roof["step_frac_of_hbm"] = step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm

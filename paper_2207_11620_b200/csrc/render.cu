@@ -1361,14 +1361,24 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
             // launched on an upper bound, so iterations queue back to back; the host
             // only reads each iteration's alive count one iteration late, to tighten
             // the bound and to stop.  Per-iteration marcher counts land in coord_hist.
-            static int64_t *h_cnt = nullptr;
-            static cudaEvent_t ev_cnt[2];
-            if (!h_cnt) {
-                if (cudaHostAlloc((void **)&h_cnt, 2 * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
+            // pinned read-back slots + events, per host thread and device (events belong to a device)
+            struct CountSlots {
+                int64_t *h = nullptr;
+                cudaEvent_t ev[2];
+            };
+            static thread_local CountSlots slots[64];
+            int dev = 0;
+            cudaGetDevice(&dev);
+            NVOL_REQUIRE(dev >= 0 && dev < 64, "device index out of range");
+            CountSlots &cs = slots[dev];
+            if (!cs.h) {
+                if (cudaHostAlloc((void **)&cs.h, 2 * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess)
                     return check_launch("render pinned counters");
-                cudaEventCreateWithFlags(&ev_cnt[0], cudaEventDisableTiming);
-                cudaEventCreateWithFlags(&ev_cnt[1], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&cs.ev[0], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&cs.ev[1], cudaEventDisableTiming);
             }
+            int64_t *h_cnt = cs.h;
+            cudaEvent_t *ev_cnt = cs.ev;
             set_count_kernel<<<1, 1, 0, s>>>(w.nact, n);
             cudaMemsetAsync(w.coord_hist, 0, 4 * (size_t)RM_HIST_CAP, s);
             int64_t bound = n;
