@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "field_exact.cuh"
@@ -1355,7 +1356,12 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
     } else {
         // alive rays: initially every hit ray (ids = 0..n-1)
         iota_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.ids[0], n);
-        if (eval_mode == 1 && !use_grid && n > 0) {
+        static int force_sync = -1;  // NVOL_RENDER_SYNC=1: the synchronous loop below (A/B, tests)
+        if (force_sync < 0) {
+            const char *e = getenv("NVOL_RENDER_SYNC");
+            force_sync = (e && atoi(e) != 0) ? 1 : 0;
+        }
+        if (eval_mode == 1 && !use_grid && n > 0 && !force_sync) {
             // Host-sync-free schedule (tcgen05 evaluator): every stage reads its live
             // count from the device (alive rays: nact, staged samples: dtotal) and is
             // launched on an upper bound, so iterations queue back to back; the host

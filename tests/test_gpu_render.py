@@ -136,6 +136,59 @@ def test_tensor_core_batched_inference_render(scene):
     assert img_psnr(img, z["img_rm_mc"]) >= 35.0
 
 
+def test_tensor_wavefront_schedule_is_scheduling_only(scene):
+    """The host-sync-free tensor wavefront (device counts, one-iteration-late bounds) gives
+    the same image, evaluation count and per-iteration alive counts as the synchronous
+    loop, bitwise, and K batching changes nothing in the image."""
+    import ast
+    import subprocess
+    import sys
+    from paper_2207_11620_b200.camera import default_camera
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    cam = default_camera(dims, 320, 180)
+    model.infer_mode = "tensor"
+    try:
+        runs = {}
+        for k in (1, 3, 8):
+            st = []
+            img = render(model, tf, cam, RenderConfig(mode="raymarch", use_macrocells=True, k_batch=k), "wavefront",
+                         grid=grid, stats_out=st)
+            runs[k] = (img, st[0])
+    finally:
+        model.infer_mode = "exact"
+    for k in (3, 8):   # (evaluation counts do depend on K: samples staged past termination are evaluated)
+        np.testing.assert_array_equal(runs[k][0], runs[1][0])
+    # the synchronous loop (NVOL_RENDER_SYNC=1 is read once per process: run it in a child)
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, 'tests'); from conftest import golden, golden_config\n"
+        "from paper_2207_11620_b200 import macrocell\n"
+        "from paper_2207_11620_b200.camera import default_camera\n"
+        "from paper_2207_11620_b200.model import build_model\n"
+        "from paper_2207_11620_b200.render import RenderConfig, render\n"
+        "from paper_2207_11620_b200.transfer import default_tf\n"
+        "z = golden('render_small.npz'); dims = tuple(int(x) for x in z['dims'])\n"
+        "m = build_model(golden_config(z), dims=dims, seed=0); m.load_blob(z['blob'])\n"
+        "g = macrocell.macrocell_from_model(m, n_g=8); tf = default_tf(); macrocell.macrocell_set_tf(g, tf)\n"
+        "m.infer_mode = 'tensor'; st = []\n"
+        "img = render(m, tf, default_camera(dims, 320, 180), RenderConfig(mode='raymarch', use_macrocells=True),"
+        " 'wavefront', grid=g, stats_out=st)\n"
+        "np.save(sys.argv[1], img); print(st[0].evals, list(st[0].alive_per_iteration))\n")
+    import os
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "img.npy")
+        env = dict(os.environ, NVOL_RENDER_SYNC="1")
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", code, out], env=env, cwd=root, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        ev, hist = r.stdout.strip().splitlines()[-1].split(" ", 1)
+        np.testing.assert_array_equal(np.load(out), runs[8][0])
+        assert int(ev) == runs[8][1].evals
+        assert ast.literal_eval(hist) == list(runs[8][1].alive_per_iteration)
+
+
 def test_online_macrocells_inside_precomputed(nv):
     # test_macrocell.py:116-139: streamed ranges never exceed the bordered precomputed ones
     from paper_2207_11620_b200 import fields, macrocell
