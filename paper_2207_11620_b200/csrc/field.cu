@@ -75,6 +75,93 @@ __global__ void __launch_bounds__(FE_THREADS) field_exact_kernel(
     }
 }
 
+// Uniform hidden width NN: the activations of each thread live in its own
+// shared-memory column (h[k] at col[k * FE_THREADS]) and the k-major weights are
+// read through L1 (one broadcast float4 per 4 outputs), so the k loop stays
+// rolled: a fully unrolled 64 x 64 layer is ~150 KB of SASS and the warps
+// starved on instruction fetch.  Same folds in the same order (acc[j] over k,
+// xmul then xadd) as mlp_exact_reg: bit-identical.
+template <int NN>
+__device__ __forceinline__ float mlp_exact_col(float *col, int nin, const float *__restrict__ wt, const MlpShape &sh) {
+    const int nl = sh.n_layers;
+    for (int li = 0; li < nl - 1; ++li) {
+        const int win = li == 0 ? nin : NN;
+        float acc[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) acc[j] = 0.0f;
+#pragma unroll 2
+        for (int k = 0; k < win; ++k) {
+            const float hk = col[k * FE_THREADS];
+            const float4 *wr = reinterpret_cast<const float4 *>(wt + k * NN);
+#pragma unroll
+            for (int j4 = 0; j4 < NN / 4; ++j4) {
+                const float4 w = __ldg(wr + j4);
+                acc[4 * j4 + 0] = xadd(acc[4 * j4 + 0], xmul(w.x, hk));
+                acc[4 * j4 + 1] = xadd(acc[4 * j4 + 1], xmul(w.y, hk));
+                acc[4 * j4 + 2] = xadd(acc[4 * j4 + 2], xmul(w.z, hk));
+                acc[4 * j4 + 3] = xadd(acc[4 * j4 + 3], xmul(w.w, hk));
+            }
+        }
+        // every hidden layer is followed by ReLU (the output layer is separate below)
+#pragma unroll
+        for (int j = 0; j < NN; ++j) col[j * FE_THREADS] = fmaxf(acc[j], 0.0f);
+        wt += win * NN;
+    }
+    // output layer NN -> 1, one serial fold
+    float o = 0.0f;
+    for (int k = 0; k < NN; ++k) o = xadd(o, xmul(__ldg(wt + k), col[k * FE_THREADS]));
+    return sh.relu_out ? fmaxf(o, 0.0f) : o;
+}
+
+template <int NN>
+__global__ void __launch_bounds__(FE_THREADS, 4) field_exact_col_kernel(
+    const float *__restrict__ coords, int64_t b, const float *__restrict__ params, const GridTables tab,
+    const float *__restrict__ wt, const MlpShape sh, int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
+    double lo, double scale, float *__restrict__ out) {
+    extern __shared__ float4 smem4[];
+    float *col = reinterpret_cast<float *>(smem4) + threadIdx.x;
+    for (int64_t base = (int64_t)blockIdx.x * FE_THREADS; base < b; base += (int64_t)gridDim.x * FE_THREADS) {
+        const int64_t i = base + threadIdx.x;
+        if (i >= b) continue;
+        float x, y, z;
+        if (decode) {
+            int64_t ix = i % dx, iy = (i / dx) % dy, iz = z0 + i / (dx * dy);
+            if (decode == 2) {  // macrocell.py:90-94: centres in float64, then cast
+                x = (float)(((double)ix + 0.5) / (double)dx);
+                y = (float)(((double)iy + 0.5) / (double)dy);
+                z = (float)(((double)iz + 0.5) / (double)dz);
+            } else {            // trainer.py:86-92: float32 arithmetic
+                x = xdiv(xadd((float)ix, 0.5f), (float)dx);
+                y = xdiv(xadd((float)iy, 0.5f), (float)dy);
+                z = xdiv(xadd((float)iz, 0.5f), (float)dz);
+            }
+        } else {
+            x = coords[3 * i];
+            y = coords[3 * i + 1];
+            z = coords[3 * i + 2];
+        }
+        encode_exact(x, y, z, params, tab, col);
+        const float v = mlp_exact_col<NN>(col, tab.n_levels * tab.n_feat, wt, sh);
+        if (decode == 1)
+            out[i] = (float)__dadd_rn(__dmul_rn((double)v, scale), lo);
+        else
+            out[i] = v;
+    }
+}
+
+// row-major (out x in) layers -> k-major (in x out), layer by layer
+__global__ void transpose_layers_kernel(const float *__restrict__ w, const MlpShape sh, float *__restrict__ wt) {
+    int off = 0;
+    for (int li = 0; li < sh.n_layers; ++li) {
+        const int win = sh.widths[li], wout = sh.widths[li + 1];
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < win * wout; q += gridDim.x * blockDim.x) {
+            const int j = q / win, k = q % win;
+            wt[off + k * wout + j] = w[off + q];
+        }
+        off += win * wout;
+    }
+}
+
 int field_exact_launch(const float *coords, int64_t b, const float *params, const GridTables &tab,
                        const float *weights, const int32_t *widths, int32_t n_layers, int32_t relu_out,
                        int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0, double lo, double scale,
@@ -105,6 +192,24 @@ int field_exact_launch(const float *coords, int64_t b, const float *params, cons
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t blocks = (b + FE_THREADS - 1) / FE_THREADS;
     unsigned grid = (unsigned)max((int64_t)1, min(blocks, (int64_t)sms * 16));
+    if (regpath && widths[0] <= nn) {
+        // column kernel: per-thread activation columns in shared memory, k-major weights via L1
+        float *wt = nullptr;
+        if (cudaMallocAsync((void **)&wt, sizeof(float) * (size_t)wtotal, s) != cudaSuccess)
+            return check_launch("exact evaluator weights");
+        transpose_layers_kernel<<<16, 256, 0, s>>>(weights, sh, wt);
+        const size_t csm = sizeof(float) * (size_t)nn * FE_THREADS;
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 60);
+            kern<<<grid, FE_THREADS, csm, s>>>(coords, b, params, tab, wt, sh, decode, dx, dy, dz, z0, lo, scale, out);
+        };
+        if (nn == 16) go(field_exact_col_kernel<16>);
+        else if (nn == 32) go(field_exact_col_kernel<32>);
+        else go(field_exact_col_kernel<64>);
+        cudaFreeAsync(wt, s);
+        return check_launch("field_eval_exact");
+    }
 #define LAUNCH_FE(NNV)                                                                                      \
     do {                                                                                                    \
         cudaFuncSetAttribute(field_exact_kernel<NNV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
