@@ -507,6 +507,8 @@ def render_bench(torch, args, rank=0, world=1):
     m.train_mode = args.mode
     train(m, InCoreSampler(fld, seed=1), steps=args.render_train_steps)
     tf = default_tf()
+    macrocell_from_model(m, n_g=16)          # warm-up (module load, scratch)
+    torch.cuda.synchronize()
     g0 = time.perf_counter()
     grid = macrocell_from_model(m, n_g=16)
     macrocell_set_tf(grid, tf)

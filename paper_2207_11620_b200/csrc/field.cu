@@ -75,44 +75,6 @@ __global__ void __launch_bounds__(FE_THREADS) field_exact_kernel(
     }
 }
 
-// Uniform hidden width NN: the activations of each thread live in its own
-// shared-memory column (h[k] at col[k * FE_THREADS]) and the k-major weights are
-// read through L1 (one broadcast float4 per 4 outputs), so the k loop stays
-// rolled: a fully unrolled 64 x 64 layer is ~150 KB of SASS and the warps
-// starved on instruction fetch.  Same folds in the same order (acc[j] over k,
-// xmul then xadd) as mlp_exact_reg: bit-identical.
-template <int NN>
-__device__ __forceinline__ float mlp_exact_col(float *col, int nin, const float *__restrict__ wt, const MlpShape &sh) {
-    const int nl = sh.n_layers;
-    for (int li = 0; li < nl - 1; ++li) {
-        const int win = li == 0 ? nin : NN;
-        float acc[NN];
-#pragma unroll
-        for (int j = 0; j < NN; ++j) acc[j] = 0.0f;
-#pragma unroll 2
-        for (int k = 0; k < win; ++k) {
-            const float hk = col[k * FE_THREADS];
-            const float4 *wr = reinterpret_cast<const float4 *>(wt + k * NN);
-#pragma unroll
-            for (int j4 = 0; j4 < NN / 4; ++j4) {
-                const float4 w = __ldg(wr + j4);
-                acc[4 * j4 + 0] = xadd(acc[4 * j4 + 0], xmul(w.x, hk));
-                acc[4 * j4 + 1] = xadd(acc[4 * j4 + 1], xmul(w.y, hk));
-                acc[4 * j4 + 2] = xadd(acc[4 * j4 + 2], xmul(w.z, hk));
-                acc[4 * j4 + 3] = xadd(acc[4 * j4 + 3], xmul(w.w, hk));
-            }
-        }
-        // every hidden layer is followed by ReLU (the output layer is separate below)
-#pragma unroll
-        for (int j = 0; j < NN; ++j) col[j * FE_THREADS] = fmaxf(acc[j], 0.0f);
-        wt += win * NN;
-    }
-    // output layer NN -> 1, one serial fold
-    float o = 0.0f;
-    for (int k = 0; k < NN; ++k) o = xadd(o, xmul(__ldg(wt + k), col[k * FE_THREADS]));
-    return sh.relu_out ? fmaxf(o, 0.0f) : o;
-}
-
 template <int NN>
 __global__ void __launch_bounds__(FE_THREADS, 4) field_exact_col_kernel(
     const float *__restrict__ coords, int64_t b, const float *__restrict__ params, const GridTables tab,
@@ -141,7 +103,7 @@ __global__ void __launch_bounds__(FE_THREADS, 4) field_exact_col_kernel(
             z = coords[3 * i + 2];
         }
         encode_exact(x, y, z, params, tab, col);
-        const float v = mlp_exact_col<NN>(col, tab.n_levels * tab.n_feat, wt, sh);
+        const float v = mlp_exact_col<NN, true>(col, tab.n_levels * tab.n_feat, wt, sh);
         if (decode == 1)
             out[i] = (float)__dadd_rn(__dmul_rn((double)v, scale), lo);
         else
@@ -194,9 +156,28 @@ int field_exact_launch(const float *coords, int64_t b, const float *params, cons
     unsigned grid = (unsigned)max((int64_t)1, min(blocks, (int64_t)sms * 16));
     if (regpath && widths[0] <= nn) {
         // column kernel: per-thread activation columns in shared memory, k-major weights via L1
-        float *wt = nullptr;
-        if (cudaMallocAsync((void **)&wt, sizeof(float) * (size_t)wtotal, s) != cudaSuccess)
-            return check_launch("exact evaluator weights");
+        // transposed-weight scratch: grow-only, per host thread and device (a per-call
+        // stream-ordered allocation went back to the driver at every host sync of the
+        // render loop and cost milliseconds)
+        struct WtScratch {
+            float *p = nullptr;
+            size_t n = 0;
+        };
+        static thread_local WtScratch scratch[64];
+        NVOL_REQUIRE(dev >= 0 && dev < 64, "device index out of range");
+        WtScratch &ws = scratch[dev];
+        if (ws.n < (size_t)wtotal) {
+            if (ws.p) {
+                cudaStreamSynchronize(s);  // the previous scratch may still be read by queued work
+                cudaFree(ws.p);
+            }
+            ws.p = nullptr;
+            ws.n = 0;
+            if (cudaMalloc((void **)&ws.p, sizeof(float) * (size_t)wtotal) != cudaSuccess)
+                return check_launch("exact evaluator weights");
+            ws.n = (size_t)wtotal;
+        }
+        float *wt = ws.p;
         transpose_layers_kernel<<<16, 256, 0, s>>>(weights, sh, wt);
         const size_t csm = sizeof(float) * (size_t)nn * FE_THREADS;
         auto go = [&](auto kern) {
@@ -207,7 +188,6 @@ int field_exact_launch(const float *coords, int64_t b, const float *params, cons
         if (nn == 16) go(field_exact_col_kernel<16>);
         else if (nn == 32) go(field_exact_col_kernel<32>);
         else go(field_exact_col_kernel<64>);
-        cudaFreeAsync(wt, s);
         return check_launch("field_eval_exact");
     }
 #define LAUNCH_FE(NNV)                                                                                      \

@@ -97,6 +97,47 @@ __device__ __forceinline__ float mlp_exact_reg(const float *feat, int nin, const
     return sh.relu_out ? fmaxf(o, 0.0f) : o;
 }
 
+// Uniform hidden width NN: the activations of each thread live in its own
+// shared-memory column (h[k] at col[k * FE_THREADS]) and the k-major weights are
+// read as broadcast float4s (through L1 from global memory, GLOBAL_W, or from
+// shared memory), one per 4 outputs, so the k loop stays
+// rolled: a fully unrolled 64 x 64 layer is ~150 KB of SASS and the warps
+// starved on instruction fetch.  The column must hold max(nin, NN) rows.  Same folds in the same order (acc[j] over k,
+// xmul then xadd) as mlp_exact_reg: bit-identical.
+template <int NN, bool GLOBAL_W>
+__device__ __forceinline__ float mlp_exact_col(float *col, int nin, const float *__restrict__ wt, const MlpShape &sh) {
+    auto ldw4 = [](const float4 *a) { return GLOBAL_W ? __ldg(a) : *a; };
+    auto ldw = [](const float *a) { return GLOBAL_W ? __ldg(a) : *a; };
+    const int nl = sh.n_layers;
+    for (int li = 0; li < nl - 1; ++li) {
+        const int win = li == 0 ? nin : NN;
+        float acc[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) acc[j] = 0.0f;
+#pragma unroll 2
+        for (int k = 0; k < win; ++k) {
+            const float hk = col[k * FE_THREADS];
+            const float4 *wr = reinterpret_cast<const float4 *>(wt + k * NN);
+#pragma unroll
+            for (int j4 = 0; j4 < NN / 4; ++j4) {
+                const float4 w = ldw4(wr + j4);
+                acc[4 * j4 + 0] = xadd(acc[4 * j4 + 0], xmul(w.x, hk));
+                acc[4 * j4 + 1] = xadd(acc[4 * j4 + 1], xmul(w.y, hk));
+                acc[4 * j4 + 2] = xadd(acc[4 * j4 + 2], xmul(w.z, hk));
+                acc[4 * j4 + 3] = xadd(acc[4 * j4 + 3], xmul(w.w, hk));
+            }
+        }
+        // every hidden layer is followed by ReLU (the output layer is separate below)
+#pragma unroll
+        for (int j = 0; j < NN; ++j) col[j * FE_THREADS] = fmaxf(acc[j], 0.0f);
+        wt += win * NN;
+    }
+    // output layer NN -> 1, one serial fold
+    float o = 0.0f;
+    for (int k = 0; k < NN; ++k) o = xadd(o, xmul(ldw(wt + k), col[k * FE_THREADS]));
+    return sh.relu_out ? fmaxf(o, 0.0f) : o;
+}
+
 // Generic widths: activations ping-pong through this thread's smem columns.
 __device__ __forceinline__ float mlp_exact_smem(float *h0, float *h1, const float *__restrict__ wt, const MlpShape &sh) {
     float *cur = h0, *nxt = h1;

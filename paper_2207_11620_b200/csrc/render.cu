@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(FE_THREADS) rm_mega_kernel(RayState *__restric
         } else {
             encode_exact(x, y, z, F.params, tab, col0);
             if constexpr (NN > 0)
-                v = mlp_exact_reg<NN>(col0, tab.n_levels * tab.n_feat, wt, sh);
+                v = mlp_exact_col<NN, false>(col0, tab.n_levels * tab.n_feat, wt, sh);
             else
                 v = mlp_exact_smem(col0, col1, wt, sh);
         }
@@ -1049,7 +1049,7 @@ __global__ void __launch_bounds__(FE_THREADS) pt_mega_kernel(PtState *__restrict
         } else {
             encode_exact(x, y, z, F.params, tab, col0);
             if constexpr (NN > 0)
-                v = mlp_exact_reg<NN>(col0, tab.n_levels * tab.n_feat, wt, sh);
+                v = mlp_exact_col<NN, false>(col0, tab.n_levels * tab.n_feat, wt, sh);
             else
                 v = mlp_exact_smem(col0, col1, wt, sh);
         }
@@ -1177,9 +1177,9 @@ static int render_pathtrace(const RmScene &S, const RenderWs &w, RayState *hits,
         int nn = (!F.use_grid && n_layers >= 2) ? widths[1] : 0;
         bool uniform = !F.use_grid && n_layers >= 2;
         for (int i = 1; i < n_layers && uniform; ++i) uniform &= widths[i] == nn;
-        const bool regpath = uniform && (nn == 16 || nn == 32 || nn == 64);  // feature columns only
+        const bool regpath = uniform && (nn == 16 || nn == 32 || nn == 64);  // one activation column
         size_t smem = sizeof(float) * (((wtot + 3) & ~3) +
-                                       (regpath ? (size_t)widths[0] : 2 * (size_t)maxw) * FE_THREADS);
+                                       (regpath ? (size_t)max((int)widths[0], nn) : 2 * (size_t)maxw) * FE_THREADS);
         unsigned grid = grid_for(n, FE_THREADS);
 #define LAUNCH_PT(NNV)                                                                                        \
     do {                                                                                                      \
@@ -1330,9 +1330,9 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
             int nn = (!use_grid && n_layers >= 2) ? widths[1] : 0;
             bool uniform = !use_grid && n_layers >= 2;
             for (int i = 1; i < n_layers && uniform; ++i) uniform &= widths[i] == nn;
-            const bool regpath = uniform && (nn == 16 || nn == 32 || nn == 64);  // feature columns only
+            const bool regpath = uniform && (nn == 16 || nn == 32 || nn == 64);  // one activation column
             size_t smem = sizeof(float) * (((wtot + 3) & ~3) +
-                                           (regpath ? (size_t)widths[0] : 2 * (size_t)maxw) * FE_THREADS);
+                                           (regpath ? (size_t)max((int)widths[0], nn) : 2 * (size_t)maxw) * FE_THREADS);
             unsigned grid = grid_for(n, FE_THREADS);
 #define LAUNCH_MK(NNV)                                                                                            \
     do {                                                                                                          \
