@@ -1,16 +1,20 @@
-"""Data-parallel training: sample sharding + one gradient all-reduce per step.
+"""Data-parallel training: sample sharding + the gradient exchange.
 
 The reference is single-process; the north star adds data
 parallelism by sample sharding.  Rank r of G processes the rows
 [r*B/G, (r+1)*B/G) of the reference's global batch — the PCG64 stream
 offset of those rows is computed exactly, so the union of the shards IS the
 single-process batch — scales its loss gradient by 1/B_global
-(network.py:108), and all-reduces (sum) the flat gradient buffer plus the loss
-sum.  Every rank then applies the identical Adam update, so parameters stay
-bit-identical across ranks without a parameter broadcast.  On GPUs the
-collective is NCCL over NVLink/NVSwitch and is captured inside the step's
-CUDA graph (trainer.StepPipeline); the host logic here is device-agnostic and
-is exercised with gloo on CPU in the tests.
+(network.py:108), and sums the flat gradient buffer plus the loss sum over the
+ranks.  Two exchanges: an all-reduce followed by the identical Adam update on
+every rank (parameters stay bit-identical without a broadcast), or the sharded
+optimizer (the default on the device pipeline): a reduce-scatter gives rank r
+the summed gradient of its 1/G slice of the flat buffer, Adam updates only that
+slice (Adam time and traffic / G), and an all-gather of the updated slices
+rebuilds the parameters everywhere — the same bytes on the wire as the
+all-reduce.  On GPUs the collectives are NCCL over NVLink/NVSwitch captured
+inside the step's CUDA graph (trainer.StepPipeline); the host logic here is
+device-agnostic and is exercised with gloo on CPU in the tests.
 """
 from __future__ import annotations
 
@@ -96,6 +100,36 @@ def allreduce_grads(flat_grads: torch.Tensor, loss_acc: torch.Tensor | None = No
         dist.all_reduce(loss_acc, op=dist.ReduceOp.SUM, group=group)
 
 
+def optimizer_shard(n: int, rank: int, world: int, align: int = 32):
+    """Sharded-optimizer slice of a flat buffer of n floats: (chunk, lo, hi).
+    Rank r owns [lo, hi) = [r*chunk, min(n, (r+1)*chunk)); chunk is a multiple of
+    `align` floats (128 bytes), so every slice keeps the flat buffer's alignment
+    modulo 128 and the float4 Adam kernel applies.  A world*chunk padded buffer
+    holds the collectives' equal-sized chunks."""
+    if world < 1 or not 0 <= rank < world:
+        raise ConfigError(f"bad rank {rank} of world {world}")
+    chunk = -(-int(n) // world)
+    chunk = -(-chunk // align) * align
+    lo = rank * chunk
+    return chunk, lo, max(lo, min(int(n), lo + chunk))
+
+
+def reduce_scatter_grads(padded_grads: torch.Tensor, out: torch.Tensor, group=None) -> None:
+    """out[:chunk] = sum over ranks of padded_grads[rank*chunk:(rank+1)*chunk] (this rank's slice)."""
+    world = dist.get_world_size(group)
+    chunk = out.numel()
+    if padded_grads.numel() != world * chunk:
+        raise ConfigError("padded gradient buffer must hold world * chunk floats")
+    dist.reduce_scatter_tensor(out, padded_grads, op=dist.ReduceOp.SUM, group=group)
+
+
+def allgather_shards(padded: torch.Tensor, rank: int, group=None) -> None:
+    """In-place all-gather: every rank's chunk of `padded` (world*chunk floats) to all ranks."""
+    world = dist.get_world_size(group)
+    chunk = padded.numel() // world
+    dist.all_gather_into_tensor(padded, padded[rank * chunk:(rank + 1) * chunk], group=group)
+
+
 def init_from_env(backend: str = "nccl"):
     """torchrun-style init (RANK / WORLD_SIZE / LOCAL_RANK / MASTER_*); returns (rank, world, local_rank)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -113,11 +147,12 @@ def init_from_env(backend: str = "nccl"):
 class DataParallelTrainer:
     """Device-resident data-parallel training of one NeuralModel per rank."""
 
-    def __init__(self, model, sampler, capacity: int, group=None):
+    def __init__(self, model, sampler, capacity: int, group=None, use_graph: bool = True):
         from .trainer import StepPipeline
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.pipeline = StepPipeline(model, sampler, capacity, rank=rank, world=world, group=group)
+        self.pipeline = StepPipeline(model, sampler, capacity, rank=rank, world=world, group=group,
+                                     use_graph=use_graph)
 
     def step(self, n: int = 1) -> None:
         self.pipeline.step(n)

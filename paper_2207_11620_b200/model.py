@@ -166,6 +166,24 @@ class NeuralModel:
             pos += w.numel()
         self._bind_views()
 
+    def rehome_flat(self, capacity: int) -> None:
+        """Move the four flat buffers into allocations holding `capacity` >= flat_size
+        floats (zero padding after the model), keeping the lead pad, so collectives can
+        work on equal-sized chunks of `flat_*_padded`; re-binds every view.  Existing
+        CUDA graphs / pipelines that captured the old pointers must be rebuilt."""
+        capacity = int(capacity)
+        if capacity < self.flat_size:
+            raise ConfigError(f"capacity {capacity} < flat size {self.flat_size}")
+        lead = self.flat_lead
+        for name in ("flat_params", "flat_grads", "flat_m", "flat_v"):
+            old = getattr(self, name)
+            buf = torch.zeros(lead + capacity, dtype=old.dtype, device=old.device)[lead:]
+            buf[:self.flat_size].copy_(old)
+            setattr(self, name + "_padded", buf)
+            setattr(self, name, buf[:self.flat_size])
+        self._bind_views()
+        self._pipeline = None
+
     def _views(self, flat: torch.Tensor):
         enc = flat[:self.enc_size]
         ws, pos = [], self.w_offset

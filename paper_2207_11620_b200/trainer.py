@@ -97,7 +97,18 @@ class StepPipeline:
         self.sampler = sampler
         self.train_mode = model._engine()
         self.B, self.b, self.row0 = B, b, row0
+        self.rank = rank
         self.world, self.group = world, group
+        # sharded optimizer (distributed.py): reduce-scatter -> Adam on this rank's slice ->
+        # all-gather; NVOL_DP_SHARDED=0 restores all-reduce + replicated Adam
+        self.sharded = world > 1 and os.environ.get("NVOL_DP_SHARDED", "1") != "0"
+        if self.sharded:
+            from .distributed import optimizer_shard
+            self.chunk, self.slo, self.shi = optimizer_shard(model.flat_size, rank, world)
+            if getattr(model, "flat_params_padded", None) is None or model.flat_params_padded.numel() != world * self.chunk:
+                model.rehome_flat(world * self.chunk)
+            self.gslice = torch.zeros(model.flat_lead + self.chunk, dtype=torch.float32,
+                                      device=model.flat_params.device)[model.flat_lead:]
         dev = model.flat_params.device
         self.bufs = [(torch.empty((self.b, 3), dtype=torch.float32, device=dev),
                       torch.empty(self.b, dtype=torch.float32, device=dev)) for _ in range(2)]
@@ -222,6 +233,22 @@ class StepPipeline:
             self.sample_into(parity, 0)
         c, t = self.bufs[parity]
         m.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_PREENCODED if self.fused else 0)
+        if self.sharded:
+            import torch.distributed as dist
+            from .distributed import allgather_shards, reduce_scatter_grads
+            reduce_scatter_grads(m.flat_grads_padded, self.gslice, self.group)
+            dist.all_reduce(self.acc, group=self.group)
+            m.flat_grads_padded.zero_()                 # this rank's gradient is consumed
+            if self.overlap:
+                main.wait_stream(self.side)
+            o4 = 4 * self.slo
+            _lib.call("nvol_adam_train_step", _lib.ptr(m.flat_params) + o4, _lib.ptr(self.gslice),
+                      _lib.ptr(m.flat_m) + o4, _lib.ptr(m.flat_v) + o4, self.shi - self.slo, _lib.ptr(self.sched),
+                      self.sched.numel() // 3, _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag),
+                      _lib.ptr(self.acc), _lib.ptr(self.losses), self.t0, self.capacity, 1.0 / self.B,
+                      _lib.ptr(self.ticket), _lib.stream())
+            allgather_shards(m.flat_params_padded, self.rank, self.group)
+            return
         if self.world > 1:
             from .distributed import allreduce_grads
             allreduce_grads(m.flat_grads, self.acc, self.group)
@@ -308,6 +335,14 @@ class StepPipeline:
             losses = self.losses[:self.done].cpu().numpy()
             self.sampler.rng.u32 = self.u32_base + 3 * self.B * self.done
         self.model.opt.t = self.t0 + self.done
+        if self.sharded:
+            # every rank holds the whole optimizer state again, and any rank's NaN stops all
+            import torch.distributed as dist
+            from .distributed import allgather_shards
+            m = self.model
+            allgather_shards(m.flat_m_padded, self.rank, self.group)
+            allgather_shards(m.flat_v_padded, self.rank, self.group)
+            dist.all_reduce(self.nan_flag, op=dist.ReduceOp.MAX, group=self.group)
         if int(self.nan_flag.item()):
             raise FloatingPointError("NaN gradient encountered during device-resident training")
         return losses

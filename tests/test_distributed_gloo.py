@@ -80,6 +80,70 @@ def test_dp_gloo_matches_single_process(oracle):
     np.testing.assert_array_equal(out[0][0], out[1][0])   # identical on every rank -> identical Adam
 
 
+def _sharded_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__)))
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import nvol_oracle as orc
+    from paper_2207_11620_b200.distributed import (allgather_shards, allreduce_grads, optimizer_shard,
+                                                   reduce_scatter_grads)
+    model, flat, lsum = _shard_grads(rank, world, step=3)
+    n = flat.size
+    p0 = np.concatenate([model.params] + [w.ravel() for w in model.weights]).astype(np.float32)
+    # sharded optimizer: reduce-scatter -> Adam on this rank's slice -> all-gather
+    chunk, lo, hi = optimizer_shard(n, rank, world, align=32)
+    padded = torch.zeros(world * chunk)
+    padded[:n] = torch.from_numpy(flat)
+    gs = torch.zeros(chunk)
+    reduce_scatter_grads(padded, gs)
+    p = np.zeros(world * chunk, np.float32)
+    p[:n] = p0
+    opt = orc.AdamState()
+    ps = p[lo:hi]
+    orc.adam_step(opt, [ps], [gs.numpy()[:hi - lo].copy()])
+    pt = torch.from_numpy(p)
+    allgather_shards(pt, rank)
+    # reference exchange: all-reduce + the replicated full Adam
+    g = torch.from_numpy(flat.copy())
+    allreduce_grads(g)
+    pr = p0.copy()
+    orc.adam_step(orc.AdamState(), [pr], [g.numpy().copy()])
+    out[rank] = (pt.numpy()[:n].copy(), pr, opt.m[0].copy(), int(lo), int(hi))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_optimizer_gloo_equals_allreduce(oracle):
+    """reduce-scatter -> slice Adam -> all-gather (the device pipeline's default
+    exchange for world > 1) gives bit-identical parameters to all-reduce + the
+    replicated Adam, on every rank (2 ranks, so both exchanges add the same two
+    partial gradients; 18,492 floats -> 128-byte chunks with an uneven last slice)."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sharded_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        sharded, replicated, m_slice, lo, hi = out[r]
+        np.testing.assert_array_equal(sharded, replicated)
+        assert lo % 32 == 0 and m_slice.size == hi - lo
+    np.testing.assert_array_equal(out[0][0], out[world - 1][0])
+
+
+def test_optimizer_shard_layout():
+    from paper_2207_11620_b200.distributed import optimizer_shard
+    for n in (1, 31, 33, 18492, 12181394):
+        for world in (1, 2, 3, 8):
+            parts = [optimizer_shard(n, r, world) for r in range(world)]
+            chunk = parts[0][0]
+            assert chunk % 32 == 0 and world * chunk >= n
+            spans = [(lo, hi) for _, lo, hi in parts if hi > lo]      # ranks past n own nothing
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert all(lo == r * chunk for r, (_, lo, hi) in enumerate(parts) if hi > lo)
+
+
 def test_shard_rows_validation():
     from paper_2207_11620_b200.distributed import shard_rows
     from paper_2207_11620_b200.errors import ConfigError

@@ -1,0 +1,76 @@
+"""Data-parallel device pipeline, two ranks sharing one GPU (gloo, eager steps): the
+sharded optimizer (reduce-scatter -> slice Adam -> all-gather) and the all-reduce
+exchange both reproduce the single-process trajectory of the same global batch, and
+every rank ends with identical parameters and the full optimizer state."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+CFG = {"encoding": {"otype": "HashGrid", "n_levels": 8, "n_features_per_level": 2,
+                    "log2_hashmap_size": 14, "base_resolution": 4},
+       "network": {"n_neurons": 32, "n_hidden_layers": 2}, "batch_size": 8192}
+STEPS = 6
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _dp_worker(rank, world, port, sharded, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NVOL_DP_SHARDED=sharded)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2207_11620_b200 import fields
+    from paper_2207_11620_b200.distributed import DataParallelTrainer
+    from paper_2207_11620_b200.model import build_model
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    model = build_model(CFG, dims=(32, 32, 32), seed=0)
+    fld = fields.rasterize("mlobb", (32, 32, 32))
+    tr = DataParallelTrainer(model, InCoreSampler(fld, seed=1), capacity=STEPS, use_graph=False)
+    assert tr.pipeline.sharded == (sharded == "1")
+    tr.step(STEPS)
+    losses = tr.finish()
+    out[rank] = (losses, model.flat_params.cpu().numpy(), model.flat_m.cpu().numpy(), model.opt.t)
+    dist.destroy_process_group()
+
+
+def _run(sharded):
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_dp_worker, args=(2, _free_port(), sharded, out), nprocs=2, join=True)
+    return dict(out)
+
+
+@pytest.mark.timeout(600)
+def test_dp_two_ranks_match_single_process(nv):
+    from paper_2207_11620_b200 import fields, trainer
+    from paper_2207_11620_b200.model import build_model
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    model = build_model(CFG, dims=(32, 32, 32), seed=0)
+    fld = fields.rasterize("mlobb", (32, 32, 32))
+    h = trainer.train(model, InCoreSampler(fld, seed=1), steps=STEPS)
+    ref_p, ref_m = model.flat_params.cpu().numpy(), model.flat_m.cpu().numpy()
+    for sharded in ("1", "0"):
+        out = _run(sharded)
+        (l0, p0, m0, t0), (l1, p1, m1, t1) = out[0], out[1]
+        np.testing.assert_array_equal(p0, p1)          # identical parameters on every rank
+        np.testing.assert_array_equal(m0, m1)          # full optimizer state on every rank
+        np.testing.assert_array_equal(l0, l1)
+        assert t0 == t1 == STEPS
+        assert l0[0] == pytest.approx(h.losses[0], rel=1e-6)   # step 0: same params, same global batch
+        np.testing.assert_allclose(l0, h.losses, rtol=2e-2)
+        np.testing.assert_allclose(p0, ref_p, rtol=0, atol=2e-3)
+        np.testing.assert_allclose(m0, ref_m, rtol=0, atol=5e-4)
