@@ -383,6 +383,31 @@ def test_tcgen05_step_matches_oracle(nv, name):
     assert rel_err(model.encoder.param_grads.cpu().numpy(), cap["enc_grads"]) < 1e-3
 
 
+@pytest.mark.timeout(600)
+def test_psnr_ensemble_within_0p1_db(nv):
+    """North-star PSNR bar (SURVEY 8c protocol): cfg1 on mlobb 64^3, 2000 steps, model
+    seed 0, sampler seeds 1-5 -- the ensemble mean PSNR of both training engines is
+    within 0.1 dB of the reference's own ensemble (tests/golden/psnr_cfg1_mlobb.json,
+    generated by running the reference)."""
+    import json
+    import os
+    from paper_2207_11620_b200 import fields, trainer
+    from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    from paper_2207_11620_b200.volume import psnr
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "psnr_cfg1_mlobb.json")))
+    dims = tuple(g["dims"])
+    fld = fields.rasterize(g["field"], dims, host=True)
+    for mode in (0, MODE_TCGEN05):
+        res = []
+        for seed in g["sampler_seeds"]:
+            m = build_model(g["config"], dims=dims, seed=g["model_seed"])
+            m.train_mode = mode
+            trainer.train(m, InCoreSampler(fld, seed=seed), steps=g["steps"])
+            res.append(psnr(fld, trainer.decode(m, dims=dims)))
+        assert abs(float(np.mean(res)) - g["mean"]) <= 0.1, (mode, res, g["mean"])
+
+
 _TC_SHAPES = [(16, 1, 4, 2), (16, 3, 4, 2), (16, 8, 6, 2), (32, 1, 6, 4), (32, 2, 16, 2), (32, 5, 8, 8),
               (64, 1, 16, 2), (64, 2, 8, 8), (64, 4, 16, 2), (64, 8, 16, 4), (32, 3, 3, 1), (64, 3, 16, 8)]
 
