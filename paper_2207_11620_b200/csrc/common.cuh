@@ -234,9 +234,24 @@ struct PcgF32Stream {
     }
 };
 
-// volume.py:148-164 _gather_corners at one point (float32 throughout).
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float ldg_hint(const float *a, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
+// volume.py:148-164 _gather_corners at one point (float32 throughout).  EVICT_FIRST:
+// the training sampler's volume reads must not push the L2-resident tables and
+// gradient out (they are touched once per step, the tables every kernel).
+template <bool EVICT_FIRST = false>
 __device__ __forceinline__ float trilinear_at(const float *__restrict__ vol, int64_t dx, int64_t dy,
                                               int64_t dz, float px, float py, float pz) {
+    const uint64_t pol = EVICT_FIRST ? l2_evict_first() : 0ull;
     float sx = xsub(xmul(px, (float)dx), 0.5f);
     float sy = xsub(xmul(py, (float)dy), 0.5f);
     float sz = xsub(xmul(pz, (float)dz), 0.5f);
@@ -252,7 +267,8 @@ __device__ __forceinline__ float trilinear_at(const float *__restrict__ vol, int
         float w = ox ? fx : xsub(1.0f, fx);
         w = xmul(w, oy ? fy : xsub(1.0f, fy));
         w = xmul(w, oz ? fz : xsub(1.0f, fz));
-        acc = xadd(acc, xmul(w, __ldg(vol + (iz * dy + iy) * dx + ix)));
+        const float *a = vol + (iz * dy + iy) * dx + ix;
+        acc = xadd(acc, xmul(w, EVICT_FIRST ? ldg_hint(a, pol) : __ldg(a)));
     }
     return acc;
 }

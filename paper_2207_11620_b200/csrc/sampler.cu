@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) sample_incore_kernel(U128 s0, U128 inc, c
     coords[3 * r] = x;
     coords[3 * r + 1] = y;
     coords[3 * r + 2] = z;
-    const float t = fminf(fmaxf(trilinear_at(vol, dx, dy, dz, x, y, z), 0.0f), 1.0f);
+    const float t = fminf(fmaxf(trilinear_at<true>(vol, dx, dy, dz, x, y, z), 0.0f), 1.0f);
     targets[r] = t;
     if (mc.lo) mc_widen(mc, dx, dy, dz, x, y, z, t);  // online macro-cells fused into the sampler
 }
