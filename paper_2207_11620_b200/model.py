@@ -132,6 +132,12 @@ class NeuralModel:
         self._pack()
         self._ws = None
         self._stage = None
+        # training engine: the tcgen05 pipeline wherever the device and the shape take it
+        # (north-star parity bar for half-precision operands: 1e-2; PSNR within 0.1 dB,
+        # test_psnr_ensemble_within_0p1_db), else the fp32 SIMT engine.  NVOL_TRAIN_ENGINE=simt
+        # (or train_mode = MODE_SIMT) selects the fp32 engine; deterministic mode always does.
+        if os.environ.get("NVOL_TRAIN_ENGINE", "auto") != "simt" and self._tc_device():
+            self.train_mode = MODE_TCGEN05
 
     # ---------------------------------------------------------------- flat buffers
     def _pack(self) -> None:
@@ -269,6 +275,14 @@ class NeuralModel:
                   c.n_features_per_level, self.mlp.config.n_neurons, self.mlp.config.n_hidden_layers,
                   int(self.mlp.config.output_activation == "relu"), 0 if self.loss_kind == "L1" else 1,
                   _lib.ptr(loss_sum), _lib.ptr(ws), ws.numel(), self._engine() | flags, _lib.stream())
+
+    def _tc_device(self) -> bool:
+        try:
+            dev = self.flat_params.device
+            return bool(dev.type == "cuda" and self.tcgen05_supported()
+                        and _lib.load().nvol_has_tcgen05(dev.index or 0))
+        except (OSError, RuntimeError):
+            return False
 
     def tcgen05_supported(self) -> bool:
         """Whether the tcgen05 training engine (MODE_TCGEN05) takes this model's shape."""
