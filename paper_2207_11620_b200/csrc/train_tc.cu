@@ -1130,7 +1130,12 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
     p.grid_sc = sms;
     p.n_coarse = 0;
     p.coarse_floats = 0;
-    for (int l = 0; l < tab.n_levels; ++l) {
+    static int max_coarse = -1;  // NVOL_SC_COARSE: cap on shared-memory levels (experiments)
+    if (max_coarse < 0) {
+        const char *e = getenv("NVOL_SC_COARSE");
+        max_coarse = e ? atoi(e) : 64;
+    }
+    for (int l = 0; l < tab.n_levels && l < max_coarse; ++l) {
         int64_t end = tab.offset[l] + tab.entries[l] * tab.n_feat;
         if (!tab.dense[l] || end * 4 > (int64_t)COARSE_BYTES) break;
         p.n_coarse = l + 1;
