@@ -498,7 +498,7 @@ def render_bench(torch, args, rank=0, world=1):
     from paper_2207_11620_b200.camera import default_camera
     from paper_2207_11620_b200.macrocell import macrocell_from_model, macrocell_set_tf
     from paper_2207_11620_b200.model import build_model
-    from paper_2207_11620_b200.render import RenderConfig, render_frame_device
+    from paper_2207_11620_b200.render import RenderConfig
     from paper_2207_11620_b200.sampler import InCoreSampler
     from paper_2207_11620_b200.trainer import train
     from paper_2207_11620_b200.transfer import default_tf
