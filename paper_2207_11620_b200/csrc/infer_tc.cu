@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(IT_THREADS, 2) infer_tc_kernel(
     const InferShape sh, const uint8_t *__restrict__ wimg, int decode, int64_t dx, int64_t dy, int64_t dz, int64_t z0,
     double lo, double scale, float *__restrict__ out, const int32_t *__restrict__ b_dev) {
     if (b_dev) b = *b_dev;  // sample count produced on the device (render loop), b was its upper bound
+    if ((int64_t)blockIdx.x * IT_TILE >= b) return;  // no tile for this CTA: skip the weight load / TMEM
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_sh;
