@@ -348,7 +348,7 @@ def run_ours(args):
     e2e = None
     if world == 1:
         from paper_2207_11620_b200.trainer import train
-        e2e_steps = max(20, min(K, 200))
+        e2e_steps = max(200, min(K, 500))   # amortises the per-call sync of train() like a real run
         host = []
         for _ in range(e2e_steps + 4):
             bt = sampler.sample(B)
