@@ -480,7 +480,8 @@ __global__ void __launch_bounds__(128) rm_step_kernel(const int32_t *__restrict_
                                                       float *__restrict__ sts, float *__restrict__ ssbar,
                                                       int32_t *__restrict__ counts, uint8_t *__restrict__ keep,
                                                       float *__restrict__ img, unsigned long long *__restrict__ evals,
-                                                      int32_t *__restrict__ coord_rays) {
+                                                      int32_t *__restrict__ coord_rays, const CamParams cam,
+                                                      const int32_t *__restrict__ hitpix) {
     const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int c = 0, marched = 0;
     // n_dev: the alive count produced on the device; n is then only its upper bound
@@ -491,7 +492,11 @@ __global__ void __launch_bounds__(128) rm_step_kernel(const int32_t *__restrict_
         keep[pos] = 0;
     } else if (pos < n) {
         const int64_t ray = ids[pos];
-        RayState R = rays[ray];
+        RayState R;
+        if (hitpix)
+            make_ray(cam, S, hitpix[ray], R);  // first iteration: the ray is generated here, not loaded
+        else
+            R = rays[ray];
         const int K = S.k_batch;
         bool alive = true;
         if (shade) {
@@ -1299,7 +1304,9 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
     int64_t n = 0;
     cudaMemcpyAsync(&n, w.nsel, 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    if (n > 0) {
+    // ray records up front for the path tracer and the in-shader marcher; the wavefront
+    // ray march generates each ray inside its first rm_step (no record write + read)
+    if (n > 0 && (S.pathtrace || architecture == 1)) {
         raygen_kernel<<<(unsigned)((n + RG_THREADS - 1) / RG_THREADS), RG_THREADS, 0, s>>>(C, S, w.ids[1], n, w.rays);
         st = check_launch("raygen");
         if (st) return st;
@@ -1394,7 +1401,8 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
                 rm_step_kernel<<<grid_for(bound, 128), 128, 0, s>>>(w.ids[cur], bound, w.nact, w.rays, S, mu,
                                                                      it > 0 ? 1 : 0, w.values, w.sxyz, w.sts, w.ssbar,
                                                                      w.counts, w.flags, img, w.evals,
-                                                                     w.coord_hist + slot);
+                                                                     w.coord_hist + slot, C,
+                                                                     it == 0 ? w.ids[1] : nullptr);
                 cub::DeviceScan::ExclusiveSum(w.cub_tmp, w.cub_bytes, w.counts, w.offs, (int)bound, s);
                 compact_ids_kernel<<<grid_for(bound, 256), 256, 0, s>>>(w.sxyz, w.ids[cur], w.counts, w.offs, bound,
                                                                          K, w.dxyz, w.dtotal);
@@ -1437,7 +1445,7 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
             cudaMemsetAsync(w.coord_rays, 0, 4, s);
             rm_step_kernel<<<grid_for(n, 128), 128, 0, s>>>(w.ids[cur], n, nullptr, w.rays, S, mu, shade ? 1 : 0, w.values,
                                                              w.sxyz, w.sts, w.ssbar, w.counts, w.flags, img, w.evals,
-                                                             w.coord_rays);
+                                                             w.coord_rays, C, shade ? nullptr : w.ids[1]);
             st = check_launch("rm_step");
             if (st) return st;
             shade = true;
