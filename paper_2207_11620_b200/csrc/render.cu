@@ -9,10 +9,11 @@
 // Two schedules, as in the reference:
 //  * in-shader (render_reference / rm_reference): one thread per ray runs its
 //    state machine to completion and evaluates Phi inline (exact evaluator);
-//  * sample streaming (render_wavefront): per iteration, rm_coord stages up to
-//    K samples per alive ray, one batched Phi evaluation runs over all staged
-//    samples (exact or tcgen05), rm_shade composites and retires rays, and a
-//    stable CUB compaction keeps the alive rays contiguous.
+//  * sample streaming (render_wavefront): per iteration, rm_step_kernel
+//    composites the previous samples of each alive ray (rm_shade) and stages up
+//    to K new ones (rm_coord), appending them densely; one batched Phi
+//    evaluation runs over all staged samples (exact or tcgen05) and a stable
+//    CUB selection keeps the list of alive ray ids contiguous.
 // Geometry (DDA, clocks, coordinates) is float64/float32 with the reference's
 // operation order and no FMA contraction (file compiled with -fmad=false).
 // pow is evaluated in float64 and rounded, which matches the reference's
@@ -478,20 +479,21 @@ __global__ void __launch_bounds__(128) rm_step_kernel(const int32_t *__restrict_
                                                       const float *__restrict__ mu, int shade,
                                                       const float *__restrict__ values, float *__restrict__ sxyz,
                                                       float *__restrict__ sts, float *__restrict__ ssbar,
-                                                      int32_t *__restrict__ counts, uint8_t *__restrict__ keep,
+                                                      uint8_t *__restrict__ keep,
                                                       float *__restrict__ img, unsigned long long *__restrict__ evals,
                                                       int32_t *__restrict__ coord_rays, const CamParams cam,
-                                                      const int32_t *__restrict__ hitpix) {
+                                                      const int32_t *__restrict__ hitpix, float *__restrict__ dxyz,
+                                                      int32_t *__restrict__ dray, int32_t *__restrict__ dcount) {
     const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int c = 0, marched = 0;
+    int64_t ray = 0;
     // n_dev: the alive count produced on the device; n is then only its upper bound
     // (launch size), and positions in [*n_dev, n) stage nothing and keep nothing
     const int64_t nact = n_dev ? *n_dev : n;
     if (pos < n && pos >= nact) {
-        counts[pos] = 0;
         keep[pos] = 0;
     } else if (pos < n) {
-        const int64_t ray = ids[pos];
+        ray = ids[pos];
         RayState R;
         if (hitpix)
             make_ray(cam, S, hitpix[ray], R);  // first iteration: the ray is generated here, not loaded
@@ -537,8 +539,30 @@ __global__ void __launch_bounds__(128) rm_step_kernel(const int32_t *__restrict_
             R.mdone = done;
             rays[ray] = R;
         }
-        counts[pos] = c;
         keep[pos] = alive ? 1 : 0;
+    }
+    // the staged samples go densely to dxyz (one atomic per warp; evaluation order does not
+    // matter: every sample is evaluated independently), with their (ray, slot) for the scatter back
+    {
+        const int lane = threadIdx.x & 31;
+        int incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+        int base = 0;
+        if (lane == 31 && wtot) base = atomicAdd(dcount, wtot);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - c;
+        const int K = S.k_batch;
+        for (int j = 0; j < c; ++j) {
+            const int64_t i = ray * K + j;
+            const int64_t d = (int64_t)base + j;
+            dxyz[3 * d] = sxyz[3 * i];
+            dxyz[3 * d + 1] = sxyz[3 * i + 1];
+            dxyz[3 * d + 2] = sxyz[3 * i + 2];
+            dray[d] = (int32_t)i;
+        }
     }
     // phi_eval_staged evaluates exactly the staged samples (_render_kernels.py:518-540)
     unsigned long long tot = (unsigned long long)c;
@@ -553,31 +577,17 @@ __global__ void __launch_bounds__(128) rm_step_kernel(const int32_t *__restrict_
     }
 }
 
-// the staged samples of the alive rays, densely: dxyz[offs[pos] + j] = sxyz[ids[pos] * K + j]
-__global__ void compact_ids_kernel(const float *__restrict__ sxyz, const int32_t *__restrict__ ids,
-                                   const int32_t *__restrict__ counts, const int32_t *__restrict__ offs, int64_t n,
-                                   int K, float *__restrict__ dxyz, int32_t *__restrict__ total) {
-    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pos >= n) return;
-    const int c = counts[pos], o = offs[pos];
-    const int64_t ray = ids[pos];
-    for (int j = 0; j < c; ++j) {
-        const int64_t i = ray * K + j;
-        dxyz[3 * (int64_t)(o + j)] = sxyz[3 * i];
-        dxyz[3 * (int64_t)(o + j) + 1] = sxyz[3 * i + 1];
-        dxyz[3 * (int64_t)(o + j) + 2] = sxyz[3 * i + 2];
-    }
-    if (pos == n - 1) *total = o + c;
+// evaluated dense samples back to their (ray, slot): values[dray[i]] = dvals[i], i < *count
+__global__ void scatter_dense_kernel(const float *__restrict__ dvals, const int32_t *__restrict__ dray,
+                                     const int32_t *__restrict__ count, int64_t bound, float *__restrict__ values) {
+    const int64_t n = min(bound, (int64_t)*count);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        values[dray[i]] = dvals[i];
 }
 
-__global__ void scatter_ids_kernel(const float *__restrict__ dvals, const int32_t *__restrict__ ids,
-                                   const int32_t *__restrict__ counts, const int32_t *__restrict__ offs, int64_t n,
-                                   int K, float *__restrict__ values) {
-    const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pos >= n) return;
-    const int c = counts[pos], o = offs[pos];
-    const int64_t ray = ids[pos];
-    for (int j = 0; j < c; ++j) values[ray * K + j] = dvals[o + j];
+static unsigned dense_grid(int64_t n) {  // grid-stride launches sized for a device-side count <= n
+    const int64_t b = (n + 255) / 256;
+    return (unsigned)(b < 1 ? 1 : (b > 148 * 8 ? 148 * 8 : b));
 }
 
 // Path tracing's position-indexed staging (one slot per ray): compacted with the
@@ -1088,7 +1098,7 @@ struct RenderWs {
     int32_t *ids[2];           // alive ray indices (ping-pong), then hit pixel ids at setup
     uint8_t *flags;
     float *sxyz, *sts, *ssbar, *values, *dxyz, *dvals;
-    int32_t *counts, *offs, *dtotal, *coord_rays, *coord_hist;
+    int32_t *counts, *offs, *dtotal, *coord_rays, *coord_hist, *dray;
     unsigned long long *evals;
     int64_t *nsel, *nact;
     void *cub_tmp;
@@ -1119,6 +1129,7 @@ static RenderWs carve(void *base, int64_t npix, int k) {
     w.offs = (int32_t *)take(npix * 4);
     w.dxyz = (float *)take(npix * k * 12);
     w.dvals = (float *)take(npix * k * 4);
+    w.dray = (int32_t *)take(npix * k * 4);
     w.dtotal = (int32_t *)take(8);
     w.coord_rays = (int32_t *)take(8);
     w.coord_hist = (int32_t *)take(4 * (int64_t)RM_HIST_CAP);
@@ -1398,21 +1409,20 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
             int cur = 0, it = 0;
             for (;;) {
                 const int slot = it < RM_HIST_CAP ? it : RM_HIST_CAP - 1;
+                cudaMemsetAsync(w.dtotal, 0, 4, s);
                 rm_step_kernel<<<grid_for(bound, 128), 128, 0, s>>>(w.ids[cur], bound, w.nact, w.rays, S, mu,
                                                                      it > 0 ? 1 : 0, w.values, w.sxyz, w.sts, w.ssbar,
-                                                                     w.counts, w.flags, img, w.evals,
+                                                                     w.flags, img, w.evals,
                                                                      w.coord_hist + slot, C,
-                                                                     it == 0 ? w.ids[1] : nullptr);
-                cub::DeviceScan::ExclusiveSum(w.cub_tmp, w.cub_bytes, w.counts, w.offs, (int)bound, s);
-                compact_ids_kernel<<<grid_for(bound, 256), 256, 0, s>>>(w.sxyz, w.ids[cur], w.counts, w.offs, bound,
-                                                                         K, w.dxyz, w.dtotal);
+                                                                     it == 0 ? w.ids[1] : nullptr, w.dxyz, w.dray,
+                                                                     w.dtotal);
                 cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, w.ids[cur], w.flags, w.ids[cur ^ 1], w.nact,
                                            bound, s);
                 st = infer_tc_launch(w.dxyz, bound * K, params, tab, weights, (uint8_t *)mlp_image, widths[1],
                                      n_layers - 1, relu_out, 0, 0, 0, 0, 0, 0.0, 1.0, w.dvals, s, it == 0, w.dtotal);
                 if (st) return st;
-                scatter_ids_kernel<<<grid_for(bound, 256), 256, 0, s>>>(w.dvals, w.ids[cur], w.counts, w.offs, bound,
-                                                                         K, w.values);
+                scatter_dense_kernel<<<dense_grid(bound * K), 256, 0, s>>>(w.dvals, w.dray, w.dtotal, bound * K,
+                                                                               w.values);
                 st = check_launch("render iteration");
                 if (st) return st;
                 cudaMemcpyAsync(&h_cnt[it & 1], w.nact, 8, cudaMemcpyDeviceToHost, s);
@@ -1443,16 +1453,15 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
         while (n > 0) {
             // shade the previous iteration's samples, stage this iteration's (one ray record pass)
             cudaMemsetAsync(w.coord_rays, 0, 4, s);
+            cudaMemsetAsync(w.dtotal, 0, 4, s);
             rm_step_kernel<<<grid_for(n, 128), 128, 0, s>>>(w.ids[cur], n, nullptr, w.rays, S, mu, shade ? 1 : 0, w.values,
-                                                             w.sxyz, w.sts, w.ssbar, w.counts, w.flags, img, w.evals,
-                                                             w.coord_rays, C, shade ? nullptr : w.ids[1]);
+                                                             w.sxyz, w.sts, w.ssbar, w.flags, img, w.evals,
+                                                             w.coord_rays, C, shade ? nullptr : w.ids[1], w.dxyz, w.dray,
+                                                             w.dtotal);
             st = check_launch("rm_step");
             if (st) return st;
             shade = true;
             // dense evaluation of the staged samples + the next alive list, one host sync
-            cub::DeviceScan::ExclusiveSum(w.cub_tmp, w.cub_bytes, w.counts, w.offs, (int)n, s);
-            compact_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.sxyz, w.ids[cur], w.counts, w.offs, n, K, w.dxyz,
-                                                                 w.dtotal);
             cub::DeviceSelect::Flagged(w.cub_tmp, w.cub_bytes, w.ids[cur], w.flags, w.ids[cur ^ 1], w.nsel, n, s);
             int32_t hv[2] = {0, 0};
             int64_t nn_next = 0;
@@ -1479,8 +1488,7 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
                                             0, 0.0, 1.0, w.dvals, s);
                 }
                 if (st) return st;
-                scatter_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(w.dvals, w.ids[cur], w.counts, w.offs, n, K,
-                                                                     w.values);
+                scatter_dense_kernel<<<dense_grid(ns), 256, 0, s>>>(w.dvals, w.dray, w.dtotal, ns, w.values);
             }
             n = nn_next;
             cur ^= 1;
