@@ -468,7 +468,10 @@ def test_tcgen05_training_converges(nv):
             runs.append(psnr(fld, trainer.decode(m, dims=(48, 48, 48))))
         res[mode] = float(np.mean(runs))
     assert res[MODE_TCGEN05] > 20.0
-    assert abs(res[MODE_TCGEN05] - res[0]) < 1.5, res
+    # one-sided: half-precision operands must not cost more than 1.5 dB against the fp32
+    # engine (three 200-step runs are chaotic to ~1.5 dB either way; the 0.1 dB parity bar
+    # is test_psnr_ensemble_within_0p1_db's, on the SURVEY protocol)
+    assert res[MODE_TCGEN05] > res[0] - 1.5, res
 
 
 @pytest.mark.parametrize("name,batch", [("cfg2", 8192), ("odd", 4000), ("cfg1", 1000)])
