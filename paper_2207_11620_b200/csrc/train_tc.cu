@@ -156,6 +156,20 @@ __device__ __forceinline__ V tab_ld(const V *p) {
         return __ldg(p);
 }
 
+// hashed-level gathers do not allocate in L1 (no reuse there), which keeps L1 for the dense
+// coarse levels every warp of a level shares (measured 29.5 -> 28.8 us per encode)
+__device__ __forceinline__ float4 ld_na4(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float2 ld_na2(const float2 *p) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+
 // One (sample i, level l) item of the encoder forward (_kernels.py:31-79), bit-exact
 // fp32, split into fp16 hi + lo and stored straight into the UMMA tile layout.
 template <int NF, bool COHERENT>
@@ -184,13 +198,19 @@ __device__ __forceinline__ void encode_item(const float *__restrict__ coords, co
         for (int k = 0; k < 8; k += 2) {
             const uint32_t lo = min(sl[k], sl[k + 1]);
             if (max(sl[k], sl[k + 1]) == lo + 1 && ((lo + par) & 1u) == 0u) {
-                const float4 q = tab_ld<COHERENT>(reinterpret_cast<const float4 *>(tb + 2 * (size_t)lo));
+                const float4 q = (!COHERENT && !dense) ? ld_na4(reinterpret_cast<const float4 *>(tb + 2 * (size_t)lo))
+                                                       : tab_ld<COHERENT>(reinterpret_cast<const float4 *>(tb + 2 * (size_t)lo));
                 const bool lo_first = sl[k] == lo;
                 v[k] = lo_first ? make_float2(q.x, q.y) : make_float2(q.z, q.w);
                 v[k + 1] = lo_first ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
             } else {
-                v[k] = tab_ld<COHERENT>(reinterpret_cast<const float2 *>(tb) + sl[k]);
-                v[k + 1] = tab_ld<COHERENT>(reinterpret_cast<const float2 *>(tb) + sl[k + 1]);
+                if (!COHERENT && !dense) {
+                    v[k] = ld_na2(reinterpret_cast<const float2 *>(tb) + sl[k]);
+                    v[k + 1] = ld_na2(reinterpret_cast<const float2 *>(tb) + sl[k + 1]);
+                } else {
+                    v[k] = tab_ld<COHERENT>(reinterpret_cast<const float2 *>(tb) + sl[k]);
+                    v[k + 1] = tab_ld<COHERENT>(reinterpret_cast<const float2 *>(tb) + sl[k + 1]);
+                }
             }
         }
 #pragma unroll
