@@ -186,8 +186,12 @@ def run_ours(args):
     from paper_2207_11620_b200.trainer import StepPipeline, decode
 
     rank, world, local = init_from_env("nccl")
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but the process group has {world} rank(s)")
     torch.cuda.set_device(local)
     _lib.load()
+    comm = {"backend": dist.get_backend() if world > 1 else None, "world": world,
+            "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if world > 1 else None}
     hbm, tc_sus, tc_burst, peak_kind = peaks()
     model = build_model(CFG2, dims=DIMS, seed=0)
     model.train_mode = args.mode
@@ -242,7 +246,7 @@ def run_ours(args):
         ev[0].record(stream)
         _lib.call("nvol_adam_train_step", _lib.ptr(model.flat_params), _lib.ptr(model.flat_grads),
                   _lib.ptr(model.flat_m), _lib.ptr(model.flat_v), model.flat_size, _lib.ptr(pipe.sched),
-                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_flag),
+                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_state),
                   _lib.ptr(pipe.acc), None, pipe.t0, 0, 1.0 / B, _lib.ptr(pipe.ticket), _lib.stream())
         ev[1].record(stream)
 
@@ -253,12 +257,33 @@ def run_ours(args):
         ev[0].record(stream)
         _lib.call("nvol_adam_encode_step", _lib.ptr(model.flat_params), _lib.ptr(model.flat_grads),
                   _lib.ptr(model.flat_m), _lib.ptr(model.flat_v), model.flat_size, _lib.ptr(pipe.sched),
-                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_flag),
+                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_state),
                   _lib.ptr(pipe.acc), None, pipe.t0, 0, 1.0 / B, _lib.ptr(pipe.work), _lib.ptr(pipe.bufs[1][0]), b,
                   off, res, ent, dense, cfg.n_levels, cfg.n_features_per_level, model.mlp.config.n_neurons,
                   model.mlp.config.n_hidden_layers, _lib.ptr(ws), ws.numel(), _lib.stream())
         ev[1].record(stream)
 
+    def exchange_fn(ev):
+        from paper_2207_11620_b200.distributed import allgather_shards, reduce_scatter_grads
+        ev[0].record(stream)
+        if pipe.sharded:
+            reduce_scatter_grads(model.flat_grads_padded, pipe.gslice, None)
+            allgather_shards(model.flat_params_padded, rank, None)
+        else:
+            dist.all_reduce(model.flat_grads)
+        ev[1].record(stream)
+
+    exchange = None
+    if world > 1:
+        snap = model.flat_params.clone()
+        t_x = float(_event_ms(torch, exchange_fn)[0])
+        model.flat_params.copy_(snap)
+        model.flat_grads.zero_()
+        t = torch.tensor([t_x], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        exchange = {"ms": float(t.item()), "bytes_per_rank": 4 * model.flat_size * (2 if pipe.sharded else 1),
+                    "kind": "NCCL reduce-scatter + all-gather (sharded optimizer)" if pipe.sharded
+                    else "NCCL all-reduce", "share_of_step": float(t.item()) / ms_per_step}
     t_sample = float(_event_ms(torch, sample_fn)[0])
     t_adam = float(_event_ms(torch, adam_fn)[0])
     kernels = {"sample_incore_kernel": t_sample, "adam_step_kernel": t_adam}
@@ -385,6 +410,13 @@ def run_ours(args):
         dt = time.perf_counter() - t0
         e2e["train_step_api"] = {"value": B * 20 / dt, "unit": "samples/s", "steps": 20}
 
+    # ---- the fp32 SIMT engine (ordered-reduction / bitwise-repeatable mode's engine) on the same step
+    simt = None
+    if args.mode == 1 and world == 1 and not args.no_simt:
+        ms_s = simt_rate(torch, model, sampler, K=min(K, 20))
+        simt = {"value": B / (ms_s * 1e-3), "unit": "samples/s", "ms_per_step": ms_s,
+                "engine": "fp32 SIMT (generic kernels, CUDA cores; what set_deterministic(True) runs)"}
+
     # ---- decode (cfg3) and render (cfg4) beside the headline
     dec = None
     if not args.no_decode:
@@ -408,12 +440,35 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dms = float(t.item())
         nvox = dd[0] * dd[1] * dd[2]
-        dec = {"value": nvox / (dms / 1e3), "unit": "samples/s", "ms": dms, "dims": list(dd),
+        live = decode_live_corners(model, dd)
+        vps = nvox / (dms / 1e3)
+        flops_vox = 2 * (32 * 64 + 3 * 64 * 64 + 64)
+        dec = {"value": vps, "unit": "samples/s", "ms": dms, "dims": list(dd),
                "mode": args.decode_mode, "workload": "cfg3: full-grid decode of the cfg2 model",
                "sharding": f"z-slabs over {world} GPU(s), max over ranks",
-               "gather_gbs": nvox * 1024 / (dms * 1e-3) / 1e9,
-               "mlp_tflops": nvox * 2 * 3 * (32 * 64 + 3 * 64 * 64) / (dms * 1e-3) / 1e12}
+               "roofline": {"bound": "l2 gather rate (encoder) / tensor (MLP)",
+                            "live_corner_gathers_per_voxel": live,
+                            "achieved_gather_gops": live * vps / 1e9, "peak_gather_gops": l2_gather,
+                            "frac": live * vps / 1e9 / l2_gather,
+                            "mlp_tflops": vps * flops_vox / 1e12, "mlp_peak_tflops": tc_sus,
+                            "mlp_frac": vps * flops_vox / 1e12 / tc_sus,
+                            "hbm_bytes_per_voxel": 4, "hbm_frac": vps * 4 / 1e9 / hbm,
+                            "basis": "corners with non-zero trilinear weight at voxel centres (zero-weight corners "
+                                     "are skipped bit-exactly); 28,800 algorithmic MLP flop per voxel"}}
         del out
+        if world == 1:
+            # e2e through the public API: decode(model, dims, to_host=True) lands the 4 GiB volume in
+            # host memory (per-slab D2H overlapped with the next slab's decode), as the reference's
+            # decode returns a host ScalarField (trainer.py:98-106); wall clock incl. allocation
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fld_h = decode(model, dims=dd, to_host=True)
+            wall = time.perf_counter() - t0
+            dec["e2e"] = {"value": nvox / wall, "unit": "samples/s", "s": wall, "h2d_bytes": 0,
+                          "d2h_bytes": nvox * 4, "api": "trainer.decode(model, dims, to_host=True) -> host "
+                                                        "ScalarField (numpy f32)",
+                          "checksum": float(np.asarray(fld_h.data[::64, ::64, ::64], np.float64).sum())}
+            del fld_h
         if rank == 0 and world == 1 and not args.no_cpu:
             dec["cpu_baseline"] = cpu_decode_rate(model.blob().cpu().numpy())
     rend = None
@@ -431,7 +486,10 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K, "warmup": W,
                 "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "vs_baseline": None,
+                "dtype": ("f32 tables / loss / Adam; fp16-operand tcgen05 MLP (split-fp16 forward, fp16 backward, "
+                          "fp32 accumulate)") if args.mode == 1 else "f32",
+                "data": "synthetic",
                 "config": {"workload": "cfg2 training step (configs[1]): synthetic 256^3 mlobb volume, HashGrid "
                                        "16 levels x 2^19 x 2 feat, 4x64 ReLU MLP, B=65536/step global, L1 + Adam",
                            "global_batch": B, "parallelism": f"dp{world}",
@@ -439,11 +497,50 @@ def run_ours(args):
                            else "simt fp32",
                            "l2": "inputs larger than L2: each step streams 390 MB of Adam state (> 126 MB L2)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary(), "decode": dec, "render": rend, "cfg5": c5,
+                "clocks": clk.summary(), "decode": dec, "render": rend, "cfg5": c5, "simt_engine": simt,
+                "exchange": exchange, "comm": comm,
                 "final_loss": float(losses[-1])}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def decode_live_corners(model, dims) -> float:
+    """Mean number of corners with non-zero trilinear weight per voxel-centre sample
+    ((i+0.5)/D per axis) over the levels -- the gathers the decode actually issues."""
+    res = [int(r) for r in model.encoder.level_resolutions]
+    tot = 0.0
+    for r in res:
+        per_axis = []
+        for d in dims:
+            i = np.arange(d, dtype=np.float32)
+            p = (i + np.float32(0.5)) / np.float32(d)
+            s = p * np.float32(r)
+            fr = s - np.floor(s)
+            per_axis.append(float(np.mean(np.where(fr == 0, 1.0, 2.0))))
+        tot += per_axis[0] * per_axis[1] * per_axis[2]
+    return tot
+
+
+def simt_rate(torch, model0, sampler, K=20):
+    """ms per device-resident cfg2 step of the fp32 SIMT engine (same model shape / batch)."""
+    from paper_2207_11620_b200.model import MODE_SIMT, build_model
+    from paper_2207_11620_b200.trainer import StepPipeline
+    m = build_model(CFG2, dims=DIMS, seed=0)
+    m.train_mode = MODE_SIMT
+    p = StepPipeline(m, sampler, capacity=K + 4)
+    p.step(3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s = torch.cuda.current_stream()
+    e0.record(s)
+    p.step(K)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    p.finish()
+    del p, m
+    return ms
 
 
 def cfg5_bench(torch, args, rank=0, world=1):
@@ -559,10 +656,20 @@ def main():
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-simt", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under the torchrun launcher (rendezvous on 127.0.0.1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

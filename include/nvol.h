@@ -47,7 +47,8 @@ extern "C" {
 /* ------------------------------------------------------------------ library */
 
 /* ABI version (bumped on any signature change; 2: the nvol_render camera parameter array gained
- * the image tile rows row0, nrows; 3: nvol_render path tracing block + 3 stats). */
+ * the image tile rows row0, nrows; 3: nvol_render path tracing block + 3 stats; 4: the training
+ * pipeline's NaN state (nvol_train_fwd_bwd / nvol_adam_train_step / nvol_adam_encode_step). */
 int nvol_abi_version(void);
 /* Static string describing the last non-zero status (thread-local). */
 const char *nvol_last_error(void);
@@ -240,14 +241,15 @@ int nvol_decode(const float *params, const int64_t *level_off, const int64_t *le
  * coords/targets: [b] rows of this rank; grad_scale = 1/B_global (L1 sign
  * gradient, network.py:108).  loss_sum (f64) accumulates sum |pred-target|.
  * mode 0 = SIMT fp32, 1 = tcgen05 (fp16 operands, fp32 accumulate), optionally
- * or-ed with NVOL_TRAIN_PREENCODED / NVOL_TRAIN_ENCODE_ONLY (below). */
+ * or-ed with NVOL_TRAIN_PREENCODED / NVOL_TRAIN_ENCODE_ONLY (below).
+ * nan_state (nullable): NaN detection + halt, see "NaN contract" below. */
 int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int64_t b_global,
                        const float *params, float *grads, const int64_t *level_off,
                        const int64_t *level_res, const int64_t *level_entries,
                        const uint8_t *level_dense, int32_t n_levels, int32_t n_feat,
                        int32_t n_neurons, int32_t n_hidden, int32_t relu_out, int32_t loss_kind,
                        double *loss_sum, void *workspace, int64_t workspace_bytes, int32_t mode,
-                       void *stream);
+                       int64_t *nan_state, void *stream);
 
 /* Profiling hook (bench.py): with n >= 4 cudaEvent_t handles set,
  * nvol_train_fwd_bwd mode 1 runs unchunked on the caller's stream and records
@@ -255,6 +257,27 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
  * each stage kernel is timed with CUDA events on its launching stream.
  * n = 0 disables.  [host] array of event handles. */
 int nvol_set_stage_events(void *const *events, int32_t n);
+
+/* Parity hooks for the tcgen05 training engine (tests only; all null in
+ * production).  While set, nvol_train_fwd_bwd mode 1 additionally writes
+ * feat  [b][n_levels*n_feat] f32: the hot encoder's fp32 features
+ *       (encode_tiles_kernel, before the fp16 split; reference
+ *       _kernels.py:31-79 grid_encode_fwd `out`),
+ * pred  [b] f32: the per-sample MLP output of mlp_tc_kernel
+ *       (network.py:61-74 Mlp.forward),
+ * dfeat [n_levels*n_feat][b] f32: the feature-major dL/dfeat the MLP hands to
+ *       the scatter (network.py:76-93 Mlp.backward return value). */
+int nvol_train_tc_debug(float *feat, float *pred, float *dfeat);
+
+/* The tcgen05 engine's encoder-backward kernel on its own (the launch
+ * nvol_train_fwd_bwd mode 1 makes after the MLP), fed a caller-provided
+ * feature-major dL/dfeat [n_levels*n_feat][stride]; accumulates into grads
+ * (the flat buffer's encoder region).  Replaces grid_encode_bwd
+ * (_kernels.py:82-92) with the corners recomputed from coords. */
+int nvol_train_tc_scatter(const float *coords, const float *dfeat, int64_t b, int64_t stride,
+                          const int64_t *level_off, const int64_t *level_res,
+                          const int64_t *level_entries, const uint8_t *level_dense,
+                          int32_t n_levels, int32_t n_feat, float *grads, void *stream);
 
 /* L2 set-aside for persisting lines (cudaLimitPersistingL2CacheSize): the
  * training step keeps its flat gradient L2-resident between Adam and the
@@ -291,12 +314,31 @@ int nvol_adam_flat_dev(float *p, float *g, float *m, float *v, int64_t n, const 
  * update, then (last block to finish, via the zero-initialised u32 *ticket)
  * losses[*step_counter - t0] = *loss_acc * inv_b (if 0 <= index < cap),
  * *loss_acc = 0 and ++*step_counter — i.e. nvol_loss_record + Adam + counter
- * advance of trainer.py:61-77 / network.py:160-183 without extra launches. */
+ * advance of trainer.py:61-77 / network.py:160-183 without extra launches.
+ * nan_state (nullable): the pipeline's NaN state, see "NaN contract" below. */
 int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, const float *sched,
                          int64_t sched_len, int64_t *step_counter, float beta1, float one_minus_beta1,
-                         float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
+                         float beta2, float one_minus_beta2, float eps, float l2, int64_t *nan_state,
                          double *loss_acc, double *losses, int64_t t0, int64_t cap, double inv_b,
                          uint32_t *ticket, void *stream);
+
+/* NaN contract of the training pipeline (network.py:160-183 adam_step checks
+ * every parameter group for a NaN gradient BEFORE updating it and raises
+ * FloatingPointError(group, flat index) without advancing t).  nan_state is a
+ * device int64[2], initialised to {INT64_MAX, 0}:
+ *   [0] the flat index where the first parameter group holding a NaN gradient
+ *       starts (INT64_MAX: none).  Set by the tcgen05 MLP kernel (NaN in
+ *       dL/dfeat -> encoder group 0; NaN in dW_j -> W_j's start) or by
+ *       nvol_nan_scan (SIMT engine); lowered by nvol_adam_train_step for a NaN
+ *       it meets itself.
+ *   [1] halted.  nvol_adam_train_step updates only q < [0] (the groups in front
+ *       of the offending one, as the reference) and, when [0] is set, halts
+ *       instead of recording the loss and advancing the step counter; the
+ *       training kernels (encode / MLP / scatter / Adam) of a halted pipeline
+ *       return at entry.  The host raises FloatingPointError with the group
+ *       and the first NaN's flat index (nvol_find_nan over that group). */
+int nvol_nan_scan(const float *g, int64_t n, const int64_t *group_starts, int32_t n_groups,
+                  int64_t *nan_state, void *stream);
 
 /* nvol_train_fwd_bwd mode flags (tcgen05 engine, mode 1 only). */
 #define NVOL_TRAIN_PREENCODED 16  /* the workspace's tile buffer already holds this batch's encoding */
@@ -314,7 +356,7 @@ int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, cons
  * _kernels.py:31-79). */
 int nvol_adam_encode_step(float *p, float *g, float *m, float *v, int64_t n, const float *sched,
                           int64_t sched_len, int64_t *step_counter, float beta1, float one_minus_beta1,
-                          float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
+                          float beta2, float one_minus_beta2, float eps, float l2, int64_t *nan_state,
                           double *loss_acc, double *losses, int64_t t0, int64_t cap, double inv_b,
                           uint32_t *work, const float *next_coords, int64_t b, const int64_t *level_off,
                           const int64_t *level_res, const int64_t *level_entries,

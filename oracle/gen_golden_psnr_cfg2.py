@@ -1,0 +1,79 @@
+"""Reference PSNR ensemble at the bench's training config (cfg2) -- test infrastructure.
+
+    OPENBLAS_NUM_THREADS=1 python oracle/gen_golden_psnr_cfg2.py --seed S [--steps N]   # one member
+    python oracle/gen_golden_psnr_cfg2.py --merge                                       # -> tests/golden/psnr_cfg2_mlobb.json
+
+SURVEY.md §8(c) protocol at configs[1]: the reference's cfg2 model (HashGrid 16 x 2^19 x 2,
+4 x 64 ReLU MLP, B = 65,536, L1 + Adam; model seed 0) trained with
+`neuralvol.trainer.train(model, InCoreSampler(field, seed=S), steps)` on
+`fields.rasterize("mlobb", (256,)*3)` for sampler seeds 1..5, then
+`psnr(field, decode(model))` at 256^3 (/root/reference/pkg/src/neuralvol/trainer.py:61-106,
+volume.py:197-242).  Reduced step count (the reference runs at ~0.8 s per cfg2 step on
+one core); the number of steps and the BLAS thread count are recorded in the fixture.
+Each member runs in its own process (the members are independent) so the ensemble
+finishes in one member's time on a multi-core host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+PART = Path("/tmp/psnr_cfg2_parts")
+CFG2 = {"encoding": {"otype": "HashGrid", "n_levels": 16, "n_features_per_level": 2,
+                     "log2_hashmap_size": 19, "base_resolution": 4},
+        "network": {"n_neurons": 64, "n_hidden_layers": 4}, "batch_size": 65536}
+DIMS = (256, 256, 256)
+
+
+def member(seed: int, steps: int) -> None:
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from neuralvol import fields
+    from neuralvol.model import build_model
+    from neuralvol.sampler import InCoreSampler
+    from neuralvol.trainer import decode, train
+    from neuralvol.volume import psnr
+    fld = fields.rasterize("mlobb", DIMS)
+    model = build_model(CFG2, dims=DIMS, seed=0)
+    t0 = time.time()
+    hist = train(model, InCoreSampler(fld, seed=seed), steps=steps)
+    t1 = time.time()
+    val = float(psnr(fld, decode(model, dims=DIMS)))
+    PART.mkdir(exist_ok=True)
+    (PART / f"seed{seed}.json").write_text(json.dumps(
+        {"seed": seed, "steps": steps, "psnr": val, "final_loss": float(hist.losses[-1]),
+         "train_s": t1 - t0, "decode_s": time.time() - t1,
+         "openblas_num_threads": os.environ.get("OPENBLAS_NUM_THREADS", "unset")}))
+    print("seed", seed, "psnr", val, flush=True)
+
+
+def merge() -> None:
+    parts = sorted((json.loads(p.read_text()) for p in PART.glob("seed*.json")), key=lambda d: d["seed"])
+    vals = [p["psnr"] for p in parts]
+    steps = {p["steps"] for p in parts}
+    threads = {p["openblas_num_threads"] for p in parts}
+    assert len(steps) == 1 and len(threads) == 1, (steps, threads)
+    (OUT / "psnr_cfg2_mlobb.json").write_text(json.dumps(
+        {"config": CFG2, "field": "mlobb", "dims": list(DIMS), "steps": steps.pop(), "model_seed": 0,
+         "sampler_seeds": [p["seed"] for p in parts], "psnr_db": vals, "mean": float(np.mean(vals)),
+         "std": float(np.std(vals)), "final_losses": [p["final_loss"] for p in parts],
+         "openblas_num_threads": threads.pop(), "reference_train_s": [p["train_s"] for p in parts],
+         "generator": "oracle/gen_golden_psnr_cfg2.py (neuralvol.trainer.train + decode + volume.psnr)"}, indent=1))
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seed", type=int)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--merge", action="store_true")
+    a = ap.parse_args()
+    if a.merge:
+        merge()
+    else:
+        member(a.seed, a.steps)

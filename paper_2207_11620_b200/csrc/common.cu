@@ -57,7 +57,7 @@ int nvol_set_deterministic(int32_t on) {
     return NVOL_OK;
 }
 
-int nvol_abi_version(void) { return 3; }  // 3: nvol_render path tracing (render_params[29], stats_out[3])
+int nvol_abi_version(void) { return 4; }  // 4: training NaN state (see nvol.h "NaN contract")
 
 const char *nvol_last_error(void) { return nvol::g_last_error; }
 

@@ -59,6 +59,27 @@ __device__ __forceinline__ void adam_one(T &p, T &g, T &m, T &v, T lr, T b1, T o
     g = (T)0;
 }
 
+// ----------------------------------------------------------------------------- NaN contract
+// The training pipeline's device NaN state (int64[2], nvol.h "NaN state"):
+// [0] = flat index where the first parameter group holding a NaN gradient starts
+// (kNanNone: none), [1] = halted.  network.py:167-171 checks each group for NaN
+// BEFORE updating it, so the groups in front of the offending one are updated
+// and the rest are not; the flat buffer keeps the groups in order, so "update
+// q < state[0]" is exactly that prefix.  The step's last Adam block then sets
+// halted and every later kernel of the pipeline returns at entry (the
+// reference raises and stops; t is not advanced).
+constexpr int64_t kNanNone = 0x7fffffffffffffffll;
+
+__device__ __forceinline__ bool nan_halted(const int64_t *ns) {
+    return ns != nullptr && *reinterpret_cast<const volatile int64_t *>(ns + 1) != 0;
+}
+__device__ __forceinline__ int64_t nan_limit(const int64_t *ns) {
+    return ns != nullptr ? *reinterpret_cast<const volatile int64_t *>(ns) : kNanNone;
+}
+__device__ __forceinline__ void nan_mark(int64_t *ns, int64_t group_start) {
+    if (ns != nullptr) atomicMin(reinterpret_cast<long long *>(ns), (long long)group_start);
+}
+
 // ----------------------------------------------------------------------------- grid tables
 // GridEncoder.kernel_tables() (encoding.py:174-177) packed by value.
 struct GridTables {

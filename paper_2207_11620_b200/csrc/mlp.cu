@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
                 atomicAdd(dst, v);
             } else {
                 if (accumulate) v += *dst;
-                if (relu) v = v > (T)0 ? v : (T)0;
+                if (relu) v = (v > (T)0 || v != v) ? v : (T)0;  // np.maximum(v, 0): NaN propagates
                 *dst = v;
             }
         }
@@ -174,7 +174,7 @@ __global__ void loss_kernel(const T *__restrict__ pred, const T *__restrict__ ta
         double g;
         if (kind == 0) {
             s = fabs(d);
-            double sg = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0);
+            double sg = d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : (d == d ? 0.0 : d));  // np.sign: NaN -> NaN
             g = __ddiv_rn(sg, denom);
         } else {
             s = __dmul_rn(d, d);
@@ -303,33 +303,53 @@ __global__ void __launch_bounds__(256) adam_vec_kernel(float *__restrict__ p, fl
 // Training-pipeline Adam step: adam_flat_kernel's update plus the step's bookkeeping in the last block to
 // finish (ticket): losses[t - t0] = loss_sum / B, loss_sum = 0, t += 1.  Every
 // block reads t before taking its ticket, so the advance cannot race a reader.
+// NaN contract (common.cuh, nan_state): only q < nan_state[0] is updated (the
+// parameter groups in front of the first one holding a NaN gradient,
+// network.py:167-171); a NaN this kernel meets itself is left in place and
+// lowers the limit.  When the limit is set the last block halts the pipeline
+// instead of recording the loss / advancing t; a halted pipeline's Adam is a no-op.
 __global__ void __launch_bounds__(256) adam_step_kernel(
     float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v, int64_t n,
     const float *__restrict__ sched, int64_t sched_len, int64_t *__restrict__ step_counter, float b1, float omb1,
-    float b2, float omb2, float eps, float l2, uint32_t *__restrict__ nan_flag, double *__restrict__ loss_acc,
+    float b2, float omb2, float eps, float l2, int64_t *__restrict__ nan_state, double *__restrict__ loss_acc,
     double *__restrict__ losses, int64_t t0, int64_t cap, double inv_b, uint32_t *__restrict__ ticket) {
+    if (nan_halted(nan_state)) return;
     const int64_t tc = *step_counter;
     const int64_t t = tc >= sched_len ? sched_len - 1 : tc;
     const float lr = sched[3 * t], c1 = sched[3 * t + 1], c2 = sched[3 * t + 2];
+    const int64_t lim = nan_limit(nan_state);
     // scalar head up to the next 128-byte boundary: each warp's float4 accesses then cover whole lines
     const int64_t head = min(n, (int64_t)(((128 - (reinterpret_cast<uintptr_t>(p) & 127)) & 127) >> 2));
     const int64_t n4 = (n - head) >> 2;
-    bool bad = false;
+    int64_t bad = kNanNone;
     float4 *p4 = reinterpret_cast<float4 *>(p + head), *g4 = reinterpret_cast<float4 *>(g + head);
     float4 *m4 = reinterpret_cast<float4 *>(m + head), *v4 = reinterpret_cast<float4 *>(v + head);
     const uint64_t keep = l2_evict_last();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    auto upd = [&](float4 &P, float4 &G, float4 &M, float4 &V) {
-        bad |= isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w);
-        adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-        adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-        adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-        adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+    // one element under the limit; a NaN gradient the detectors upstream did not see stays unapplied
+    auto one = [&](float &P, float &G, float &M, float &V, int64_t q) {
+        if (q >= lim) return;
+        if (isnan(G)) {
+            bad = min(bad, q);
+            return;
+        }
+        adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
     };
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; j < n4; j += stride) {
         float4 P = __ldcs(p4 + j), G = ld4_hint(g4 + j, keep), M = __ldcs(m4 + j), V = __ldcs(v4 + j);
-        upd(P, G, M, V);
+        const int64_t q = head + 4 * j;
+        if (q + 3 < lim && !(isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w))) {
+            adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+            adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+            adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+            adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        } else {
+            one(P.x, G.x, M.x, V.x, q);
+            one(P.y, G.y, M.y, V.y, q + 1);
+            one(P.z, G.z, M.z, V.z, q + 2);
+            one(P.w, G.w, M.w, V.w, q + 3);
+        }
         __stcs(p4 + j, P);
         st4_hint(g4 + j, G, keep);
         __stcs(m4 + j, M);
@@ -338,25 +358,51 @@ __global__ void __launch_bounds__(256) adam_step_kernel(
     for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < head + (n - head - 4 * n4); jj += stride) {
         const int64_t q = jj < head ? jj : head + 4 * n4 + (jj - head);  // head then tail elements
         float P = p[q], G = g[q], M = m[q], V = v[q];
-        bad |= isnan(G);
-        adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        one(P, G, M, V, q);
         p[q] = P;
         g[q] = G;
         m[q] = M;
         v[q] = V;
     }
-    if (nan_flag && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nan_flag, 1u);
+    if (bad != kNanNone) nan_mark(nan_state, bad);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
             __threadfence();
+            *ticket = 0u;
+            if (nan_limit(nan_state) != kNanNone) {
+                nan_state[1] = 1;  // halt: the step is not recorded, t does not advance
+                return;
+            }
             const int64_t k = tc - t0;
             if (losses && k >= 0 && k < cap) losses[k] = *reinterpret_cast<volatile double *>(loss_acc) * inv_b;
             if (loss_acc) *loss_acc = 0.0;
             *step_counter = tc + 1;
-            *ticket = 0u;
         }
+    }
+}
+
+// SIMT training engine's NaN detector (the tcgen05 engine detects in its MLP
+// kernel): marks the start of every parameter group whose gradient holds a NaN.
+struct GroupStarts {
+    int64_t start[16];
+    int n;
+};
+__global__ void nan_scan_kernel(const float *__restrict__ g, int64_t n, const GroupStarts gs,
+                                int64_t *__restrict__ nan_state) {
+    if (nan_halted(nan_state)) return;
+    int64_t first = kNanNone;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        if (isnan(g[j])) {
+            first = min(first, j);
+            break;
+        }
+    if (first != kNanNone) {
+        int64_t st = 0;
+        for (int i = 0; i < gs.n; ++i)
+            if (gs.start[i] <= first) st = gs.start[i];
+        nan_mark(nan_state, st);
     }
 }
 
@@ -448,7 +494,7 @@ int nvol_loss_and_grad(const void *pred, const void *target, int64_t b, int32_t 
 
 int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, const float *sched, int64_t sched_len,
                          int64_t *step_counter, float beta1, float one_minus_beta1, float beta2,
-                         float one_minus_beta2, float eps, float l2, uint32_t *nan_flag, double *loss_acc,
+                         float one_minus_beta2, float eps, float l2, int64_t *nan_state, double *loss_acc,
                          double *losses, int64_t t0, int64_t cap, double inv_b, uint32_t *ticket, void *stream) {
     NVOL_REQUIRE(p && g && m && v && sched && step_counter && ticket && sched_len >= 1, "null pointer");
     NVOL_REQUIRE(((uintptr_t)p & 127) == ((uintptr_t)g & 127) && ((uintptr_t)p & 127) == ((uintptr_t)m & 127) &&
@@ -456,8 +502,18 @@ int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, cons
                  "flat Adam buffers must share their alignment modulo 128 bytes");
     adam_step_kernel<<<stream_grid((n + 3) / 4), 256, 0, as_stream(stream)>>>(
         p, g, m, v, n, sched, sched_len, step_counter, beta1, one_minus_beta1, beta2, one_minus_beta2, eps, l2,
-        nan_flag, loss_acc, losses, t0, cap, inv_b, ticket);
+        nan_state, loss_acc, losses, t0, cap, inv_b, ticket);
     return check_launch("adam_train_step");
+}
+
+int nvol_nan_scan(const float *g, int64_t n, const int64_t *group_starts, int32_t n_groups, int64_t *nan_state,
+                  void *stream) {
+    NVOL_REQUIRE(g && group_starts && nan_state && n_groups >= 1 && n_groups <= 16, "bad arguments");
+    GroupStarts gs;
+    gs.n = n_groups;
+    for (int i = 0; i < n_groups; ++i) gs.start[i] = group_starts[i];
+    nan_scan_kernel<<<stream_grid(n), 256, 0, as_stream(stream)>>>(g, n, gs, nan_state);
+    return check_launch("nan_scan");
 }
 
 int nvol_loss_record(double *acc, double *losses, const int64_t *step_counter, int64_t t0, int64_t cap,

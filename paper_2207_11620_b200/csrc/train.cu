@@ -38,7 +38,8 @@ static int64_t ws_simt(int64_t b, int m, int n, int nn, int nh) {
 
 int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_t b_global, const float *params,
                     float *grads, const GridTables &tab, int nn, int nh, int relu_out, int loss_kind,
-                    double *loss_sum, void *workspace, int64_t ws_bytes, int flags, cudaStream_t s);
+                    double *loss_sum, void *workspace, int64_t ws_bytes, int flags, int64_t *nan_state,
+                    cudaStream_t s);
 int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh);
 
 }  // namespace nvol
@@ -52,6 +53,7 @@ int nvol_loss_and_grad_scaled(const void *, const void *, int64_t, int64_t, int3
 int nvol_mlp_forward(int64_t, int32_t, const int32_t *, const void *const *, void *const *, int32_t, int32_t, void *);
 int nvol_mlp_backward(int64_t, int32_t, const int32_t *, const void *const *, const void *const *, const void *,
                       void *const *, void *, void *, void *, int32_t, int32_t, void *);
+int nvol_nan_scan(const float *, int64_t, const int64_t *, int32_t, int64_t *, void *);
 
 int64_t nvol_train_workspace_bytes(int64_t b, int32_t n_levels, int32_t n_feat, int32_t n_neurons, int32_t n_hidden,
                                    int32_t mode) {
@@ -63,7 +65,8 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
                        float *grads, const int64_t *level_off, const int64_t *level_res,
                        const int64_t *level_entries, const uint8_t *level_dense, int32_t n_levels, int32_t n_feat,
                        int32_t n_neurons, int32_t n_hidden, int32_t relu_out, int32_t loss_kind, double *loss_sum,
-                       void *workspace, int64_t workspace_bytes, int32_t mode, void *stream) {
+                       void *workspace, int64_t workspace_bytes, int32_t mode, int64_t *nan_state,
+                       void *stream) {
     GridTables tab;
     int st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
     if (st) return st;
@@ -79,7 +82,7 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
     cudaStream_t s = as_stream(stream);
     if (mode == 1)
         return train_tc_launch(coords, targets, b, b_global, params, grads, tab, n_neurons, n_hidden, relu_out,
-                               loss_kind, loss_sum, workspace, workspace_bytes, flags, s);
+                               loss_kind, loss_sum, workspace, workspace_bytes, flags, nan_state, s);
     const int m = n_levels, n = n_feat, nn = n_neurons, nh = n_hidden;
     const int nl = nh + 1;
     Ws w{(char *)workspace, 0};
@@ -104,7 +107,10 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
     int64_t off = 0;
     for (int l = 0; l < m; ++l) off = max(off, tab.offset[l] + tab.entries[l] * n);
     off = flat_weight_offset(params, off);  // W_0 starts 16-byte aligned (see nvol.h, flat layout)
+    int64_t starts[16];  // parameter-group starts in the flat buffer (encoder, W_0, ...)
+    starts[0] = 0;
     for (int i = 0; i < nl; ++i) {
+        if (i + 1 < 16) starts[i + 1] = off;
         wptr[i] = params + off;
         gptr[i] = grads + off;
         off += (int64_t)widths[i] * widths[i + 1];
@@ -121,6 +127,7 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
     if (st) return st;
     st = nvol_grid_encode_bwd_coords(coords, dfeat, b, level_off, level_res, level_entries, level_dense, m, n,
                                      grads, 4, g_deterministic, stream);
+    if (st == NVOL_OK && nan_state) st = nvol_nan_scan(grads, off, starts, nl + 1 < 16 ? nl + 1 : 16, nan_state, stream);
     (void)s;
     return st;
 }

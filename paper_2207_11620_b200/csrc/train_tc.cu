@@ -175,7 +175,7 @@ __device__ __forceinline__ float2 ld_na2(const float2 *p) {
 template <int NF, bool COHERENT>
 __device__ __forceinline__ void encode_item(const float *__restrict__ coords, const float *__restrict__ params,
                                             const GridTables &tab, int ninp, uint8_t *__restrict__ xtiles, int l,
-                                            int64_t i) {
+                                            int64_t i, float *__restrict__ dbg_feat = nullptr) {
     const int m = tab.n_levels;
     const int32_t res = tab.res[l];
     const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
@@ -227,6 +227,10 @@ __device__ __forceinline__ void encode_item(const float *__restrict__ coords, co
             for (int f = 0; f < NF; ++f) acc[f] = xadd(acc[f], xmul(w, tab_ld<COHERENT>(tb + (size_t)sl[k] * NF + f)));
         }
     }
+    if (dbg_feat) {  // parity hook (nvol_train_tc_debug): the fp32 features, sample-major [b][m*NF]
+#pragma unroll
+        for (int f = 0; f < NF; ++f) dbg_feat[i * (m * NF) + l * NF + f] = acc[f];
+    }
     const int64_t tile = i >> 7;
     const int s = (int)(i & 127);
     // per tile: fp16 hi tile followed by the fp16 lo tile (split-fp16 forward)
@@ -257,13 +261,15 @@ __device__ __forceinline__ void encode_item(const float *__restrict__ coords, co
 template <int NF>
 __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restrict__ coords, int64_t b,
                                                            const float *__restrict__ params, const GridTables tab,
-                                                           int ninp, uint8_t *__restrict__ xtiles) {
+                                                           int ninp, uint8_t *__restrict__ xtiles,
+                                                           float *__restrict__ dbg_feat,
+                                                           const int64_t *__restrict__ nan_state) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= b * tab.n_levels) return;
+    if (t >= b * tab.n_levels || nan_halted(nan_state)) return;
     // level-major: a warp covers 32 consecutive samples of one level (uniform
     // level constants, coalesced coordinates, L1 reuse on coarse levels)
     const int l = (int)(t / b);
-    encode_item<NF, false>(coords, params, tab, ninp, xtiles, l, t - (int64_t)l * b);
+    encode_item<NF, false>(coords, params, tab, ninp, xtiles, l, t - (int64_t)l * b, dbg_feat);
 }
 
 // ---------------------------------------------------------------------------- Adam(k) + encode(k+1)
@@ -287,7 +293,7 @@ struct AdamArgs {
     int64_t sched_len;
     int64_t *counter;
     float b1, omb1, b2, omb2, eps, l2;
-    uint32_t *nan_flag;
+    int64_t *nan_state;
     double *loss_acc, *losses;
     int64_t t0, cap;
     double inv_b;
@@ -328,10 +334,21 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__device__ __forceinline__ void adam_scalar(const AdamArgs &a, int64_t q, float lr, float c1, float c2, bool &bad) {
-    float P = a.p[q], G = a.g[q], M = a.m[q], V = a.v[q];
-    bad |= isnan(G);
+// one parameter under the NaN contract (common.cuh): only q < lim, a NaN gradient stays unapplied
+__device__ __forceinline__ void adam_lim(const AdamArgs &a, float &P, float &G, float &M, float &V, int64_t q,
+                                         int64_t lim, float lr, float c1, float c2, int64_t &bad) {
+    if (q >= lim) return;
+    if (isnan(G)) {
+        bad = min(bad, q);
+        return;
+    }
     adam_one<float>(P, G, M, V, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+}
+
+__device__ __forceinline__ void adam_scalar(const AdamArgs &a, int64_t q, float lr, float c1, float c2, int64_t lim,
+                                            int64_t &bad) {
+    float P = a.p[q], G = a.g[q], M = a.m[q], V = a.v[q];
+    adam_lim(a, P, G, M, V, q, lim, lr, c1, c2, bad);
     a.p[q] = P;
     a.g[q] = G;
     a.m[q] = M;
@@ -348,7 +365,9 @@ __global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, 
                                                                     uint32_t *__restrict__ work) {
     __shared__ float4 ring[AE_D][4][AE_ADAM_WARPS * 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (nan_halted(a.nan_state)) return;
     const int64_t tc = *a.counter;
+    const int64_t lim = nan_limit(a.nan_state);
     const int m = tab.n_levels;
     if (warp < AE_ADAM_WARPS) {
         const int64_t t = tc >= a.sched_len ? a.sched_len - 1 : tc;
@@ -357,7 +376,7 @@ __global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, 
         float4 *m4 = reinterpret_cast<float4 *>(a.m + head), *v4 = reinterpret_cast<float4 *>(a.v + head);
         const uint64_t keep = l2_evict_last();
         const int64_t ntail = a.n - head - 4 * n4;
-        bool bad = false;
+        int64_t bad = kNanNone;
         auto dequeue = [&]() -> int64_t {
             uint32_t c = 0;
             if (lane == 0) c = atomicAdd(work, 1u);
@@ -390,11 +409,18 @@ __global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, 
             const int64_t j = cc * AE_WARP_F4 + cu * 32 + lane;
             if (j < n4) {
                 float4 P = ring[slot][0][tid], G = ring[slot][1][tid], M = ring[slot][2][tid], V = ring[slot][3][tid];
-                bad |= isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w);
-                adam_one<float>(P.x, G.x, M.x, V.x, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
-                adam_one<float>(P.y, G.y, M.y, V.y, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
-                adam_one<float>(P.z, G.z, M.z, V.z, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
-                adam_one<float>(P.w, G.w, M.w, V.w, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                const int64_t q = head + 4 * j;
+                if (q + 3 < lim && !(isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w))) {
+                    adam_one<float>(P.x, G.x, M.x, V.x, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                    adam_one<float>(P.y, G.y, M.y, V.y, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                    adam_one<float>(P.z, G.z, M.z, V.z, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                    adam_one<float>(P.w, G.w, M.w, V.w, lr, a.b1, a.omb1, a.b2, a.omb2, c1, c2, a.eps, a.l2);
+                } else {
+                    adam_lim(a, P.x, G.x, M.x, V.x, q, lim, lr, c1, c2, bad);
+                    adam_lim(a, P.y, G.y, M.y, V.y, q + 1, lim, lr, c1, c2, bad);
+                    adam_lim(a, P.z, G.z, M.z, V.z, q + 2, lim, lr, c1, c2, bad);
+                    adam_lim(a, P.w, G.w, M.w, V.w, q + 3, lim, lr, c1, c2, bad);
+                }
                 p4[j] = P;                    // default policy: the encoder warps gather it next
                 st4_hint(g4 + j, G, keep);    // the zeroed gradient stays in L2 for the next scatter
                 __stcs(m4 + j, M);
@@ -404,8 +430,8 @@ __global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, 
             slot = slot + 1 == AE_D ? 0 : slot + 1;
             if (++cu == AE_CHUNK_U) {
                 // chunk done: scalar head (chunk 0) / tail (last chunk), then publish
-                if (cc == 0 && lane < head) adam_scalar(a, lane, lr, c1, c2, bad);
-                if (cc == nch - 1 && lane < ntail) adam_scalar(a, head + 4 * n4 + lane, lr, c1, c2, bad);
+                if (cc == 0 && lane < head) adam_scalar(a, lane, lr, c1, c2, lim, bad);
+                if (cc == nch - 1 && lane < ntail) adam_scalar(a, head + 4 * n4 + lane, lr, c1, c2, lim, bad);
                 __threadfence();
                 __syncwarp();
                 if (lane < m && lc.lo[lane] <= cc && cc <= lc.hi[lane]) atomicAdd(work + 2 + lane, 1u);
@@ -414,7 +440,7 @@ __global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, 
             }
         }
         cp_async_wait<0>();
-        if (a.nan_flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nan_flag, 1u);
+        if (bad != kNanNone) nan_mark(a.nan_state, bad);
     } else {
         const int64_t nblk = (b + 31) >> 5;
         const int64_t n_enc = (int64_t)gridDim.x * AE_ENC_WARPS;
@@ -447,10 +473,15 @@ __global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, 
         __threadfence();
         if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
             __threadfence();
-            const int64_t k = tc - a.t0;
-            if (a.losses && k >= 0 && k < a.cap) a.losses[k] = *reinterpret_cast<volatile double *>(a.loss_acc) * a.inv_b;
-            if (a.loss_acc) *a.loss_acc = 0.0;
-            *a.counter = tc + 1;
+            if (nan_limit(a.nan_state) != kNanNone) {
+                a.nan_state[1] = 1;  // halt (NaN contract): no loss record, t does not advance
+            } else {
+                const int64_t k = tc - a.t0;
+                if (a.losses && k >= 0 && k < a.cap)
+                    a.losses[k] = *reinterpret_cast<volatile double *>(a.loss_acc) * a.inv_b;
+                if (a.loss_acc) *a.loss_acc = 0.0;
+                *a.counter = tc + 1;
+            }
             for (int l = 0; l < m; ++l) work[2 + l] = 0u;
             work[0] = 0u;
             work[1] = 0u;
@@ -467,6 +498,10 @@ __device__ __forceinline__ void group_cols(int w, int h, int ng, int &c0, int &n
     c0 = k0 * 16;
     nc = k1 > k0 ? (k1 - k0) * 16 : 0;
 }
+
+// ReLU with numpy's NaN semantics (np.maximum(x, 0) propagates NaN; fmaxf would swallow it),
+// so a NaN parameter reaches the gradients as in the reference and trips the NaN contract
+__device__ __forceinline__ float relu_nan(float x) { return (x > 0.0f || x != x) ? x : 0.0f; }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
@@ -567,7 +602,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
     const uint8_t *__restrict__ xtiles, const float *__restrict__ targets, int64_t b, double inv_bglobal, float dscale,
     const TcShape sh, const float *__restrict__ wflat, double *__restrict__ loss_sum, float *__restrict__ dfeat,
-    int64_t stride, float *__restrict__ dw_grads) {
+    int64_t stride, float *__restrict__ dw_grads, float *__restrict__ dbg_pred, int64_t *__restrict__ nan_state,
+    int64_t woff) {
+    if (nan_halted(nan_state)) return;  // NaN contract: a halted pipeline does no more work
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar_x[2], bar_xr[2], bar_acc[2], bar_op[2], bar_w, bar_dwo;
     __shared__ uint32_t tmem_base_sh;
@@ -576,6 +613,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
     const int NN = sh.nn, NINP = sh.ninp, NH = sh.nh, NIN = sh.nin;
     const int64_t ntiles = (b + TILE - 1) / TILE;
     const int64_t xtile_bytes = 2 * (int64_t)sh.xhalf;
+    int64_t nan_at = kNanNone;  // NaN contract: start of the first parameter group this thread saw a NaN gradient in
 
     // ---- prologue: fp32 weights staged by one bulk copy, packed to fp16 hi/lo tiles
     float *stage = reinterpret_cast<float *>(smem + sh.o_d[0]);
@@ -822,7 +860,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                 tc::tmem_wait_ld();
                 auto chunk = [&](float(&v)[16], int c) {
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) v[e] = fmaxf(v[e] + vl[e] * (1.0f / tc::kLoScale), 0.0f);
+                    for (int e = 0; e < 16; ++e) v[e] = relu_nan(v[e] + vl[e] * (1.0f / tc::kLoScale));
                     store_row_f16(dst, s, c, NN, v, false);
                     if (!last) {
 #pragma unroll
@@ -845,18 +883,19 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
             s_part[hh * TILE + s] = outp;
             named_sync(1 + t, 256);
             const float o = (s_part[s] + s_part[TILE + s]) * (1.0f / tc::kActScale);
-            const float pred = sh.relu_out ? fmaxf(o, 0.0f) : o;
+            const float pred = sh.relu_out ? relu_nan(o) : o;
+            if (dbg_pred && valid && hh == 0) dbg_pred[row] = pred;  // parity hook (nvol_train_tc_debug)
             const double d = (double)pred - (double)tgt;
             double g, sl;
             if (sh.loss_kind == 0) {
                 sl = fabs(d);
-                g = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_bglobal;
+                g = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : (d == d ? 0.0 : d))) * inv_bglobal;  // np.sign(NaN) = NaN
             } else {
                 sl = d * d;
                 g = 2.0 * d * inv_bglobal;
             }
             float gf = (float)g;
-            if (sh.relu_out && !(pred > 0.0f)) gf = 0.0f;
+            if (sh.relu_out && !(pred > 0.0f)) gf *= 0.0f;  // d * (act > 0): a NaN d stays NaN (numpy)
             if (!valid) {
                 gf = 0.0f;
                 sl = 0.0;
@@ -874,7 +913,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                         float hv[16], dv[16];
                         load_row_f16(lbuf, s, c, NN, hv);
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) dv[e] = hv[e] > 0.0f ? gd * s_wout[c + e] : 0.0f;
+                        for (int e = 0; e < 16; ++e) dv[e] = hv[e] > 0.0f ? gd * s_wout[c + e] : gd * s_wout[c + e] * 0.0f;
                         store_row_f16(dbuf, s, c, NN, dv, false);
                     }
                 }
@@ -908,7 +947,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                         load_row_f16(hj, s, c, NN, hv);
                         if (ch == 0) tc::tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) v[ch][e] = hv[e] > 0.0f ? v[ch][e] : 0.0f;
+                        for (int e = 0; e < 16; ++e) v[ch][e] = hv[e] > 0.0f ? v[ch][e] : v[ch][e] * 0.0f;
                         store_row_f16(dbuf, s, c, NN, v[ch], false);
                     }
                 } else {
@@ -925,7 +964,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                             // feature-major dL/dfeat [NIN][B]: a warp stores 32 consecutive rows per column
 #pragma unroll
                             for (int e = 0; e < 16; ++e)
-                                if (c + e < NIN) dfeat[(int64_t)(c + e) * stride + row] = v[e] * (1.0f / dscale);
+                                if (c + e < NIN) {
+                                    const float dv = v[e] * (1.0f / dscale);
+                                    if (isnan(dv)) nan_at = 0;  // the encoder group (group 0) gets a NaN gradient
+                                    dfeat[(int64_t)(c + e) * stride + row] = dv;
+                                }
                         }
                     }
                 }
@@ -963,6 +1006,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
                     tc::tmem_ld16(tmem + lane_base + sh.t_dw[j] + c, v);
                     tc::tmem_wait_ld();
                     if (o < NN) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if (c + e < win && isnan(v[e])) nan_at = min(nan_at, woff + base);  // W_j's group
                         float *g = dw_grads + base + (int64_t)o * win + c;
                         if (c + 16 <= win && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
 #pragma unroll
@@ -984,9 +1030,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
             float v[16];
             tc::tmem_ld16(tmem + lane_base + sh.t_dwout, v);  // columns 0..15 (8 allocated + neighbours; only 0 used)
             tc::tmem_wait_ld();
-            if (o < NN) atomicAdd(dw_grads + base + o, v[0] * unscale);
+            if (o < NN) {
+                if (isnan(v[0])) nan_at = min(nan_at, woff + base);
+                atomicAdd(dw_grads + base + o, v[0] * unscale);
+            }
         }
     }
+    if (nan_at != kNanNone) nan_mark(nan_state, nan_at);
     tc::fence_before();
     __syncthreads();
 #ifdef NVOL_TIMELINE
@@ -1001,7 +1051,9 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
                                                                 const float *__restrict__ dfeat, int64_t b,
                                                                 int64_t stride,
                                                                 const GridTables tab, int n_coarse, int coarse_floats,
-                                                                float *__restrict__ grads) {
+                                                                float *__restrict__ grads,
+                                                                const int64_t *__restrict__ nan_state) {
+    if (nan_halted(nan_state)) return;
     extern __shared__ float acc_s[];
     const uint64_t keep = l2_evict_last();
     for (int q = threadIdx.x; q < coarse_floats; q += SC_THREADS) acc_s[q] = 0.0f;
@@ -1177,6 +1229,13 @@ int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
 }
 
 static cudaEvent_t g_stage_events[8];
+// Parity hooks (nvol_train_tc_debug): the hot kernels additionally write the fp32 features
+// (encode_tiles_kernel), the per-sample prediction (mlp_tc_kernel) and a copy of the
+// feature-major dL/dfeat; all null in production.
+struct TcDebug {
+    float *feat = nullptr, *pred = nullptr, *dfeat = nullptr;
+};
+static TcDebug g_dbg;
 static int g_stage_events_n = 0;
 
 struct SideStreams {
@@ -1202,7 +1261,8 @@ static SideStreams &side_streams() {
 
 int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_t b_global, const float *params,
                     float *grads, const GridTables &tab, int nn, int nh, int relu_out, int loss_kind,
-                    double *loss_sum, void *workspace, int64_t ws_bytes, int flags, cudaStream_t s) {
+                    double *loss_sum, void *workspace, int64_t ws_bytes, int flags, int64_t *nan_state,
+                    cudaStream_t s) {
     TcPlan p;
     if (!make_plan(p, b, tab, nn, nh, relu_out, loss_kind)) {
         set_error("MLP / grid shape not supported by the tcgen05 path");
@@ -1249,14 +1309,15 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         const unsigned egrid = grid_for(nb * tab.n_levels, 256);
         uint8_t *xtc = xt + t0 * tile_bytes;
         const float *cc = coords + 3 * r0;
+        float *dfe = g_dbg.feat ? g_dbg.feat + r0 * (int64_t)tab.n_levels * tab.n_feat : nullptr;
         if (!pre) {
             if (nb % TILE)  // rows past the batch must be zero (0 x garbage could be NaN in dW)
                 cudaMemsetAsync(xtc + (nb / TILE) * tile_bytes, 0, (size_t)tile_bytes, se);
             switch (tab.n_feat) {
-                case 1: encode_tiles_kernel<1><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
-                case 2: encode_tiles_kernel<2><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
-                case 4: encode_tiles_kernel<4><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
-                default: encode_tiles_kernel<8><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc); break;
+                case 1: encode_tiles_kernel<1><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, dfe, nan_state); break;
+                case 2: encode_tiles_kernel<2><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, dfe, nan_state); break;
+                case 4: encode_tiles_kernel<4><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, dfe, nan_state); break;
+                default: encode_tiles_kernel<8><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, dfe, nan_state); break;
             }
             st = check_launch("encode_tiles_kernel");
             if (st) return st;
@@ -1270,9 +1331,13 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         const int64_t ct = (nb + TILE - 1) / TILE;
         const int gm = (int)(ct < p.grid_mlp ? ct : p.grid_mlp);
         mlp_tc_kernel<<<gm, PP_THREADS, p.sh.smem_bytes, s>>>(xtc, targets + r0, nb, 1.0 / (double)b_global, dscale,
-                                                              p.sh, params + woff, loss_sum, dfeat + r0, b, grads + woff);
+                                                              p.sh, params + woff, loss_sum, dfeat + r0, b, grads + woff,
+                                                              g_dbg.pred ? g_dbg.pred + r0 : nullptr, nan_state, woff);
         st = check_launch("mlp_tc_kernel");
         if (st) return st;
+        if (g_dbg.dfeat)
+            cudaMemcpy2DAsync(g_dbg.dfeat + r0, (size_t)b * 4, dfeat + r0, (size_t)b * 4, (size_t)nb * 4,
+                              (size_t)p.sh.nin, cudaMemcpyDeviceToDevice, s);
         if (nc > 1) {
             cudaEventRecord(ss.mlp_done[c], s);
             cudaStreamWaitEvent(sc, ss.mlp_done[c], 0);
@@ -1282,7 +1347,7 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
 #define LAUNCH_SC(NFV)                                                                                             \
     case NFV:                                                                                                      \
         scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, sc>>>(cc, dfeat + r0, nb, b, tab, p.n_coarse,            \
-                                                                p.coarse_floats, grads);                       \
+                                                                p.coarse_floats, grads, nan_state);            \
         break;
             LAUNCH_SC(1)
             LAUNCH_SC(2)
@@ -1323,6 +1388,50 @@ extern "C" int nvol_debug_timeline(unsigned long long *host, int32_t n) {
 }
 #endif
 
+extern "C" int nvol_train_tc_debug(float *feat, float *pred, float *dfeat) {
+    nvol::g_dbg.feat = feat;
+    nvol::g_dbg.pred = pred;
+    nvol::g_dbg.dfeat = dfeat;
+    return NVOL_OK;
+}
+
+// The training step's encoder-backward kernel (scatter_kernel) on its own, fed a
+// caller-provided feature-major dL/dfeat [n_levels*n_feat][stride] -- exactly the
+// launch nvol_train_fwd_bwd (mode 1) makes after the MLP.
+extern "C" int nvol_train_tc_scatter(const float *coords, const float *dfeat, int64_t b, int64_t stride,
+                                     const int64_t *level_off, const int64_t *level_res,
+                                     const int64_t *level_entries, const uint8_t *level_dense, int32_t n_levels,
+                                     int32_t n_feat, float *grads, void *stream) {
+    using namespace nvol;
+    NVOL_REQUIRE(coords && dfeat && grads && b >= 1 && stride >= b, "bad arguments");
+    GridTables tab;
+    int st = pack_tables(tab, level_off, level_res, level_entries, level_dense, n_levels, n_feat);
+    if (st) return st;
+    TcPlan p;
+    // the scatter's coarse-level plan does not depend on the MLP shape: any supported one
+    if (!make_plan(p, b, tab, 64, 1, 1, 0) && !make_plan(p, b, tab, 16, 1, 1, 0)) {
+        set_error("grid shape not supported by the tcgen05 path");
+        return NVOL_EINVAL;
+    }
+    const size_t csm = (size_t)p.coarse_floats * 4;
+    cudaStream_t s = as_stream(stream);
+    switch (n_feat) {
+#define LAUNCH_SC1(NFV)                                                                                          \
+    case NFV:                                                                                                    \
+        cudaFuncSetAttribute(scatter_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);        \
+        scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, s>>>(coords, dfeat, b, stride, tab, p.n_coarse,      \
+                                                               p.coarse_floats, grads, nullptr);                \
+        break;
+        LAUNCH_SC1(1)
+        LAUNCH_SC1(2)
+        LAUNCH_SC1(4)
+        LAUNCH_SC1(8)
+#undef LAUNCH_SC1
+        default: set_error("n_feat must be 1, 2, 4 or 8"); return NVOL_EINVAL;
+    }
+    return check_launch("scatter_kernel");
+}
+
 extern "C" int64_t nvol_l2_persist(int64_t bytes) {
     int dev = 0, maxp = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return -1;
@@ -1356,7 +1465,7 @@ extern "C" int nvol_has_tcgen05(int device) {
 // nvol_train_fwd_bwd(mode 1 | NVOL_TRAIN_PREENCODED) skips its encode kernel.
 extern "C" int nvol_adam_encode_step(float *p, float *g, float *m, float *v, int64_t n, const float *sched,
                                      int64_t sched_len, int64_t *step_counter, float beta1, float one_minus_beta1,
-                                     float beta2, float one_minus_beta2, float eps, float l2, uint32_t *nan_flag,
+                                     float beta2, float one_minus_beta2, float eps, float l2, int64_t *nan_state,
                                      double *loss_acc, double *losses, int64_t t0, int64_t cap, double inv_b,
                                      uint32_t *work, const float *next_coords, int64_t b, const int64_t *level_off,
                                      const int64_t *level_res, const int64_t *level_entries,
@@ -1384,7 +1493,7 @@ extern "C" int nvol_adam_encode_step(float *p, float *g, float *m, float *v, int
     const int64_t tile_bytes = 2 * TILE * pl.sh.ninp * 2;
     if (b % TILE) cudaMemsetAsync(xt + (b / TILE) * tile_bytes, 0, (size_t)tile_bytes, s);
     AdamArgs a{p,    g,    m,    v,        n,        sched,  sched_len, step_counter, beta1, one_minus_beta1,
-               beta2, one_minus_beta2, eps, l2, nan_flag, loss_acc, losses, t0, cap, inv_b};
+               beta2, one_minus_beta2, eps, l2, nan_state, loss_acc, losses, t0, cap, inv_b};
     // flat layout: scalar head up to the next 128-byte boundary, float4 body in warp chunks, scalar tail
     const int64_t head = std::min(n, (int64_t)(((128 - ((uintptr_t)p & 127)) & 127) >> 2));
     const int64_t n4 = (n - head) >> 2;

@@ -38,6 +38,7 @@ _ENCODER_OTYPES = {
 _ENCODER_KIND_TO_OTYPE = {v: k for k, v in _ENCODER_OTYPES.items()}
 
 # Training-step engines (nvol_train_fwd_bwd `mode`).
+NAN_NONE = (1 << 63) - 1   # nvol.h NaN contract: no parameter group holds a NaN gradient
 MODE_SIMT = 0      # generic kernels, fp32 CUDA cores
 MODE_TCGEN05 = 1   # fused tile pipeline, tcgen05 fp16 operands / fp32 accumulate
 TRAIN_PREENCODED = 16   # mode flag, nvol.h NVOL_TRAIN_PREENCODED
@@ -128,7 +129,6 @@ class NeuralModel:
             raise ConfigError(f"unknown loss otype {self.loss_kind!r}; expected 'L1' or 'L2'")
         self.train_mode = MODE_SIMT
         self.infer_mode = "exact"        # eval_fused / eval_batch / decode: "exact" or "tensor"
-        self.strict_nan = False           # True: reference NaN semantics (find_nan before Adam, +1 sync)
         self._pack()
         self._ws = None
         self._stage = None
@@ -262,10 +262,12 @@ class NeuralModel:
         return self._ws
 
     def fwd_bwd_device(self, coords: torch.Tensor, targets: torch.Tensor, loss_sum: torch.Tensor,
-                       b_global: Optional[int] = None, flags: int = 0) -> None:
+                       b_global: Optional[int] = None, flags: int = 0,
+                       nan_state: Optional[torch.Tensor] = None) -> None:
         """Encode -> MLP -> loss -> backprop -> encoder scatter into flat_grads (no Adam).
         flags (tcgen05 engine): TRAIN_PREENCODED skips the encode (the tile buffer was
-        filled by nvol_adam_encode_step), TRAIN_ENCODE_ONLY stops after it."""
+        filled by nvol_adam_encode_step), TRAIN_ENCODE_ONLY stops after it.  nan_state
+        (int64[2], nvol.h "NaN contract"): NaN-gradient detection and halt."""
         b = coords.shape[0]
         c = self.encoder.config
         ws = self._workspace(b)
@@ -274,7 +276,8 @@ class NeuralModel:
                   _lib.ptr(self.flat_params), _lib.ptr(self.flat_grads), off, res, ent, dense, c.n_levels,
                   c.n_features_per_level, self.mlp.config.n_neurons, self.mlp.config.n_hidden_layers,
                   int(self.mlp.config.output_activation == "relu"), 0 if self.loss_kind == "L1" else 1,
-                  _lib.ptr(loss_sum), _lib.ptr(ws), ws.numel(), self._engine() | flags, _lib.stream())
+                  _lib.ptr(loss_sum), _lib.ptr(ws), ws.numel(), self._engine() | flags, _lib.ptr(nan_state),
+                  _lib.stream())
 
     def _tc_device(self) -> bool:
         try:
@@ -296,25 +299,55 @@ class NeuralModel:
         from .encoding import deterministic
         return MODE_SIMT if deterministic() else self.train_mode
 
-    def adam_device(self, nan_flag: Optional[torch.Tensor] = None) -> None:
-        """One flat Adam step (network.py:160-183) with host-cast scalars; advances opt.t."""
-        if self.strict_nan:
-            first = torch.empty(1, dtype=torch.int64, device=self.flat_grads.device)
-            for gi, g in enumerate(self.param_groups()[1]):
-                _lib.call("nvol_find_nan", _lib.ptr(g), g.numel(), _lib.ptr(first), 4, _lib.stream())
-                j = int(first.item())
-                if j >= 0:
-                    raise FloatingPointError(f"NaN gradient in parameter group {gi} at flat index {j}")
+    # ---------------------------------------------------------------- NaN contract
+    def group_starts(self) -> list:
+        """Flat-buffer start of each parameter group [enc.params, W_0, W_1, ...] (param_groups order)."""
+        starts, pos = [0], self.w_offset
+        for sh in self.w_shapes:
+            starts.append(pos)
+            pos += int(np.prod(sh))
+        return starts
+
+    def nan_error(self, limit: int) -> FloatingPointError:
+        """network.py:167-171: FloatingPointError(group, flat index of the group's first NaN) for the
+        NaN state's limit (the start of the first group whose gradient holds a NaN)."""
+        starts = self.group_starts()
+        gi = max(i for i, st in enumerate(starts) if st <= limit)
+        g = self.param_groups()[1][gi].reshape(-1)
+        first = torch.empty(1, dtype=torch.int64, device=g.device)
+        _lib.call("nvol_find_nan", _lib.ptr(g), g.numel(), _lib.ptr(first), 4, _lib.stream())
+        j = int(first.item())
+        return FloatingPointError(f"NaN gradient in parameter group {gi} at flat index {max(j, 0)}")
+
+    def _nan_state(self) -> torch.Tensor:
+        if getattr(self, "_nanst", None) is None:
+            self._nanst = torch.tensor([NAN_NONE, 0], dtype=torch.int64, device=self.flat_params.device)
+        return self._nanst
+
+    def adam_device(self, nan_state: Optional[torch.Tensor] = None) -> None:
+        """One flat Adam step (network.py:160-183) with host-cast scalars on the device
+        (nvol_adam_train_step over a one-row schedule); only the parameter groups in
+        front of the first one holding a NaN gradient are updated (nan_state)."""
         lr, c1, c2 = adam_scalars(self.opt, self.opt.t)
         f = lambda x: float(np.float32(x))  # noqa: E731  dt(...) of network.py:172-181
         o = self.opt
-        _lib.call("nvol_adam_step", _lib.ptr(self.flat_params), _lib.ptr(self.flat_grads), _lib.ptr(self.flat_m),
-                  _lib.ptr(self.flat_v), self.flat_size, f(lr), f(o.beta1), f(1.0 - o.beta1), f(o.beta2),
-                  f(1.0 - o.beta2), f(c1), f(c2), f(o.epsilon), f(o.l2_reg), 4, _lib.stream())
-        o.t += 1
+        dev = self.flat_params.device
+        if getattr(self, "_adam1", None) is None:
+            self._adam1 = (torch.zeros(3, dtype=torch.float32).pin_memory(), torch.zeros(3, dtype=torch.float32,
+                           device=dev), torch.zeros(1, dtype=torch.int64, device=dev),
+                           torch.zeros(1, dtype=torch.int32, device=dev))
+        hs, sched, counter, ticket = self._adam1
+        hs.numpy()[:] = (lr, c1, c2)     # train_step syncs every call: the previous copy has landed
+        sched.copy_(hs, non_blocking=True)
+        _lib.call("nvol_adam_train_step", _lib.ptr(self.flat_params), _lib.ptr(self.flat_grads),
+                  _lib.ptr(self.flat_m), _lib.ptr(self.flat_v), self.flat_size, _lib.ptr(sched), 1,
+                  _lib.ptr(counter), f(o.beta1), f(1.0 - o.beta1), f(o.beta2), f(1.0 - o.beta2), f(o.epsilon),
+                  f(o.l2_reg), _lib.ptr(nan_state), None, None, 0, 0, 0.0, _lib.ptr(ticket), _lib.stream())
 
     def train_step(self, batch) -> float:
-        """One optimization step; returns the pre-update loss (model.py:154-174)."""
+        """One optimization step; returns the pre-update loss (model.py:154-174).
+        A NaN gradient raises FloatingPointError(group, flat index) with the groups in
+        front of the offending one updated and opt.t not advanced (network.py:167-171)."""
         coords, targets = batch.coords, batch.targets
         if coords.shape[0] != self.batch_size:
             raise ConfigError(f"batch size {coords.shape[0]} != configured {self.batch_size}")
@@ -322,9 +355,16 @@ class NeuralModel:
             return self._train_step_generic(coords, targets)
         c, t = self._stage_batch(coords, targets)
         loss_sum = torch.zeros(1, dtype=torch.float64, device=c.device)
-        self.fwd_bwd_device(c, t, loss_sum)
-        self.adam_device()
-        return float(loss_sum.item()) / c.shape[0]
+        ns = self._nan_state()
+        self.fwd_bwd_device(c, t, loss_sum, nan_state=ns)
+        self.adam_device(ns)
+        loss = float(loss_sum.item()) / c.shape[0]
+        lim = int(ns[0].item())
+        if lim != NAN_NONE:
+            ns.copy_(torch.tensor([NAN_NONE, 0], dtype=torch.int64))
+            raise self.nan_error(lim)
+        self.opt.t += 1
+        return loss
 
     def _stage_batch(self, coords, targets):
         """Device copies of a host batch through pinned staging buffers."""

@@ -28,7 +28,7 @@ import torch
 
 from . import _lib
 from .errors import ConfigError, FormatError
-from .model import MODE_TCGEN05, TRAIN_ENCODE_ONLY, TRAIN_PREENCODED, NeuralModel, build_model
+from .model import MODE_TCGEN05, NAN_NONE, TRAIN_ENCODE_ONLY, TRAIN_PREENCODED, NeuralModel, build_model
 from .network import adam_scalars, lr_at
 from .sampler import InCoreSampler
 from .volume import ScalarField, VolumeMeta
@@ -124,7 +124,8 @@ class StepPipeline:
         self.capacity = int(capacity)
         self.losses = torch.zeros(self.capacity, dtype=torch.float64, device=dev)
         self.acc = torch.zeros(1, dtype=torch.float64, device=dev)
-        self.nan_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        # NaN contract (nvol.h): [first NaN group's flat start, halted]; checked by every step kernel
+        self.nan_state = torch.tensor([NAN_NONE, 0], dtype=torch.int64, device=dev)
         o = model.opt
         rows = []
         for t in range(self.t0 + self.capacity + 1):
@@ -149,8 +150,10 @@ class StepPipeline:
         # skips its encode.  Off by default: measured on B200 at cfg2 the two halves
         # share L2 throughput, so the fused launch (145 us) is slower than Adam +
         # encode back to back (70 + 31 us) -- DESIGN.md "Step-tail fusion"
-        self.fused = (self.overlap and self.train_mode == MODE_TCGEN05
+        # (not with the sharded optimizer: its step tail is the slice Adam + all-gather)
+        self.fused = (self.overlap and self.train_mode == MODE_TCGEN05 and not self.sharded
                       and os.environ.get("NVOL_FUSED_TAIL", "0") == "1")
+        self.fingerprint = pipeline_fingerprint(model)
         self.work = torch.zeros(2 + 32, dtype=torch.int32, device=dev)   # NVOL_MAX_LEVELS
         if self.host_feed:
             self.copy_stream = torch.cuda.Stream(device=dev)
@@ -232,19 +235,21 @@ class StepPipeline:
         else:
             self.sample_into(parity, 0)
         c, t = self.bufs[parity]
-        m.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_PREENCODED if self.fused else 0)
+        m.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_PREENCODED if self.fused else 0,
+                         nan_state=self.nan_state)
         if self.sharded:
             import torch.distributed as dist
             from .distributed import allgather_shards, reduce_scatter_grads
             reduce_scatter_grads(m.flat_grads_padded, self.gslice, self.group)
             dist.all_reduce(self.acc, group=self.group)
+            dist.all_reduce(self.nan_state[:1], op=dist.ReduceOp.MIN, group=self.group)
             m.flat_grads_padded.zero_()                 # this rank's gradient is consumed
             if self.overlap:
                 main.wait_stream(self.side)
             o4 = 4 * self.slo
             _lib.call("nvol_adam_train_step", _lib.ptr(m.flat_params) + o4, _lib.ptr(self.gslice),
                       _lib.ptr(m.flat_m) + o4, _lib.ptr(m.flat_v) + o4, self.shi - self.slo, _lib.ptr(self.sched),
-                      self.sched.numel() // 3, _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag),
+                      self.sched.numel() // 3, _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_state),
                       _lib.ptr(self.acc), _lib.ptr(self.losses), self.t0, self.capacity, 1.0 / self.B,
                       _lib.ptr(self.ticket), _lib.stream())
             allgather_shards(m.flat_params_padded, self.rank, self.group)
@@ -252,6 +257,8 @@ class StepPipeline:
         if self.world > 1:
             from .distributed import allreduce_grads
             allreduce_grads(m.flat_grads, self.acc, self.group)
+            import torch.distributed as dist
+            dist.all_reduce(self.nan_state[:1], op=dist.ReduceOp.MIN, group=self.group)
         if self.overlap:
             main.wait_stream(self.side)                 # join before the counter advances
         if self.fused:
@@ -260,7 +267,7 @@ class StepPipeline:
             ws = m._workspace(self.b)
             _lib.call("nvol_adam_encode_step", _lib.ptr(m.flat_params), _lib.ptr(m.flat_grads), _lib.ptr(m.flat_m),
                       _lib.ptr(m.flat_v), m.flat_size, _lib.ptr(self.sched), self.sched.numel() // 3,
-                      _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag), _lib.ptr(self.acc),
+                      _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_state), _lib.ptr(self.acc),
                       _lib.ptr(self.losses), self.t0, self.capacity, 1.0 / self.B, _lib.ptr(self.work),
                       _lib.ptr(self.bufs[parity ^ 1][0]), self.b, off, res, ent, dense, cfg.n_levels,
                       cfg.n_features_per_level, m.mlp.config.n_neurons, m.mlp.config.n_hidden_layers,
@@ -268,7 +275,7 @@ class StepPipeline:
             return
         _lib.call("nvol_adam_train_step", _lib.ptr(m.flat_params), _lib.ptr(m.flat_grads), _lib.ptr(m.flat_m),
                   _lib.ptr(m.flat_v), m.flat_size, _lib.ptr(self.sched), self.sched.numel() // 3,
-                  _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_flag), _lib.ptr(self.acc),
+                  _lib.ptr(self.counter), *self.adam_consts, _lib.ptr(self.nan_state), _lib.ptr(self.acc),
                   _lib.ptr(self.losses), self.t0, self.capacity, 1.0 / self.B, _lib.ptr(self.ticket), _lib.stream())
 
     def launches_per_step(self) -> int:
@@ -299,7 +306,8 @@ class StepPipeline:
                 # this call's first batch: encode it with the current parameters (the
                 # previous call's look-ahead encode may predate a parameter change)
                 c, t = self.bufs[parity]
-                self.model.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_ENCODE_ONLY)
+                self.model.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_ENCODE_ONLY,
+                                          nan_state=self.nan_state)
             if self.done == 0:
                 self._body(parity)                      # eager first step (warms up / lazily allocates)
             elif not self.use_graph:
@@ -326,26 +334,51 @@ class StepPipeline:
             self.done += 1
 
     def finish(self) -> np.ndarray:
-        """Synchronise, commit host-side state, return the per-step losses."""
+        """Synchronise, commit host-side state, return the per-step losses.
+
+        NaN contract (network.py:160-183): a step whose gradient holds a NaN updated only
+        the parameter groups in front of the offending one and halted the pipeline; the
+        steps queued after it did nothing.  opt.t counts the applied steps only, the
+        sampler stands after the failing step's batch (drawn, as the reference draws it
+        before train_step raises), and FloatingPointError(group, flat index) is raised."""
+        m = self.model
         if self.host_feed:
             torch.cuda.current_stream().synchronize()
             losses = self.loss_host[:self.done].numpy().copy()
             self.staged = [None, None]
         else:
             losses = self.losses[:self.done].cpu().numpy()
-            self.sampler.rng.u32 = self.u32_base + 3 * self.B * self.done
-        self.model.opt.t = self.t0 + self.done
         if self.sharded:
-            # every rank holds the whole optimizer state again, and any rank's NaN stops all
-            import torch.distributed as dist
+            # every rank holds the whole optimizer state again
             from .distributed import allgather_shards
-            m = self.model
             allgather_shards(m.flat_m_padded, self.rank, self.group)
             allgather_shards(m.flat_v_padded, self.rank, self.group)
-            dist.all_reduce(self.nan_flag, op=dist.ReduceOp.MAX, group=self.group)
-        if int(self.nan_flag.item()):
-            raise FloatingPointError("NaN gradient encountered during device-resident training")
-        return losses
+        lim = int(self.nan_state[0].item())
+        applied = self.done if lim == NAN_NONE else int(self.counter.item()) - self.t0
+        m.opt.t = self.t0 + applied
+        if not self.host_feed:
+            self.sampler.rng.u32 = self.u32_base + 3 * self.B * (applied + (lim != NAN_NONE))
+        if lim == NAN_NONE:
+            return losses
+        if self.sharded:
+            # the summed gradient of the failing step lives in the ranks' slices
+            from .distributed import allgather_shards
+            n = self.shi - self.slo
+            m.flat_grads_padded[self.rank * self.chunk:self.rank * self.chunk + n].copy_(self.gslice[:n])
+            allgather_shards(m.flat_grads_padded, self.rank, self.group)
+        err = m.nan_error(lim)
+        m._pipeline = None                      # halted: the next train() builds a fresh pipeline
+        raise err
+
+
+def pipeline_fingerprint(model: NeuralModel) -> tuple:
+    """Everything a StepPipeline bakes in at construction (Adam schedule and constants,
+    loss / output activation captured in its graphs, engine, batch, buffers): a cached
+    pipeline is reused only while this is unchanged (the reference reads opt every step)."""
+    o = model.opt
+    return (o.base_lr, o.beta1, o.beta2, o.epsilon, o.l2_reg, o.decay_start, o.decay_interval, o.decay_base,
+            model.loss_kind, model.mlp.config.output_activation, model._engine(), model.batch_size,
+            model.flat_params.data_ptr())
 
 
 def _cached_pipeline(model: NeuralModel, sampler, steps: int, mc_grid=None) -> "StepPipeline":
@@ -356,7 +389,7 @@ def _cached_pipeline(model: NeuralModel, sampler, steps: int, mc_grid=None) -> "
     if p is not None:
         ok = (p.sampler is sampler and p.mc_grid is mc_grid and p.t0 + p.done == model.opt.t
               and p.done + steps <= p.capacity
-              and p.train_mode == model._engine() and p.B == model.batch_size
+              and p.fingerprint == pipeline_fingerprint(model)
               and (p.host_feed or sampler.rng.u32 == p.u32_base + 3 * p.B * p.done))
         if ok:
             return p
@@ -445,10 +478,16 @@ def decode(model: NeuralModel, dims=None, slab_z: int | None = None, to_host: bo
 
     The whole volume is decoded by one launch (slab boundaries cannot change
     any value: each voxel is evaluated independently); slab_z only chunks the
-    launches.  The result stays on the device unless to_host."""
+    launches.  The result stays on the device unless to_host, which lands it in
+    host memory as the reference does (a numpy f32 array), with each slab's D2H
+    overlapped with the next slab's decode (_decode_to_host)."""
     dims = tuple(dims if dims is not None else model.dims)
     dx, dy, dz = dims
     _require_grid_model(model)
+    lo, hi = model.value_range
+    meta = VolumeMeta(dims=dims, dtype="f32", value_range=(lo, hi))
+    if to_host:
+        return ScalarField(meta=meta, data=_decode_to_host(model, dims, slab_z))
     data = torch.empty((dz, dy, dx), dtype=torch.float32, device=model.flat_params.device)
     step = dz if slab_z is None else int(slab_z)
     if step < 1:
@@ -456,9 +495,55 @@ def decode(model: NeuralModel, dims=None, slab_z: int | None = None, to_host: bo
     for z0 in range(0, dz, step):
         nz = min(step, dz - z0)
         decode_brick(model, dims, z0, nz, data[z0:z0 + nz])
-    lo, hi = model.value_range
-    meta = VolumeMeta(dims=dims, dtype="f32", value_range=(lo, hi))
-    return ScalarField(meta=meta, data=data.cpu().numpy() if to_host else data)
+    return ScalarField(meta=meta, data=data)
+
+
+_HOST_SLAB_BYTES = 64 << 20     # device/pinned slab size of the host-landing decode
+_HOST_RING = 4                  # slabs in flight (decode -> D2H -> host copy)
+
+
+def _decode_to_host(model: NeuralModel, dims, slab_z=None) -> np.ndarray:
+    """Decode into a host numpy array: a ring of device slabs + pinned staging slabs;
+    slab k's decode (main stream) overlaps slab k-1's D2H (copy stream) and slab k-2's
+    host copy into the output array (worker threads, GIL released by numpy)."""
+    from concurrent.futures import ThreadPoolExecutor
+    dx, dy, dz = dims
+    plane = dx * dy
+    nzs = int(slab_z) if slab_z else max(1, min(dz, _HOST_SLAB_BYTES // max(4 * plane, 1)))
+    if nzs < 1:
+        raise ConfigError("slab_z must be >= 1")
+    out = np.empty((dz, dy, dx), dtype=np.float32)
+    dev = model.flat_params.device
+    nring = min(_HOST_RING, -(-dz // nzs))
+    dbuf = [torch.empty((nzs, dy, dx), dtype=torch.float32, device=dev) for _ in range(nring)]
+    hbuf = [torch.empty((nzs, dy, dx), dtype=torch.float32).pin_memory() for _ in range(nring)]
+    decoded = [torch.cuda.Event() for _ in range(nring)]
+    landed = [torch.cuda.Event() for _ in range(nring)]
+    main = torch.cuda.current_stream()
+    copy = torch.cuda.Stream(device=dev)
+    pending = [None] * nring
+
+    def host_copy(k, z0, nz):
+        landed[k].synchronize()
+        np.copyto(out[z0:z0 + nz], hbuf[k][:nz].numpy())
+
+    with ThreadPoolExecutor(max_workers=nring) as pool:
+        for i, z0 in enumerate(range(0, dz, nzs)):
+            k = i % nring
+            nz = min(nzs, dz - z0)
+            if pending[k] is not None:
+                pending[k].result()             # pinned slot k is free again (its D2H landed too)
+            decode_brick(model, dims, z0, nz, dbuf[k][:nz])
+            decoded[k].record(main)
+            copy.wait_event(decoded[k])
+            with torch.cuda.stream(copy):
+                hbuf[k][:nz].copy_(dbuf[k][:nz], non_blocking=True)
+            landed[k].record(copy)              # (slot k is reused only after pending[k]: D2H + copy done)
+            pending[k] = pool.submit(host_copy, k, z0, nz)
+        for f in pending:
+            if f is not None:
+                f.result()
+    return out
 
 
 def compression_ratio(model: NeuralModel, meta: VolumeMeta) -> float:

@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
     assert set(_lib.EXPORTS) <= set(names) | {"nvol_last_error"}
-    assert L.nvol_abi_version() == 3
+    assert L.nvol_abi_version() == 4
 
 
 def test_library_is_sm100a():

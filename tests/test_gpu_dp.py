@@ -29,8 +29,9 @@ def _free_port():
     return p
 
 
-def _dp_worker(rank, world, port, sharded, out):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NVOL_DP_SHARDED=sharded)
+def _dp_worker(rank, world, port, sharded, out, steps=STEPS):
+    # NVOL_FUSED_TAIL=1 must not engage with the sharded optimizer (its step tail is the slice Adam)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NVOL_DP_SHARDED=sharded, NVOL_FUSED_TAIL="1")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     from paper_2207_11620_b200 import fields
@@ -39,18 +40,19 @@ def _dp_worker(rank, world, port, sharded, out):
     from paper_2207_11620_b200.sampler import InCoreSampler
     model = build_model(CFG, dims=(32, 32, 32), seed=0)
     fld = fields.rasterize("mlobb", (32, 32, 32))
-    tr = DataParallelTrainer(model, InCoreSampler(fld, seed=1), capacity=STEPS, use_graph=False)
+    tr = DataParallelTrainer(model, InCoreSampler(fld, seed=1), capacity=steps, use_graph=False)
     assert tr.pipeline.sharded == (sharded == "1")
-    tr.step(STEPS)
+    assert not (tr.pipeline.sharded and tr.pipeline.fused)
+    tr.step(steps)
     losses = tr.finish()
     out[rank] = (losses, model.flat_params.cpu().numpy(), model.flat_m.cpu().numpy(), model.opt.t)
     dist.destroy_process_group()
 
 
-def _run(sharded):
+def _run(sharded, steps=STEPS):
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.spawn(_dp_worker, args=(2, _free_port(), sharded, out), nprocs=2, join=True)
+    mp.spawn(_dp_worker, args=(2, _free_port(), sharded, out, steps), nprocs=2, join=True)
     return dict(out)
 
 
@@ -61,9 +63,24 @@ def test_dp_two_ranks_match_single_process(nv):
     from paper_2207_11620_b200.sampler import InCoreSampler
     model = build_model(CFG, dims=(32, 32, 32), seed=0)
     fld = fields.rasterize("mlobb", (32, 32, 32))
+    h1 = trainer.train(model, InCoreSampler(fld, seed=1), steps=1)
+    one_p, one_m = model.flat_params.cpu().numpy(), model.flat_m.cpu().numpy()
+    model = build_model(CFG, dims=(32, 32, 32), seed=0)
     h = trainer.train(model, InCoreSampler(fld, seed=1), steps=STEPS)
     ref_p, ref_m = model.flat_params.cpu().numpy(), model.flat_m.cpu().numpy()
     for sharded in ("1", "0"):
+        # one step, tight: same global batch, gradients summed in a different order only
+        # (float atomics / the exchange), so a wrong shard row offset or slice offset shows
+        (l0, p0, m0, t0), (l1, p1, m1, t1) = (lambda o: (o[0], o[1]))(_run(sharded, steps=1))
+        np.testing.assert_array_equal(p0, p1)
+        assert l0[0] == pytest.approx(h1.losses[0], rel=1e-6)
+        np.testing.assert_allclose(m0, one_m, rtol=1e-4, atol=1e-9)
+        moved = np.abs(one_p - build_model(CFG, dims=(32, 32, 32), seed=0).flat_params.cpu().numpy()) > 0
+        assert moved.mean() > 0.5
+        # Adam's first step is ~lr * sign(g): only a gradient that cancels to ~0 (sign decided
+        # by summation order) may land on the other side, by at most 2 lr
+        d = np.abs(p0 - one_p)
+        assert (d <= 1e-6).mean() > 0.9999 and d.max() <= 2 * 0.005 + 1e-6, (d.max(), (d > 1e-6).sum())
         out = _run(sharded)
         (l0, p0, m0, t0), (l1, p1, m1, t1) = out[0], out[1]
         np.testing.assert_array_equal(p0, p1)          # identical parameters on every rank

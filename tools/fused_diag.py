@@ -28,7 +28,7 @@ def fused(b):
         ev[0].record(stream)
         _lib.call("nvol_adam_encode_step", _lib.ptr(model.flat_params), _lib.ptr(model.flat_grads),
                   _lib.ptr(model.flat_m), _lib.ptr(model.flat_v), model.flat_size, _lib.ptr(pipe.sched),
-                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_flag),
+                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_state),
                   _lib.ptr(pipe.acc), None, pipe.t0, 0, 1.0 / B, _lib.ptr(pipe.work), _lib.ptr(pipe.bufs[1][0]), b,
                   off, res, ent, dense, cfg.n_levels, cfg.n_features_per_level, model.mlp.config.n_neurons,
                   model.mlp.config.n_hidden_layers, _lib.ptr(ws), ws.numel(), _lib.stream())
@@ -48,7 +48,7 @@ def adam():
         ev[0].record(stream)
         _lib.call("nvol_adam_train_step", _lib.ptr(model.flat_params), _lib.ptr(model.flat_grads),
                   _lib.ptr(model.flat_m), _lib.ptr(model.flat_v), model.flat_size, _lib.ptr(pipe.sched),
-                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_flag),
+                  pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts, _lib.ptr(pipe.nan_state),
                   _lib.ptr(pipe.acc), None, pipe.t0, 0, 1.0 / B, _lib.ptr(pipe.ticket), _lib.stream())
         ev[1].record(stream)
     return float(bench._event_ms(torch, fn)[0]) * 1e3
