@@ -49,7 +49,8 @@ _SIGS = {
     "nvol_field_eval_tc": [P, I64, P, P, P, P, P, I32, I32, P, P, I32, I32, P, P, P],
     "nvol_mlp_image_bytes": [I32, I32, I32, I32],
     "nvol_decode": [P, P, P, P, P, I32, I32, P, P, I32, I32, I64, I64, I64, I64, I64, F64, F64, P, I32, P, P],
-    "nvol_train_fwd_bwd": [P, P, I64, I64, P, P, P, P, P, P, I32, I32, I32, I32, I32, I32, P, P, I64, I32, P],
+    "nvol_train_fwd_bwd": [P, P, I64, I64, P, P, P, P, P, P, I32, I32, I32, I32, I32, I32, P, P, I64, I32, P, P],
+    "nvol_nan_scan": [P, I64, P, I32, P, P],
     "nvol_train_workspace_bytes": [I64, I32, I32, I32, I32, I32],
     "nvol_train_tc_supported": [I32, I32, I32, I32],
     "nvol_adam_flat_dev": [P, P, P, P, I64, P, I64, P, F32, F32, F32, F32, F32, F32, P, P],
@@ -107,7 +108,10 @@ def check(status: int, what: str = "") -> None:
 
 
 def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args), name)
+    fn = getattr(load(), name)
+    if len(args) != len(fn.argtypes):   # ctypes would pass extras with int conversion (truncated pointers)
+        raise TypeError(f"{name}: {len(args)} arguments for {len(fn.argtypes)} parameters")
+    check(fn(*args), name)
 
 
 def ptr(t) -> int | None:

@@ -97,3 +97,18 @@ def test_vnr_header_roundtrip_host(tmp_path):
     payload = json.dumps(cfg, sort_keys=True).encode()
     raw = MODEL_MAGIC + struct.pack("<II", MODEL_VERSION, len(payload)) + payload + np.ones(3, "<f4").tobytes()
     assert raw[:4] == b"VNRM" and struct.unpack("<II", raw[4:12]) == (1, len(payload))
+
+
+def test_binding_arity_matches_header():
+    """Every ctypes signature in _lib has exactly the parameter count the header
+    declares (a missing argument would be passed with ctypes' default int
+    conversion -- a truncated pointer on the device path)."""
+    from paper_2207_11620_b200 import _lib
+    text = (ROOT / "include" / "nvol.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    decls = {m.group(1): m.group(2) for m in re.finditer(r"\b(nvol_\w+)\s*\(([^;{]*?)\)\s*;", text, re.S)}
+    for name, args in _lib._SIGS.items():
+        assert name in decls, name
+        params = decls[name].strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        assert n == len(args), (name, n, len(args))
