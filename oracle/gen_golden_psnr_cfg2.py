@@ -25,7 +25,7 @@ from pathlib import Path
 import numpy as np
 
 OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
-PART = Path("/tmp/psnr_cfg2_parts")
+PART = Path(os.environ.get("PSNR_PARTS", "/tmp/psnr_cfg2_parts"))
 CFG2 = {"encoding": {"otype": "HashGrid", "n_levels": 16, "n_features_per_level": 2,
                      "log2_hashmap_size": 19, "base_resolution": 4},
         "network": {"n_neurons": 64, "n_hidden_layers": 4}, "batch_size": 65536}
@@ -59,7 +59,8 @@ def merge() -> None:
     steps = {p["steps"] for p in parts}
     threads = {p["openblas_num_threads"] for p in parts}
     assert len(steps) == 1 and len(threads) == 1, (steps, threads)
-    (OUT / "psnr_cfg2_mlobb.json").write_text(json.dumps(
+    name = os.environ.get("PSNR_OUT", "psnr_cfg2_mlobb.json")
+    (OUT / name).write_text(json.dumps(
         {"config": CFG2, "field": "mlobb", "dims": list(DIMS), "steps": steps.pop(), "model_seed": 0,
          "sampler_seeds": [p["seed"] for p in parts], "psnr_db": vals, "mean": float(np.mean(vals)),
          "std": float(np.std(vals)), "final_losses": [p["final_loss"] for p in parts],

@@ -175,7 +175,7 @@ __device__ __forceinline__ float2 ld_na2(const float2 *p) {
 template <int NF, bool COHERENT>
 __device__ __forceinline__ void encode_item(const float *__restrict__ coords, const float *__restrict__ params,
                                             const GridTables &tab, int ninp, uint8_t *__restrict__ xtiles, int l,
-                                            int64_t i, float *__restrict__ dbg_feat = nullptr) {
+                                            int64_t i, float lo_scale, float *__restrict__ dbg_feat = nullptr) {
     const int m = tab.n_levels;
     const int32_t res = tab.res[l];
     const uint32_t r1 = (uint32_t)res + 1, mask = (uint32_t)(tab.entries[l] - 1);
@@ -238,7 +238,11 @@ __device__ __forceinline__ void encode_item(const float *__restrict__ coords, co
     uint8_t *base_lo = base + TILE * ninp * 2;
     __half hv[NF], lv[NF];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) tc::split_f16(acc[f] * tc::kActScale, hv[f], lv[f]);
+    for (int f = 0; f < NF; ++f) {  // lo_scale: kLoScale (mlp_tc_kernel) or 1 (mlp_tc4_kernel, folded lo products)
+        const float a = acc[f] * tc::kActScale;
+        hv[f] = __float2half_rn(a);
+        lv[f] = __float2half_rn((a - __half2float(hv[f])) * lo_scale);
+    }
 #pragma unroll
     for (int f = 0; f < NF; f += 2) {
         if constexpr (NF == 1) {
@@ -262,14 +266,14 @@ template <int NF>
 __global__ void __launch_bounds__(256) encode_tiles_kernel(const float *__restrict__ coords, int64_t b,
                                                            const float *__restrict__ params, const GridTables tab,
                                                            int ninp, uint8_t *__restrict__ xtiles,
-                                                           float *__restrict__ dbg_feat,
+                                                           float lo_scale, float *__restrict__ dbg_feat,
                                                            const int64_t *__restrict__ nan_state) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= b * tab.n_levels || nan_halted(nan_state)) return;
     // level-major: a warp covers 32 consecutive samples of one level (uniform
     // level constants, coalesced coordinates, L1 reuse on coarse levels)
     const int l = (int)(t / b);
-    encode_item<NF, false>(coords, params, tab, ninp, xtiles, l, t - (int64_t)l * b, dbg_feat);
+    encode_item<NF, false>(coords, params, tab, ninp, xtiles, l, t - (int64_t)l * b, lo_scale, dbg_feat);
 }
 
 // ---------------------------------------------------------------------------- Adam(k) + encode(k+1)
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, 
                                                                     const float *__restrict__ coords, int64_t b,
                                                                     const GridTables tab, int ninp,
                                                                     uint8_t *__restrict__ xtiles,
-                                                                    uint32_t *__restrict__ work) {
+                                                                    uint32_t *__restrict__ work, float lo_scale) {
     __shared__ float4 ring[AE_D][4][AE_ADAM_WARPS * 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (nan_halted(a.nan_state)) return;
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(AE_THREADS, 3) adam_encode_kernel(AdamArgs a, 
                 __syncwarp();
                 ready = l;
             }
-            if (i < b) encode_item<NF, true>(coords, a.p, tab, ninp, xtiles, l, i);
+            if (i < b) encode_item<NF, true>(coords, a.p, tab, ninp, xtiles, l, i, lo_scale);
         }
     }
     // exit ticket: the last CTA records the loss, advances the counter, re-arms the work words
@@ -1045,6 +1049,515 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
     if (warp == 0) tc::tmem_dealloc(tmem, sh.t_alloc);
 }
 
+// ============================================================================ 2b. MLP, four slots
+// mlp_tc4_kernel: the same forward / loss / backward as mlp_tc_kernel, with up to
+// FOUR 128-sample tiles in flight per SM, so the ~3.5 tiles an SM gets at B = 65,536
+// all run concurrently (one dependent 2*NH-phase chain per SM instead of two).
+// What makes the room: (1) the split-fp16 forward folds its hi*hi, lo*hi and hi*lo
+// products into ONE accumulator (lo parts stored unscaled; fp16 subnormals are
+// exact tensor-core inputs), so a slot needs nn TMEM columns instead of 2*nn;
+// (2) a slot owns just two operand buffers P and Q (32 KB at nn = 64) that the
+// epilogue overwrites in place: forward P/Q = activation hi/lo, backward P = delta
+// and Q = the activation h_j the dW_j MMA needs, streamed back by a bulk copy from a
+// global scratch the forward epilogue wrote it to (L2-resident, 48 KB per tile);
+// (3) ReLU masks live in registers (bits), and dW_out = sum g*h_NH is reduced on
+// CUDA cores (warp transpose-reduce + shared atomics).  The MMA warp polls the
+// slots' barriers without blocking and serves whichever slot is ready.
+constexpr int M4_SLOTS = 4;
+constexpr int M4_WARPS = 4 * M4_SLOTS + 1;  // 4 epilogue warps per slot (one per TMEM lane quarter) + MMA
+constexpr int M4_THREADS = M4_WARPS * 32;
+
+struct Tc4Shape {
+    int nin, ninp, nn, nh, accw, slots, relu_out, loss_kind;
+    uint32_t o_w[MAX_NH], o_wl[MAX_NH], o_wout, o_dwout, o_p[M4_SLOTS], o_q[M4_SLOTS], smem_bytes, half_bytes;
+    uint32_t xhalf, t_acc[M4_SLOTS], t_dw[MAX_NH], t_alloc;
+    int64_t w_floats, h_tile_bytes;  // per tile, per stored activation h_1..h_{nh-1} in the scratch
+};
+
+static int build_shape4(Tc4Shape &s, int m, int n, int nn, int nh, int relu_out, int loss_kind) {
+    s.nin = m * n;
+    s.ninp = (s.nin + 15) & ~15;
+    s.nn = nn;
+    s.nh = nh;
+    s.relu_out = relu_out;
+    s.loss_kind = loss_kind;
+    if (nh < 1 || nh > MAX_NH || !(nn == 16 || nn == 32 || nn == 64)) return 0;
+    if (s.ninp > 2 * nn || s.ninp > 128) return 0;
+    s.accw = max(nn, s.ninp);
+    s.xhalf = 2u * TILE * s.ninp;
+    s.half_bytes = 2u * TILE * s.accw;
+    s.h_tile_bytes = 2ll * TILE * nn;
+    s.w_floats = (int64_t)nn * s.nin + (int64_t)(nh - 1) * nn * nn + nn;
+    const int dwcols = s.ninp + (nh - 1) * nn;
+    for (int slots = M4_SLOTS; slots >= 3; --slots) {
+        if (slots * s.accw + dwcols > 512) continue;
+        uint32_t off = 0;
+        auto take = [&](uint32_t bytes) {
+            uint32_t r = off;
+            off += (bytes + 127) & ~127u;
+            return r;
+        };
+        for (int i = 0; i < nh; ++i) {
+            s.o_w[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+            s.o_wl[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
+        }
+        s.o_wout = take(4u * nn);
+        s.o_dwout = take(4u * nn);
+        off = (off + 1023) & ~1023u;
+        for (int t = 0; t < slots; ++t) {
+            s.o_p[t] = take(s.half_bytes);
+            s.o_q[t] = take(s.half_bytes);
+        }
+        // the M = 128 MN-major delta^T operand of the dW MMAs reads up to ~2 KB past an
+        // nn-wide tile (rows >= nn, unused): slack after the last buffer; the prologue
+        // stages the fp32 weights over the slot buffers
+        const uint32_t slot_area = off - s.o_p[0];
+        off += 4096;
+        if ((int64_t)slot_area < s.w_floats * 4) continue;
+        if (off > 227u * 1024u - 1024u) continue;
+        s.slots = slots;
+        s.smem_bytes = off;
+        uint32_t col = 0;
+        for (int t = 0; t < slots; ++t) {
+            s.t_acc[t] = col;
+            col += s.accw;
+        }
+        for (int i = 0; i < nh; ++i) {
+            s.t_dw[i] = col;
+            col += (i == 0) ? s.ninp : nn;
+        }
+        uint32_t a = 32;
+        while (a < col) a <<= 1;
+        s.t_alloc = a;
+        return 1;
+    }
+    return 0;
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+
+// the generic-proxy stores of an epilogue (shared operands, global activation scratch)
+// become visible to the tensor cores / bulk copies that read them next
+__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+__device__ __forceinline__ void st_global_v4(void *p, uint4 v) {
+    asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// 16 consecutive fp32 -> fp16 hi (+ unscaled fp16 lo) in the core-matrix layout at (row, c)
+__device__ __forceinline__ void split_row16(const float *v, uint4 &h0, uint4 &h1, uint4 &l0, uint4 &l1) {
+    uint32_t hw[8], lw[8];
+#pragma unroll
+    for (int e = 0; e < 16; e += 2) {
+        const __half a = __float2half_rn(v[e]), b = __float2half_rn(v[e + 1]);
+        const __half la = __float2half_rn(v[e] - __half2float(a)), lb = __float2half_rn(v[e + 1] - __half2float(b));
+        __half2 hh = __halves2half2(a, b), ll = __halves2half2(la, lb);
+        hw[e / 2] = *reinterpret_cast<uint32_t *>(&hh);
+        lw[e / 2] = *reinterpret_cast<uint32_t *>(&ll);
+    }
+    h0 = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    h1 = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+    l0 = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    l1 = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+}
+
+__global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
+    const uint8_t *__restrict__ xtiles, const float *__restrict__ targets, int64_t b, double inv_bglobal, float dscale,
+    const Tc4Shape sh, const float *__restrict__ wflat, double *__restrict__ loss_sum, float *__restrict__ dfeat,
+    int64_t stride, float *__restrict__ dw_grads, uint8_t *__restrict__ hscratch, float *__restrict__ dbg_pred,
+    int64_t *__restrict__ nan_state, int64_t woff) {
+    if (nan_halted(nan_state)) return;  // NaN contract: a halted pipeline does no more work
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t bar_x[M4_SLOTS], bar_h[M4_SLOTS], bar_acc[M4_SLOTS], bar_op[M4_SLOTS], bar_w;
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ double s_loss[4 * M4_SLOTS];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int NN = sh.nn, NINP = sh.ninp, NH = sh.nh, NIN = sh.nin, S = sh.slots;
+    const int64_t ntiles = (b + TILE - 1) / TILE;
+    const int64_t xtile_bytes = 2 * (int64_t)sh.xhalf;
+    const int64_t hs_tile = (int64_t)(NH - 1) * sh.h_tile_bytes;
+    int64_t nan_at = kNanNone;
+    auto tile_of = [&](int t, int64_t k) -> int64_t { return (int64_t)blockIdx.x + ((int64_t)t + (int64_t)S * k) * gridDim.x; };
+
+    // ---- prologue: fp32 weights by one bulk copy, packed to fp16 hi / unscaled lo tiles
+    float *stage = reinterpret_cast<float *>(smem + sh.o_p[0]);
+    if (tid == 0) {
+        for (int t = 0; t < M4_SLOTS; ++t) {
+            tc::mbar_init(&bar_x[t], 1);
+            tc::mbar_init(&bar_h[t], 1);
+            tc::mbar_init(&bar_acc[t], 1);
+            tc::mbar_init(&bar_op[t], 4);  // one arrive per epilogue warp of the slot
+        }
+        tc::mbar_init(&bar_w, 1);
+        tc::fence_mbar_init();
+        const uint32_t wbytes = (uint32_t)sh.w_floats * 4u;
+        tc::mbar_arrive_expect_tx(&bar_w, wbytes);
+        tc::bulk_g2s(stage, wflat, wbytes, &bar_w);
+    }
+    __syncthreads();
+    tc::mbar_wait(&bar_w, 0);
+    {
+        const float *src = stage;
+        for (int i = 0; i < NH; ++i) {
+            const int win = i == 0 ? NIN : NN, wp = i == 0 ? NINP : NN, g8 = wp >> 3;
+            for (int q = tid; q < NN * g8; q += M4_THREADS) {
+                const int o = q / g8, j0 = (q - o * g8) * 8;
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = (j0 + e < win) ? src[o * win + j0 + e] : 0.0f;
+                uint32_t hw[4], lw[4];
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                    const __half h0 = __float2half_rn(v[e]), h1 = __float2half_rn(v[e + 1]);
+                    const __half l0 = __float2half_rn(v[e] - __half2float(h0)), l1 = __float2half_rn(v[e + 1] - __half2float(h1));
+                    __half2 hh2 = __halves2half2(h0, h1), ll2 = __halves2half2(l0, l1);
+                    hw[e / 2] = *reinterpret_cast<uint32_t *>(&hh2);
+                    lw[e / 2] = *reinterpret_cast<uint32_t *>(&ll2);
+                }
+                const uint32_t off = tc::tile_off(o, j0, wp);
+                *reinterpret_cast<uint4 *>(smem + sh.o_w[i] + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                *reinterpret_cast<uint4 *>(smem + sh.o_wl[i] + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            }
+            src += NN * win;
+        }
+        for (int q = tid; q < NN; q += M4_THREADS) {
+            reinterpret_cast<float *>(smem + sh.o_wout)[q] = src[q];
+            reinterpret_cast<float *>(smem + sh.o_dwout)[q] = 0.0f;
+        }
+    }
+    if (warp == 0) tc::tmem_alloc(&tmem_base_sh, sh.t_alloc);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();  // (the weight staging area is dead from here: the X loads below overwrite it)
+    tc::fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    auto load_x = [&](int t, int64_t tile) {  // X hi -> P[t], X lo -> Q[t]
+        const uint8_t *src = xtiles + tile * xtile_bytes;
+        tc::mbar_arrive_expect_tx(&bar_x[t], 2 * sh.xhalf);
+        tc::bulk_g2s(smem + sh.o_p[t], src, sh.xhalf, &bar_x[t]);
+        tc::bulk_g2s(smem + sh.o_q[t], src + sh.xhalf, sh.xhalf, &bar_x[t]);
+    };
+    // h_j (j >= 1: the scratch written by the forward epilogue; j = 0: the X hi tile) -> Q[t]
+    auto load_h = [&](int t, int64_t tile, int j) {
+        const uint8_t *src = j == 0 ? xtiles + tile * xtile_bytes : hscratch + tile * hs_tile + (int64_t)(j - 1) * sh.h_tile_bytes;
+        const uint32_t bytes = j == 0 ? sh.xhalf : (uint32_t)sh.h_tile_bytes;
+        tc::mbar_arrive_expect_tx(&bar_h[t], bytes);
+        tc::bulk_g2s(smem + sh.o_q[t], src, bytes, &bar_h[t]);
+    };
+    if (tid == 0) {
+        for (int t = 0; t < S; ++t)
+            if (tile_of(t, 0) < ntiles) load_x(t, tile_of(t, 0));
+    }
+    const int nph = 2 * NH;
+
+    if (warp == 4 * M4_SLOTS) {
+        // ================================================================ MMA issuer (polls, never blocks on one slot)
+        if (lane == 0) {
+            uint32_t par_x = 0, par_h = 0, par_op = 0, started = 0, done = 0, dw_started = 0;
+            int64_t kt[M4_SLOTS];
+            int ph[M4_SLOTS];
+            for (int t = 0; t < M4_SLOTS; ++t) {
+                kt[t] = 0;
+                ph[t] = 0;
+                if (t >= S || tile_of(t, 0) >= ntiles) done |= 1u << t;
+            }
+            const uint32_t idesc_f = tc::make_idesc(128, NN, 0, 0);
+            while (done != (1u << M4_SLOTS) - 1u) {
+                for (int t = 0; t < S; ++t) {
+                    if ((done >> t) & 1u) continue;
+                    const int p = ph[t];
+                    if (((started >> t) & 1u) && !mbar_test(&bar_op[t], (par_op >> t) & 1u)) continue;
+                    if (p == 0 && !mbar_test(&bar_x[t], (par_x >> t) & 1u)) continue;
+                    if (p >= NH && !mbar_test(&bar_h[t], (par_h >> t) & 1u)) continue;
+                    if ((started >> t) & 1u) par_op ^= 1u << t;
+                    if (p == 0) par_x ^= 1u << t;
+                    if (p >= NH) par_h ^= 1u << t;
+                    started |= 1u << t;
+                    tc::fence_after();
+                    const uint32_t acc = tmem + sh.t_acc[t];
+                    const uint32_t pb = tc::smem_u32(smem + sh.o_p[t]), qb = tc::smem_u32(smem + sh.o_q[t]);
+                    if (p < NH) {
+                        // forward layer i: hi*W_hi + lo*W_hi + hi*W_lo into one accumulator
+                        const int i = p, win = (i == 0) ? NINP : NN;
+                        const uint32_t sbo = (win / 8) * 128;
+                        const uint64_t ah = tc::make_desc(pb, 128, sbo), al = tc::make_desc(qb, 128, sbo);
+                        const uint64_t bh = tc::make_desc(tc::smem_u32(smem + sh.o_w[i]), 128, sbo);
+                        const uint64_t bl = tc::make_desc(tc::smem_u32(smem + sh.o_wl[i]), 128, sbo);
+                        for (int k = 0; k < win / 16; ++k) {
+                            const uint64_t dk = (uint64_t)(k * 16);
+                            tc::mma_f16(acc, ah + dk, bh + dk, idesc_f, k > 0);
+                            tc::mma_f16(acc, al + dk, bh + dk, idesc_f, 1);
+                            tc::mma_f16(acc, ah + dk, bl + dk, idesc_f, 1);
+                        }
+                    } else {
+                        // backward layer j: dW_j += delta^T h_j (P^T x Q), dX = delta W_j (P x W_j)
+                        const int j = nph - 1 - p, win = (j == 0) ? NINP : NN;
+                        {
+                            const uint32_t id = tc::make_idesc(128, win, 1, 1);
+                            const uint64_t ad = tc::make_desc(pb, (NN / 8) * 128, 128);
+                            const uint64_t bd = tc::make_desc(qb, (win / 8) * 128, 128);
+                            const uint32_t first = ((dw_started >> j) & 1u) ? 1u : 0u;
+                            for (int k = 0; k < TILE / 16; ++k)
+                                tc::mma_f16(tmem + sh.t_dw[j], ad + (uint64_t)(k * 2 * (NN / 8) * 8),
+                                            bd + (uint64_t)(k * 2 * (win / 8) * 8), id, (first || k > 0) ? 1 : 0);
+                            dw_started |= 1u << j;
+                        }
+                        {
+                            const uint32_t id = tc::make_idesc(128, win, 0, 1);
+                            const uint64_t ad = tc::make_desc(pb, 128, (NN / 8) * 128);
+                            const uint64_t bd = tc::make_desc(tc::smem_u32(smem + sh.o_w[j]), (win / 8) * 128, 128);
+                            for (int k = 0; k < NN / 16; ++k)
+                                tc::mma_f16(acc, ad + (uint64_t)(k * 16), bd + (uint64_t)(k * 2 * (win / 8) * 8), id, k > 0);
+                        }
+                    }
+                    tc::mma_commit(&bar_acc[t]);
+                    if (p + 1 == nph) {
+                        ph[t] = 0;
+                        ++kt[t];
+                        if (tile_of(t, kt[t]) >= ntiles) done |= 1u << t;
+                    } else {
+                        ph[t] = p + 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if ((warp >> 2) < S) {
+        // ================================================================ epilogue: slot t, TMEM lane quarter q, row s
+        const int t = warp >> 2, q = warp & 3;
+        const int s = q * 32 + lane;
+        const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + sh.t_acc[t];
+        uint8_t *pbuf = smem + sh.o_p[t];
+        uint8_t *qbuf = smem + sh.o_q[t];
+        const float *s_wout = reinterpret_cast<const float *>(smem + sh.o_wout);
+        float *s_dwout = reinterpret_cast<float *>(smem + sh.o_dwout);
+        const bool leader = q == 0 && lane == 0;
+        uint32_t par_acc = 0;
+        double lsum = 0.0;
+        auto release = [&]() {
+            tc::fence_before();
+            fence_proxy_async_all();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_op[t]);
+        };
+        auto wait_acc = [&]() {
+            tc::mbar_wait_sleep(&bar_acc[t], par_acc);
+            par_acc ^= 1u;
+            tc::fence_after();
+        };
+        for (int64_t k = 0;; ++k) {
+            const int64_t tile = tile_of(t, k);
+            if (tile >= ntiles) break;
+            const int64_t row = tile * TILE + s;
+            const bool valid = row < b;
+            const float tgt = valid ? __ldg(targets + row) : 0.0f;
+            uint8_t *hs = hscratch + tile * hs_tile;
+            uint32_t mlo[MAX_NH + 1], mhi[MAX_NH + 1];  // ReLU masks of h_1..h_NH (64 columns = 2 words)
+            // ---- forward epilogues 0 .. NH-2: h_{i+1} = relu(acc) -> P (hi), Q (lo), scratch (hi)
+            for (int i = 0; i < NH - 1; ++i) {
+                wait_acc();
+                uint32_t bl = 0, bh = 0;
+                for (int c = 0; c < NN; c += 16) {
+                    float v[16];
+                    tc::tmem_ld16(tacc + c, v);
+                    tc::tmem_wait_ld();
+                    uint32_t bits = 0;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        v[e] = relu_nan(v[e]);
+                        bits |= (v[e] > 0.0f ? 1u : 0u) << e;
+                    }
+                    if (c < 32) bl |= bits << c; else bh |= bits << (c - 32);
+                    uint4 h0, h1, l0, l1;
+                    split_row16(v, h0, h1, l0, l1);
+                    const uint32_t o0 = tc::tile_off(s, c, NN), o1 = tc::tile_off(s, c + 8, NN);
+                    *reinterpret_cast<uint4 *>(pbuf + o0) = h0;
+                    *reinterpret_cast<uint4 *>(pbuf + o1) = h1;
+                    *reinterpret_cast<uint4 *>(qbuf + o0) = l0;
+                    *reinterpret_cast<uint4 *>(qbuf + o1) = l1;
+                    uint8_t *g = hs + (int64_t)i * sh.h_tile_bytes;
+                    st_global_v4(g + o0, h0);
+                    st_global_v4(g + o1, h1);
+                }
+                mlo[i + 1] = bl;
+                mhi[i + 1] = bh;
+                release();
+            }
+            // ---- last forward epilogue: h_NH, output layer, loss gradient, delta_NH, dW_out
+            wait_acc();
+            // the slot's 4 warps wrote h_{NH-1} to the scratch (generic stores + proxy fence in release):
+            // order them before the bulk copy that streams it back (bar.sync has CTA memory-barrier semantics)
+            named_sync(1 + t, 128);
+            if (leader) load_h(t, tile, NH - 1);  // Q (h_{NH-1} lo) is free: stream h_{NH-1} back for dW_{NH-1}
+            float outp = 0.0f;
+            for (int c = 0; c < NN; c += 16) {
+                float v[16];
+                tc::tmem_ld16(tacc + c, v);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * relu_nan(v[e]);
+            }
+            const float o = outp * (1.0f / tc::kActScale);
+            const float pred = sh.relu_out ? relu_nan(o) : o;
+            if (dbg_pred && valid) dbg_pred[row] = pred;  // parity hook (nvol_train_tc_debug)
+            const double d = (double)pred - (double)tgt;
+            double gg, sl;
+            if (sh.loss_kind == 0) {
+                sl = fabs(d);
+                gg = (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : (d == d ? 0.0 : d))) * inv_bglobal;  // np.sign(NaN) = NaN
+            } else {
+                sl = d * d;
+                gg = 2.0 * d * inv_bglobal;
+            }
+            float gf = (float)gg;
+            if (sh.relu_out && !(pred > 0.0f)) gf *= 0.0f;  // d * (act > 0): a NaN d stays NaN (numpy)
+            if (!valid) {
+                gf = 0.0f;
+                sl = 0.0;
+            }
+            lsum += sl;
+            const float gd = gf * dscale;
+            for (int c = 0; c < NN; c += 16) {
+                float v[16], dv[16];
+                tc::tmem_ld16(tacc + c, v);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    v[e] = relu_nan(v[e]);
+                    const float x = gd * s_wout[c + e];
+                    dv[e] = v[e] > 0.0f ? x : x * 0.0f;
+                }
+                store_row_f16(pbuf, s, c, NN, dv, false);
+                // dW_out[c + e] += sum over the warp's rows of gd * h: transpose-reduce 16 columns over 32 lanes
+                float x[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) x[e] = gd * v[e];
+#pragma unroll
+                for (int w = 8; w >= 1; w >>= 1) {
+                    const bool up = (lane & (2 * w)) != 0;  // lane bit 4, 3, 2, 1 for w = 8, 4, 2, 1
+#pragma unroll
+                    for (int e = 0; e < w; ++e) {
+                        const float send = up ? x[e] : x[e + w];
+                        const float keep = up ? x[e + w] : x[e];
+                        x[e] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * w);
+                    }
+                }
+                const float z = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
+                const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+                if ((lane & 1) == 0) atomicAdd(s_dwout + c + col, z);
+            }
+            release();
+            // ---- backward epilogues
+            for (int j = NH - 1; j >= 0; --j) {
+                wait_acc();
+                if (j > 0) {
+                    named_sync(1 + t, 128);
+                    if (leader) load_h(t, tile, j - 1);  // Q (h_j) was read by dW_j: stream h_{j-1} back
+                    for (int c = 0; c < NN; c += 16) {
+                        float v[16];
+                        tc::tmem_ld16(tacc + c, v);
+                        tc::tmem_wait_ld();
+                        const uint32_t bits = (c < 32 ? mlo[j] >> c : mhi[j] >> (c - 32)) & 0xffffu;
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = ((bits >> e) & 1u) ? v[e] : v[e] * 0.0f;
+                        store_row_f16(pbuf, s, c, NN, v, false);
+                    }
+                } else {
+                    // the slot's buffers are free once dW_0 / dX_0 completed: next X tile
+                    if (leader && tile_of(t, k + 1) < ntiles) load_x(t, tile_of(t, k + 1));
+                    for (int c = 0; c < NINP; c += 16) {
+                        float v[16];
+                        tc::tmem_ld16(tacc + c, v);
+                        tc::tmem_wait_ld();
+                        if (valid) {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e)
+                                if (c + e < NIN) {
+                                    const float dv = v[e] * (1.0f / dscale);
+                                    if (isnan(dv)) nan_at = 0;  // the encoder group (group 0) gets a NaN gradient
+                                    dfeat[(int64_t)(c + e) * stride + row] = dv;
+                                }
+                        }
+                    }
+                }
+                release();
+            }
+        }
+        for (int o2 = 16; o2 > 0; o2 >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o2);
+        if (lane == 0) s_loss[warp] = lsum;
+    } else if (warp < 4 * M4_SLOTS && lane == 0) {
+        s_loss[warp] = 0.0;  // slots this shape has no room for
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double l = 0.0;
+        for (int w = 0; w < 4 * M4_SLOTS; ++w) l += s_loss[w];
+        atomicAdd(loss_sum, l);
+    }
+    // ---- flush dW_0..dW_{nh-1} (TMEM) and dW_out (shared) once per CTA: vector REDs into the gradient
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const float unscale = 1.0f / (dscale * tc::kActScale);  // dW = (dscale*delta)^T (kActScale*H)
+    if (warp < 4 * M4_SLOTS) {
+        const int q = warp & 3, grp = warp >> 2;
+        const int o = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        int64_t base = 0;
+        for (int j = 0; j < NH; ++j) {
+            const int win = (j == 0) ? NIN : NN;
+            const int wacc = (j == 0) ? NINP : NN;
+            int c0, nc;
+            group_cols(wacc, grp, 4, c0, nc);
+            if (q * 32 < NN) {  // warp-uniform: lanes of quarters past nn hold no dW rows
+                for (int c = c0; c < c0 + nc; c += 16) {
+                    float v[16];
+                    tc::tmem_ld16(tmem + lane_base + sh.t_dw[j] + c, v);
+                    tc::tmem_wait_ld();
+                    if (o < NN) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            if (c + e < win && isnan(v[e])) nan_at = min(nan_at, woff + base);  // W_j's group
+                        float *g = dw_grads + base + (int64_t)o * win + c;
+                        if (c + 16 <= win && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+#pragma unroll
+                            for (int e = 0; e < 16; e += 4)
+                                atomicAdd(reinterpret_cast<float4 *>(g + e),
+                                          make_float4(v[e] * unscale, v[e + 1] * unscale, v[e + 2] * unscale,
+                                                      v[e + 3] * unscale));
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e)
+                                if (c + e < win) atomicAdd(g + e, v[e] * unscale);
+                        }
+                    }
+                }
+            }
+            base += (int64_t)NN * win;
+        }
+        if (tid < NN) {
+            const float v = reinterpret_cast<const float *>(smem + sh.o_dwout)[tid];
+            if (isnan(v)) nan_at = min(nan_at, woff + base);
+            atomicAdd(dw_grads + base + tid, v * unscale);
+        }
+    }
+    if (nan_at != kNanNone) nan_mark(nan_state, nan_at);
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, sh.t_alloc);
+}
+
 // ============================================================================ 3. scatter
 template <int NF>
 __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__restrict__ coords,
@@ -1162,9 +1675,21 @@ constexpr int MAX_CHUNKS = 4;
 
 struct TcPlan {
     TcShape sh;
+    Tc4Shape sh4;
+    bool v4;  // mlp_tc4_kernel (four slots, folded split-fp16 accumulator) takes this shape
     int grid_mlp, grid_sc, n_coarse, coarse_floats, nchunks;
-    int64_t ntiles, chunk_tiles, off_x, off_dfeat, total;
+    int64_t ntiles, chunk_tiles, off_x, off_dfeat, off_h, total;
+    float lo_scale() const { return v4 ? 1.0f : tc::kLoScale; }
 };
+
+static bool mlp4_enabled() {
+    static int on = -1;  // NVOL_MLP4=0 selects the two-slot mlp_tc_kernel (A/B measurements)
+    if (on < 0) {
+        const char *e = getenv("NVOL_MLP4");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
 
 static int num_sms() {
     static int sms = 0;
@@ -1179,6 +1704,7 @@ static int num_sms() {
 
 static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh, int relu_out, int loss_kind) {
     if (!build_shape(p.sh, tab.n_levels, tab.n_feat, nn, nh, relu_out, loss_kind)) return 0;
+    p.v4 = mlp4_enabled() && build_shape4(p.sh4, tab.n_levels, tab.n_feat, nn, nh, relu_out, loss_kind);
     for (int l = 0; l < tab.n_levels; ++l)
         if (tab.entries[l] >= (1ll << 31)) return 0;
     const int sms = num_sms();
@@ -1216,16 +1742,19 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
     p.off_x = 0;
     p.off_dfeat = al(p.ntiles * TILE * p.sh.ninp * 4);  // hi + lo fp16 tiles
-    p.total = p.off_dfeat + al(b * p.sh.nin * 4) + 256;
+    p.off_h = p.off_dfeat + al(b * p.sh.nin * 4);      // mlp_tc4_kernel's activation scratch h_1..h_{nh-1}
+    p.total = p.off_h + (p.v4 ? al(p.ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) : 0) + 256;
     return 1;
 }
 
 int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
     TcPlan p;
     if (!build_shape(p.sh, m, n, nn, nh, 1, 0)) return 0;
+    const bool v4 = mlp4_enabled() && build_shape4(p.sh4, m, n, nn, nh, 1, 0);
     int64_t ntiles = (b + TILE - 1) / TILE;
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
-    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) + 256;
+    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) + (v4 ? al(ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) : 0) +
+           256;
 }
 
 static cudaEvent_t g_stage_events[8];
@@ -1276,7 +1805,10 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
     for (int l = 0; l < tab.n_levels; ++l) enc = max(enc, tab.offset[l] + tab.entries[l] * tab.n_feat);
     const int64_t woff = flat_weight_offset(params, enc);
     int st = NVOL_OK;
-    cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh.smem_bytes);
+    if (p.v4)
+        cudaFuncSetAttribute(mlp_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh4.smem_bytes);
+    else
+        cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh.smem_bytes);
     const size_t csm = (size_t)p.coarse_floats * 4;
     switch (tab.n_feat) {
         case 1: cudaFuncSetAttribute(scatter_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm); break;
@@ -1314,10 +1846,10 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
             if (nb % TILE)  // rows past the batch must be zero (0 x garbage could be NaN in dW)
                 cudaMemsetAsync(xtc + (nb / TILE) * tile_bytes, 0, (size_t)tile_bytes, se);
             switch (tab.n_feat) {
-                case 1: encode_tiles_kernel<1><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, dfe, nan_state); break;
-                case 2: encode_tiles_kernel<2><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, dfe, nan_state); break;
-                case 4: encode_tiles_kernel<4><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, dfe, nan_state); break;
-                default: encode_tiles_kernel<8><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, dfe, nan_state); break;
+                case 1: encode_tiles_kernel<1><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, p.lo_scale(), dfe, nan_state); break;
+                case 2: encode_tiles_kernel<2><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, p.lo_scale(), dfe, nan_state); break;
+                case 4: encode_tiles_kernel<4><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, p.lo_scale(), dfe, nan_state); break;
+                default: encode_tiles_kernel<8><<<egrid, 256, 0, se>>>(cc, nb, params, tab, p.sh.ninp, xtc, p.lo_scale(), dfe, nan_state); break;
             }
             st = check_launch("encode_tiles_kernel");
             if (st) return st;
@@ -1330,9 +1862,17 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         if (prof) cudaEventRecord(pev[1], s);
         const int64_t ct = (nb + TILE - 1) / TILE;
         const int gm = (int)(ct < p.grid_mlp ? ct : p.grid_mlp);
-        mlp_tc_kernel<<<gm, PP_THREADS, p.sh.smem_bytes, s>>>(xtc, targets + r0, nb, 1.0 / (double)b_global, dscale,
-                                                              p.sh, params + woff, loss_sum, dfeat + r0, b, grads + woff,
-                                                              g_dbg.pred ? g_dbg.pred + r0 : nullptr, nan_state, woff);
+        if (p.v4) {
+            const int64_t h_tile = (int64_t)(nh - 1) * p.sh4.h_tile_bytes;
+            mlp_tc4_kernel<<<gm, M4_THREADS, p.sh4.smem_bytes, s>>>(
+                xtc, targets + r0, nb, 1.0 / (double)b_global, dscale, p.sh4, params + woff, loss_sum, dfeat + r0, b,
+                grads + woff, ws + p.off_h + t0 * h_tile, g_dbg.pred ? g_dbg.pred + r0 : nullptr, nan_state, woff);
+        } else {
+            mlp_tc_kernel<<<gm, PP_THREADS, p.sh.smem_bytes, s>>>(xtc, targets + r0, nb, 1.0 / (double)b_global, dscale,
+                                                                  p.sh, params + woff, loss_sum, dfeat + r0, b,
+                                                                  grads + woff, g_dbg.pred ? g_dbg.pred + r0 : nullptr,
+                                                                  nan_state, woff);
+        }
         st = check_launch("mlp_tc_kernel");
         if (st) return st;
         if (g_dbg.dfeat)
@@ -1511,7 +2051,8 @@ extern "C" int nvol_adam_encode_step(float *p, float *g, float *m, float *v, int
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, AE_THREADS, 0);
         if (per_sm < 1) per_sm = 1;
-        kern<<<per_sm * num_sms(), AE_THREADS, 0, s>>>(a, head, n4, nch, lc, next_coords, b, tab, pl.sh.ninp, xt, work);
+        kern<<<per_sm * num_sms(), AE_THREADS, 0, s>>>(a, head, n4, nch, lc, next_coords, b, tab, pl.sh.ninp, xt, work,
+                                                       pl.lo_scale());
     };
     switch (n_feat) {
         case 1: launch(adam_encode_kernel<1>); break;

@@ -186,11 +186,12 @@ def test_tc_predictions_per_sample(cfg2_case):
 def _robust(k, pred_gpu):
     """Samples whose L1 sign and every ReLU mask cannot flip under operand rounding:
     sign(pred - t) agrees between the device and the oracle, |pred - t| > 1e-4 and
-    every pre-activation is > 1e-3 of its layer's max magnitude (SURVEY §8(c):
-    'exclude samples whose sign(pred-target) or ReLU mask flips')."""
+    every pre-activation is > 1e-5 of its layer's max magnitude -- ~10x the split-fp16
+    forward's pre-activation error (~22 mantissa bits accumulated over K <= 64)
+    ('exclude samples whose sign(pred-target) or ReLU mask flips')."""
     d_ref = k["pred"].astype(np.float64) - k["t"]
     d_gpu = pred_gpu.astype(np.float64) - k["t"]
-    return (np.sign(d_ref) == np.sign(d_gpu)) & (np.abs(d_ref) > 1e-4) & (k["zmin"] > 1e-3)
+    return (np.sign(d_ref) == np.sign(d_gpu)) & (np.abs(d_ref) > 1e-4) & (k["zmin"] > 1e-5)
 
 
 def test_tc_gradients_per_element(cfg2_case):
@@ -202,8 +203,12 @@ def test_tc_gradients_per_element(cfg2_case):
     k = cfg2_case
     m, ref = k["model"], k["ref"]
     _, h0 = _tc_step(m, k["c"], k["t"])
-    keep = _robust(k, h0.pred.cpu().numpy())
-    assert keep.mean() > 0.9, keep.mean()            # the excluded kinks are a small minority
+    pg = h0.pred.cpu().numpy()
+    keep = _robust(k, pg)
+    d_ref = k["pred"].astype(np.float64) - k["t"]
+    why = {"sign": float((np.sign(d_ref) != np.sign(pg.astype(np.float64) - k["t"])).mean()),
+           "small_d": float((np.abs(d_ref) <= 1e-4).mean()), "relu_margin": float((k["zmin"] <= 1e-5).mean())}
+    assert keep.mean() > 0.9, (keep.mean(), why)     # the excluded kinks are a small minority
     c, t = k["c"][keep], k["t"][keep]
     nb = c.shape[0]
     # oracle: the reference's step restricted to the kept rows, gradient scale 1/B (network.py:108)
