@@ -1146,9 +1146,8 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t phase) {
     return ok != 0;
 }
 
-// the generic-proxy stores of an epilogue (shared operands, global activation scratch)
-// become visible to the tensor cores / bulk copies that read them next
-__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
+// the generic-proxy stores of the activation scratch become visible to the bulk copies that read them
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 __device__ __forceinline__ void st_global_v4(void *p, uint4 v) {
     asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -1347,7 +1346,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
         double lsum = 0.0;
         auto release = [&]() {
             tc::fence_before();
-            fence_proxy_async_all();
+            tc::fence_proxy_async();  // shared operands -> the tensor cores
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_op[t]);
         };
@@ -1396,8 +1395,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             }
             // ---- last forward epilogue: h_NH, output layer, loss gradient, delta_NH, dW_out
             wait_acc();
-            // the slot's 4 warps wrote h_{NH-1} to the scratch (generic stores + proxy fence in release):
-            // order them before the bulk copy that streams it back (bar.sync has CTA memory-barrier semantics)
+            // the slot's 4 warps wrote h_1..h_{NH-1} to the scratch (generic stores): proxy fence, then
+            // order them before the bulk copies that stream them back (bar.sync: CTA memory barrier).
+            // Done once per tile, phases after the stores, so the fence finds them retired.
+            fence_proxy_async_global();
             named_sync(1 + t, 128);
             if (leader) load_h(t, tile, NH - 1);  // Q (h_{NH-1} lo) is free: stream h_{NH-1} back for dW_{NH-1}
             float outp = 0.0f;
@@ -1462,7 +1463,6 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             for (int j = NH - 1; j >= 0; --j) {
                 wait_acc();
                 if (j > 0) {
-                    named_sync(1 + t, 128);
                     if (leader) load_h(t, tile, j - 1);  // Q (h_j) was read by dW_j: stream h_{j-1} back
                     for (int c = 0; c < NN; c += 16) {
                         float v[16];

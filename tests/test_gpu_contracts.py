@@ -228,3 +228,22 @@ def test_outofcore_refresh_never_races_queued_batches(nv, tmp_path):
             np.testing.assert_array_equal(bt.targets.cpu().numpy(), orc.trilinear(data, c, clip=True))
     finally:
         s.close()
+
+
+def test_vnr_written_by_the_reference_loads_and_round_trips(nv, tmp_path):
+    """a .vnr the reference wrote (oracle/gen_golden_vnr.py, trainer.py:125-138)
+    loads here with its config, dims and value range; eval_fused is bit-identical to the
+    reference's; decode matches the reference's decode (eval_batch, BLAS-ordered, so to
+    float rounding); and save_model writes the reference's file back byte for byte."""
+    from conftest import GOLDEN
+    from paper_2207_11620_b200 import trainer
+    z = golden("vnr_cfg1.npz")
+    m = trainer.load_model(GOLDEN / "ref_cfg1.vnr")
+    assert m.dims == (48, 48, 48) and tuple(m.value_range) == (2.0, 5.0)
+    np.testing.assert_array_equal(m.eval_fused(z["coords"]), z["eval_fused"])
+    np.testing.assert_allclose(m.eval_batch(z["coords"]), z["eval_batch"], rtol=0, atol=1e-6)
+    d = trainer.decode(m, dims=tuple(int(x) for x in z["dims"]), to_host=True).data
+    np.testing.assert_allclose(d, z["decode"], rtol=0, atol=3e-6 * 3.0)
+    out = tmp_path / "again.vnr"
+    trainer.save_model(m, out)
+    assert out.read_bytes() == (GOLDEN / "ref_cfg1.vnr").read_bytes()
