@@ -1273,6 +1273,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             }
             const uint32_t idesc_f = tc::make_idesc(128, NN, 0, 0);
             while (done != (1u << M4_SLOTS) - 1u) {
+                bool issued = false;
                 for (int t = 0; t < S; ++t) {
                     if ((done >> t) & 1u) continue;
                     const int p = ph[t];
@@ -1321,6 +1322,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                         }
                     }
                     tc::mma_commit(&bar_acc[t]);
+                    issued = true;
                     if (p + 1 == nph) {
                         ph[t] = 0;
                         ++kt[t];
@@ -1329,6 +1331,9 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                         ph[t] = p + 1;
                     }
                 }
+                // nothing ready: back off instead of stealing issue slots from the epilogue
+                // warps that share this warp's scheduler
+                if (!issued) __nanosleep(64);
             }
         }
         __syncwarp();
