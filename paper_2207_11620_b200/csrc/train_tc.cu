@@ -1272,6 +1272,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                 if (t >= S || tile_of(t, 0) >= ntiles) done |= 1u << t;
             }
             const uint32_t idesc_f = tc::make_idesc(128, NN, 0, 0);
+#ifdef NVOL_TIMELINE
+            int mma_n = 0;
+            TL(4000, gtime());
+#endif
             while (done != (1u << M4_SLOTS) - 1u) {
                 bool issued = false;
                 for (int t = 0; t < S; ++t) {
@@ -1285,6 +1289,9 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                     if (p >= NH) par_h ^= 1u << t;
                     started |= 1u << t;
                     tc::fence_after();
+#ifdef NVOL_TIMELINE
+                    TL(2 * (mma_n & 511), gtime());
+#endif
                     const uint32_t acc = tmem + sh.t_acc[t];
                     const uint32_t pb = tc::smem_u32(smem + sh.o_p[t]), qb = tc::smem_u32(smem + sh.o_q[t]);
                     if (p < NH) {
@@ -1323,6 +1330,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                     }
                     tc::mma_commit(&bar_acc[t]);
                     issued = true;
+#ifdef NVOL_TIMELINE
+                    TL(2 * (mma_n & 511) + 1, ((unsigned long long)t << 60) | ((unsigned long long)p << 52) | (gtime() & ((1ull << 52) - 1)));
+                    ++mma_n;
+#endif
                     if (p + 1 == nph) {
                         ph[t] = 0;
                         ++kt[t];
@@ -1349,16 +1360,26 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
         const bool leader = q == 0 && lane == 0;
         uint32_t par_acc = 0;
         double lsum = 0.0;
+#ifdef NVOL_TIMELINE
+        int epi_n = 0;
+#endif
         auto release = [&]() {
             tc::fence_before();
             tc::fence_proxy_async();  // shared operands -> the tensor cores
             __syncwarp();
+#ifdef NVOL_TIMELINE
+            if (leader) TL(1024 + t * 256 + 2 * (epi_n & 127) + 1, gtime());
+            ++epi_n;
+#endif
             if (lane == 0) mbar_arrive(&bar_op[t]);
         };
         auto wait_acc = [&]() {
             tc::mbar_wait_sleep(&bar_acc[t], par_acc);
             par_acc ^= 1u;
             tc::fence_after();
+#ifdef NVOL_TIMELINE
+            if (leader) TL(1024 + t * 256 + 2 * (epi_n & 127), gtime());
+#endif
         };
         for (int64_t k = 0;; ++k) {
             const int64_t tile = tile_of(t, k);
@@ -1560,6 +1581,9 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     if (nan_at != kNanNone) nan_mark(nan_state, nan_at);
     tc::fence_before();
     __syncthreads();
+#ifdef NVOL_TIMELINE
+    if (tid == 0) TL(4001, gtime());
+#endif
     if (warp == 0) tc::tmem_dealloc(tmem, sh.t_alloc);
 }
 
