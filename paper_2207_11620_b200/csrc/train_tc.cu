@@ -1134,6 +1134,14 @@ static int build_shape4(Tc4Shape &s, int m, int n, int nn, int nh, int relu_out,
     return 0;
 }
 
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(p));
+    return p != 0;
+}
+
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t phase) {
     uint32_t ok;
     asm volatile(
@@ -1262,92 +1270,106 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
 
     if (warp == 4 * M4_SLOTS) {
         // ================================================================ MMA issuer (polls, never blocks on one slot)
-        if (lane == 0) {
-            uint32_t par_x = 0, par_h = 0, par_op = 0, started = 0, done = 0, dw_started = 0;
-            int64_t kt[M4_SLOTS];
-            int ph[M4_SLOTS];
+        // The whole warp runs the loop converged, every decision is a warp vote and every
+        // operand address is computed arithmetically from kernel parameters, so the state and
+        // the descriptors stay warp-uniform (uniform registers): one elected lane issues each
+        // phase's tcgen05.mma chain without per-instruction register->uniform moves.
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+        const uint32_t sbase = tc::smem_u32(smem);
+        const uint32_t w1 = 4u * NN * NINP, wst = 4u * NN * NN, wlo1 = 2u * NN * NN;  // o_w / o_wl by layer
+        const uint32_t dw0 = (uint32_t)S * sh.accw;
+        uint32_t par_x = 0, par_h = 0, par_op = 0, started = 0, done = 0, dw_started = 0;
+        int64_t kt[M4_SLOTS];
+        int ph[M4_SLOTS];
+#pragma unroll
+        for (int t = 0; t < M4_SLOTS; ++t) {
+            kt[t] = 0;
+            ph[t] = 0;
+            if (t >= S || tile_of(t, 0) >= ntiles) done |= 1u << t;
+        }
+        const uint32_t idesc_f = tc::make_idesc(128, NN, 0, 0);
+#ifdef NVOL_TIMELINE
+        int mma_n = 0;
+        if (lane == 0) TL(4000, gtime());
+#endif
+        while (done != (1u << M4_SLOTS) - 1u) {
+            bool issued = false;
+#pragma unroll
             for (int t = 0; t < M4_SLOTS; ++t) {
-                kt[t] = 0;
-                ph[t] = 0;
-                if (t >= S || tile_of(t, 0) >= ntiles) done |= 1u << t;
-            }
-            const uint32_t idesc_f = tc::make_idesc(128, NN, 0, 0);
+                if ((done >> t) & 1u) continue;
+                const int p = ph[t];
+                bool ok = true;
+                if ((started >> t) & 1u) ok = mbar_test(&bar_op[t], (par_op >> t) & 1u);
+                if (ok && p == 0) ok = mbar_test(&bar_x[t], (par_x >> t) & 1u);
+                if (ok && p >= NH) ok = mbar_test(&bar_h[t], (par_h >> t) & 1u);
+                if (!__all_sync(0xffffffffu, ok)) continue;
+                if ((started >> t) & 1u) par_op ^= 1u << t;
+                if (p == 0) par_x ^= 1u << t;
+                if (p >= NH) par_h ^= 1u << t;
+                started |= 1u << t;
+                tc::fence_after();
 #ifdef NVOL_TIMELINE
-            int mma_n = 0;
-            TL(4000, gtime());
+                if (lane == 0) TL(2 * (mma_n & 511), gtime());
 #endif
-            while (done != (1u << M4_SLOTS) - 1u) {
-                bool issued = false;
-                for (int t = 0; t < S; ++t) {
-                    if ((done >> t) & 1u) continue;
-                    const int p = ph[t];
-                    if (((started >> t) & 1u) && !mbar_test(&bar_op[t], (par_op >> t) & 1u)) continue;
-                    if (p == 0 && !mbar_test(&bar_x[t], (par_x >> t) & 1u)) continue;
-                    if (p >= NH && !mbar_test(&bar_h[t], (par_h >> t) & 1u)) continue;
-                    if ((started >> t) & 1u) par_op ^= 1u << t;
-                    if (p == 0) par_x ^= 1u << t;
-                    if (p >= NH) par_h ^= 1u << t;
-                    started |= 1u << t;
-                    tc::fence_after();
-#ifdef NVOL_TIMELINE
-                    TL(2 * (mma_n & 511), gtime());
-#endif
-                    const uint32_t acc = tmem + sh.t_acc[t];
-                    const uint32_t pb = tc::smem_u32(smem + sh.o_p[t]), qb = tc::smem_u32(smem + sh.o_q[t]);
-                    if (p < NH) {
-                        // forward layer i: hi*W_hi + lo*W_hi + hi*W_lo into one accumulator
-                        const int i = p, win = (i == 0) ? NINP : NN;
-                        const uint32_t sbo = (win / 8) * 128;
-                        const uint64_t ah = tc::make_desc(pb, 128, sbo), al = tc::make_desc(qb, 128, sbo);
-                        const uint64_t bh = tc::make_desc(tc::smem_u32(smem + sh.o_w[i]), 128, sbo);
-                        const uint64_t bl = tc::make_desc(tc::smem_u32(smem + sh.o_wl[i]), 128, sbo);
+                const uint32_t acc = tmem_u + (uint32_t)t * sh.accw;
+                const uint32_t pb = sbase + sh.o_p[0] + 2u * (uint32_t)t * sh.half_bytes, qb = pb + sh.half_bytes;
+                if (p < NH) {
+                    // forward layer i: hi*W_hi + lo*W_hi + hi*W_lo into one accumulator
+                    const int i = p, win = (i == 0) ? NINP : NN;
+                    const uint32_t sbo = (win / 8) * 128;
+                    const uint32_t ow = i == 0 ? 0u : w1 + (uint32_t)(i - 1) * wst;
+                    const uint32_t owl = ow + (i == 0 ? 2u * NN * NINP : wlo1);
+                    const uint64_t ah = tc::make_desc(pb, 128, sbo), al = tc::make_desc(qb, 128, sbo);
+                    const uint64_t bh = tc::make_desc(sbase + ow, 128, sbo), bl = tc::make_desc(sbase + owl, 128, sbo);
+                    if (elect_one()) {
                         for (int k = 0; k < win / 16; ++k) {
                             const uint64_t dk = (uint64_t)(k * 16);
                             tc::mma_f16(acc, ah + dk, bh + dk, idesc_f, k > 0);
                             tc::mma_f16(acc, al + dk, bh + dk, idesc_f, 1);
                             tc::mma_f16(acc, ah + dk, bl + dk, idesc_f, 1);
                         }
-                    } else {
-                        // backward layer j: dW_j += delta^T h_j (P^T x Q), dX = delta W_j (P x W_j)
-                        const int j = nph - 1 - p, win = (j == 0) ? NINP : NN;
-                        {
-                            const uint32_t id = tc::make_idesc(128, win, 1, 1);
-                            const uint64_t ad = tc::make_desc(pb, (NN / 8) * 128, 128);
-                            const uint64_t bd = tc::make_desc(qb, (win / 8) * 128, 128);
-                            const uint32_t first = ((dw_started >> j) & 1u) ? 1u : 0u;
-                            for (int k = 0; k < TILE / 16; ++k)
-                                tc::mma_f16(tmem + sh.t_dw[j], ad + (uint64_t)(k * 2 * (NN / 8) * 8),
-                                            bd + (uint64_t)(k * 2 * (win / 8) * 8), id, (first || k > 0) ? 1 : 0);
-                            dw_started |= 1u << j;
-                        }
-                        {
-                            const uint32_t id = tc::make_idesc(128, win, 0, 1);
-                            const uint64_t ad = tc::make_desc(pb, 128, (NN / 8) * 128);
-                            const uint64_t bd = tc::make_desc(tc::smem_u32(smem + sh.o_w[j]), (win / 8) * 128, 128);
-                            for (int k = 0; k < NN / 16; ++k)
-                                tc::mma_f16(acc, ad + (uint64_t)(k * 16), bd + (uint64_t)(k * 2 * (win / 8) * 8), id, k > 0);
-                        }
+                        tc::mma_commit(&bar_acc[t]);
                     }
-                    tc::mma_commit(&bar_acc[t]);
-                    issued = true;
-#ifdef NVOL_TIMELINE
-                    TL(2 * (mma_n & 511) + 1, ((unsigned long long)t << 60) | ((unsigned long long)p << 52) | (gtime() & ((1ull << 52) - 1)));
-                    ++mma_n;
-#endif
-                    if (p + 1 == nph) {
-                        ph[t] = 0;
-                        ++kt[t];
-                        if (tile_of(t, kt[t]) >= ntiles) done |= 1u << t;
-                    } else {
-                        ph[t] = p + 1;
+                } else {
+                    // backward layer j: dW_j += delta^T h_j (P^T x Q), dX = delta W_j (P x W_j)
+                    const int j = nph - 1 - p, win = (j == 0) ? NINP : NN;
+                    const uint32_t ow = j == 0 ? 0u : w1 + (uint32_t)(j - 1) * wst;
+                    const uint32_t tdw = tmem_u + dw0 + (j == 0 ? 0u : (uint32_t)NINP + (uint32_t)(j - 1) * NN);
+                    const uint32_t id1 = tc::make_idesc(128, win, 1, 1), id2 = tc::make_idesc(128, win, 0, 1);
+                    const uint64_t ad1 = tc::make_desc(pb, (NN / 8) * 128, 128);
+                    const uint64_t bd1 = tc::make_desc(qb, (win / 8) * 128, 128);
+                    const uint64_t ad2 = tc::make_desc(pb, 128, (NN / 8) * 128);
+                    const uint64_t bd2 = tc::make_desc(sbase + ow, (win / 8) * 128, 128);
+                    const uint32_t first = ((dw_started >> j) & 1u) ? 1u : 0u;
+                    if (elect_one()) {
+                        for (int k = 0; k < TILE / 16; ++k)
+                            tc::mma_f16(tdw, ad1 + (uint64_t)(k * 2 * (NN / 8) * 8), bd1 + (uint64_t)(k * 2 * (win / 8) * 8), id1,
+                                        (first || k > 0) ? 1 : 0);
+                        for (int k = 0; k < NN / 16; ++k)
+                            tc::mma_f16(acc, ad2 + (uint64_t)(k * 16), bd2 + (uint64_t)(k * 2 * (win / 8) * 8), id2, k > 0);
+                        tc::mma_commit(&bar_acc[t]);
                     }
+                    dw_started |= 1u << j;
                 }
-                // nothing ready: back off instead of stealing issue slots from the epilogue
-                // warps that share this warp's scheduler
-                if (!issued) __nanosleep(64);
+                __syncwarp();
+                issued = true;
+#ifdef NVOL_TIMELINE
+                if (lane == 0)
+                    TL(2 * (mma_n & 511) + 1, ((unsigned long long)t << 60) | ((unsigned long long)p << 52) | (gtime() & ((1ull << 52) - 1)));
+                ++mma_n;
+#endif
+                if (p + 1 == nph) {
+                    ph[t] = 0;
+                    ++kt[t];
+                    if (tile_of(t, kt[t]) >= ntiles) done |= 1u << t;
+                } else {
+                    ph[t] = p + 1;
+                }
             }
+            // nothing ready: back off instead of stealing issue slots from the epilogue
+            // warps that share this warp's scheduler
+            if (!issued) __nanosleep(64);
         }
-        __syncwarp();
     } else if ((warp >> 2) < S) {
         // ================================================================ epilogue: slot t, TMEM lane quarter q, row s
         const int t = warp >> 2, q = warp & 3;
