@@ -1185,6 +1185,9 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     int64_t stride, float *__restrict__ dw_grads, uint8_t *__restrict__ hscratch, float *__restrict__ dbg_pred,
     int64_t *__restrict__ nan_state, int64_t woff) {
     if (nan_halted(nan_state)) return;  // NaN contract: a halted pipeline does no more work
+#ifdef NVOL_TIMELINE
+    if (threadIdx.x == 0) TL(4002, gtime());
+#endif
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar_x[M4_SLOTS], bar_h[M4_SLOTS], bar_acc[M4_SLOTS], bar_op[M4_SLOTS], bar_w;
     __shared__ uint32_t tmem_base_sh;
@@ -1557,6 +1560,9 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+#ifdef NVOL_TIMELINE
+    if (threadIdx.x == 0) TL(4003, gtime());
+#endif
     const float unscale = 1.0f / (dscale * tc::kActScale);  // dW = (dscale*delta)^T (kActScale*H)
     if (warp < 4 * M4_SLOTS) {
         const int q = warp & 3, grp = warp >> 2;

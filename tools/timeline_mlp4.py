@@ -25,6 +25,9 @@ buf = (ctypes.c_ulonglong * 4096)()
 lib.nvol_debug_timeline(buf, 4096)
 a = np.array(buf[:], dtype=np.uint64)
 t0, t1 = int(a[4000]), int(a[4001])
+e0, fl = int(a[4002]), int(a[4003])
+print(f"CTA0: entry -> MMA warp start {(t0 - e0) / 1e3:.2f} us (prologue), MMA start -> flush {(fl - t0) / 1e3:.2f} us, "
+      f"flush -> end {(t1 - fl) / 1e3:.2f} us, total {(t1 - e0) / 1e3:.2f} us")
 print(f"CTA0 kernel span (MMA warp start -> end) {(t1 - t0) / 1e3:.2f} us")
 mask = (1 << 52) - 1
 for k in range(200):
