@@ -1071,6 +1071,7 @@ struct Tc4Shape {
     int nin, ninp, nn, nh, accw, slots, relu_out, loss_kind;
     uint32_t o_w[MAX_NH], o_wl[MAX_NH], o_wout, o_dwout, o_p[M4_SLOTS], o_q[M4_SLOTS], smem_bytes, half_bytes;
     uint32_t xhalf, t_acc[M4_SLOTS], t_dw[MAX_NH], t_alloc;
+    uint32_t img_bytes;              // the packed weight image [0, img_bytes) of shared memory (pack_w4)
     int64_t w_floats, h_tile_bytes;  // per tile, per stored activation h_1..h_{nh-1} in the scratch
 };
 
@@ -1102,7 +1103,8 @@ static int build_shape4(Tc4Shape &s, int m, int n, int nn, int nh, int relu_out,
             s.o_wl[i] = take(2u * nn * (i == 0 ? s.ninp : nn));
         }
         s.o_wout = take(4u * nn);
-        s.o_dwout = take(4u * nn);
+        s.img_bytes = off;
+        s.o_dwout = take(4u * nn * 4 * M4_SLOTS);  // dW_out partials, one row per epilogue warp
         off = (off + 1023) & ~1023u;
         for (int t = 0; t < slots; ++t) {
             s.o_p[t] = take(s.half_bytes);
@@ -1157,6 +1159,12 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t phase) {
 // the generic-proxy stores of the activation scratch become visible to the bulk copies that read them
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
+// dead step scratch (activation scratch, X tiles, dL/dfeat): drop the 128-byte L2 line without a
+// DRAM write-back once its last reader is done (the next step rewrites it before reading)
+__device__ __forceinline__ void discard_l2(const void *p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 __device__ __forceinline__ void st_global_v4(void *p, uint4 v) {
     asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
@@ -1179,11 +1187,53 @@ __device__ __forceinline__ void split_row16(const float *v, uint4 &h0, uint4 &h1
     l1 = make_uint4(lw[4], lw[5], lw[6], lw[7]);
 }
 
+// The MLP weights as mlp_tc4_kernel's shared-memory image [0, img_bytes): per layer the fp16 hi
+// tile then the unscaled fp16 lo tile (core-matrix layout, input columns padded to ninp), then
+// the fp32 output row.  Built once per step by the first blocks of the encoder kernel (or
+// pack_w4_kernel), so the MLP kernel's prologue is one bulk copy.
+__device__ __forceinline__ void pack_w4(const float *__restrict__ w, int nin, int ninp, int nn, int nh,
+                                        uint8_t *__restrict__ img, int64_t t0, int64_t nthreads) {
+    const uint32_t w1 = 4u * nn * ninp, wst = 4u * nn * nn;
+    const float *src = w;
+    for (int i = 0; i < nh; ++i) {
+        const int win = i == 0 ? nin : nn, wp = i == 0 ? ninp : nn, g8 = wp >> 3;
+        const uint32_t ow = i == 0 ? 0u : w1 + (uint32_t)(i - 1) * wst;
+        const uint32_t owl = ow + (i == 0 ? 2u * nn * ninp : 2u * nn * nn);
+        for (int64_t q = t0; q < (int64_t)nn * g8; q += nthreads) {
+            const int o = (int)(q / g8), j0 = (int)(q - (int64_t)o * g8) * 8;
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+                const float a = (j0 + e < win) ? src[o * win + j0 + e] : 0.0f;
+                const float b = (j0 + e + 1 < win) ? src[o * win + j0 + e + 1] : 0.0f;
+                const __half ha = __float2half_rn(a), hb = __float2half_rn(b);
+                const __half la = __float2half_rn(a - __half2float(ha)), lb = __float2half_rn(b - __half2float(hb));
+                __half2 hh = __halves2half2(ha, hb), ll = __halves2half2(la, lb);
+                hw[e / 2] = *reinterpret_cast<uint32_t *>(&hh);
+                lw[e / 2] = *reinterpret_cast<uint32_t *>(&ll);
+            }
+            const uint32_t off = tc::tile_off(o, j0, wp);
+            *reinterpret_cast<uint4 *>(img + ow + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4 *>(img + owl + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+        src += (int64_t)nn * win;
+    }
+    const uint32_t owout = w1 + (uint32_t)(nh - 1) * wst;
+    for (int64_t q = t0; q < nn; q += nthreads) reinterpret_cast<float *>(img + owout)[q] = src[q];
+}
+
+constexpr int PACK_BLOCKS = 8;
+
+__global__ void __launch_bounds__(256) pack_w4_kernel(const float *__restrict__ w, int nin, int ninp, int nn, int nh,
+                                                      uint8_t *__restrict__ img) {
+    pack_w4(w, nin, ninp, nn, nh, img, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
 __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     const uint8_t *__restrict__ xtiles, const float *__restrict__ targets, int64_t b, double inv_bglobal, float dscale,
     const Tc4Shape sh, const float *__restrict__ wflat, double *__restrict__ loss_sum, float *__restrict__ dfeat,
     int64_t stride, float *__restrict__ dw_grads, uint8_t *__restrict__ hscratch, float *__restrict__ dbg_pred,
-    int64_t *__restrict__ nan_state, int64_t woff) {
+    int64_t *__restrict__ nan_state, int64_t woff, const uint8_t *__restrict__ wimg) {
     if (nan_halted(nan_state)) return;  // NaN contract: a halted pipeline does no more work
 #ifdef NVOL_TIMELINE
     if (threadIdx.x == 0) TL(4002, gtime());
@@ -1200,8 +1250,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     int64_t nan_at = kNanNone;
     auto tile_of = [&](int t, int64_t k) -> int64_t { return (int64_t)blockIdx.x + ((int64_t)t + (int64_t)S * k) * gridDim.x; };
 
-    // ---- prologue: fp32 weights by one bulk copy, packed to fp16 hi / unscaled lo tiles
-    float *stage = reinterpret_cast<float *>(smem + sh.o_p[0]);
+    // ---- prologue: the packed weight image (pack_w4) by one bulk copy
     if (tid == 0) {
         for (int t = 0; t < M4_SLOTS; ++t) {
             tc::mbar_init(&bar_x[t], 1);
@@ -1211,41 +1260,12 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
         }
         tc::mbar_init(&bar_w, 1);
         tc::fence_mbar_init();
-        const uint32_t wbytes = (uint32_t)sh.w_floats * 4u;
-        tc::mbar_arrive_expect_tx(&bar_w, wbytes);
-        tc::bulk_g2s(stage, wflat, wbytes, &bar_w);
+        tc::mbar_arrive_expect_tx(&bar_w, sh.img_bytes);
+        tc::bulk_g2s(smem, wimg, sh.img_bytes, &bar_w);
     }
+    for (int q = tid; q < 4 * M4_SLOTS * NN; q += M4_THREADS) reinterpret_cast<float *>(smem + sh.o_dwout)[q] = 0.0f;
     __syncthreads();
     tc::mbar_wait(&bar_w, 0);
-    {
-        const float *src = stage;
-        for (int i = 0; i < NH; ++i) {
-            const int win = i == 0 ? NIN : NN, wp = i == 0 ? NINP : NN, g8 = wp >> 3;
-            for (int q = tid; q < NN * g8; q += M4_THREADS) {
-                const int o = q / g8, j0 = (q - o * g8) * 8;
-                float v[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = (j0 + e < win) ? src[o * win + j0 + e] : 0.0f;
-                uint32_t hw[4], lw[4];
-#pragma unroll
-                for (int e = 0; e < 8; e += 2) {
-                    const __half h0 = __float2half_rn(v[e]), h1 = __float2half_rn(v[e + 1]);
-                    const __half l0 = __float2half_rn(v[e] - __half2float(h0)), l1 = __float2half_rn(v[e + 1] - __half2float(h1));
-                    __half2 hh2 = __halves2half2(h0, h1), ll2 = __halves2half2(l0, l1);
-                    hw[e / 2] = *reinterpret_cast<uint32_t *>(&hh2);
-                    lw[e / 2] = *reinterpret_cast<uint32_t *>(&ll2);
-                }
-                const uint32_t off = tc::tile_off(o, j0, wp);
-                *reinterpret_cast<uint4 *>(smem + sh.o_w[i] + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                *reinterpret_cast<uint4 *>(smem + sh.o_wl[i] + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-            }
-            src += NN * win;
-        }
-        for (int q = tid; q < NN; q += M4_THREADS) {
-            reinterpret_cast<float *>(smem + sh.o_wout)[q] = src[q];
-            reinterpret_cast<float *>(smem + sh.o_dwout)[q] = 0.0f;
-        }
-    }
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, sh.t_alloc);
     tc::fence_proxy_async();
     tc::fence_before();
@@ -1507,7 +1527,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                 }
                 const float z = x[0] + __shfl_xor_sync(0xffffffffu, x[0], 1);
                 const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-                if ((lane & 1) == 0) atomicAdd(s_dwout + c + col, z);
+                if ((lane & 1) == 0) s_dwout[warp * NN + c + col] += z;  // this warp's row: one owner lane per column
             }
             release();
             // ---- backward epilogues
@@ -1515,6 +1535,8 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                 wait_acc();
                 if (j > 0) {
                     if (leader) load_h(t, tile, j - 1);  // Q (h_j) was read by dW_j: stream h_{j-1} back
+                    for (int64_t ln = s; ln * 128 < sh.h_tile_bytes; ln += TILE)  // h_j's scratch is dead
+                        discard_l2(hs + (int64_t)(j - 1) * sh.h_tile_bytes + ln * 128);
                     for (int c = 0; c < NN; c += 16) {
                         float v[16];
                         tc::tmem_ld16(tacc + c, v);
@@ -1527,6 +1549,8 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                 } else {
                     // the slot's buffers are free once dW_0 / dX_0 completed: next X tile
                     if (leader && tile_of(t, k + 1) < ntiles) load_x(t, tile_of(t, k + 1));
+                    for (int64_t ln = s; ln * 128 < xtile_bytes; ln += TILE)  // this X tile is dead
+                        discard_l2(xtiles + tile * xtile_bytes + ln * 128);
                     for (int c = 0; c < NINP; c += 16) {
                         float v[16];
                         tc::tmem_ld16(tacc + c, v);
@@ -1601,7 +1625,8 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             base += (int64_t)NN * win;
         }
         if (tid < NN) {
-            const float v = reinterpret_cast<const float *>(smem + sh.o_dwout)[tid];
+            float v = 0.0f;
+            for (int w = 0; w < 4 * M4_SLOTS; ++w) v += reinterpret_cast<const float *>(smem + sh.o_dwout)[w * NN + tid];
             if (isnan(v)) nan_at = min(nan_at, woff + base);
             atomicAdd(dw_grads + base + tid, v * unscale);
         }
@@ -1622,7 +1647,8 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
                                                                 int64_t stride,
                                                                 const GridTables tab, int n_coarse, int coarse_floats,
                                                                 float *__restrict__ grads,
-                                                                const int64_t *__restrict__ nan_state) {
+                                                                const int64_t *__restrict__ nan_state,
+                                                                int discard_dfeat) {
     if (nan_halted(nan_state)) return;
     extern __shared__ float acc_s[];
     const uint64_t keep = l2_evict_last();
@@ -1645,6 +1671,15 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
             const int l = grp * SC_LG + u;
 #pragma unroll
             for (int f = 0; f < NF; ++f) dg[u][f] = l < m ? __ldg(dfeat + (int64_t)(l * NF + f) * stride + i) : 0.0f;
+        }
+        if (discard_dfeat && (threadIdx.x & 31) == 0) {
+            // the step's dL/dfeat scratch: this warp was the only reader of these lines
+            // (32 consecutive samples of one level group, b % 32 == 0)
+#pragma unroll
+            for (int u = 0; u < SC_LG; ++u)
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+                    if (grp * SC_LG + u < m) discard_l2(dfeat + (int64_t)((grp * SC_LG + u) * NF + f) * stride + i);
         }
 #pragma unroll
         for (int u = 0; u < SC_LG; ++u) {
@@ -1735,7 +1770,7 @@ struct TcPlan {
     Tc4Shape sh4;
     bool v4;  // mlp_tc4_kernel (four slots, folded split-fp16 accumulator) takes this shape
     int grid_mlp, grid_sc, n_coarse, coarse_floats, nchunks;
-    int64_t ntiles, chunk_tiles, off_x, off_dfeat, off_h, total;
+    int64_t ntiles, chunk_tiles, off_x, off_dfeat, off_h, off_img, total;
     float lo_scale() const { return v4 ? 1.0f : tc::kLoScale; }
 };
 
@@ -1800,7 +1835,8 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
     p.off_x = 0;
     p.off_dfeat = al(p.ntiles * TILE * p.sh.ninp * 4);  // hi + lo fp16 tiles
     p.off_h = p.off_dfeat + al(b * p.sh.nin * 4);      // mlp_tc4_kernel's activation scratch h_1..h_{nh-1}
-    p.total = p.off_h + (p.v4 ? al(p.ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) : 0) + 256;
+    p.off_img = p.off_h + (p.v4 ? al(p.ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) : 0);  // packed weights
+    p.total = p.off_img + (p.v4 ? al(p.sh4.img_bytes) : 0) + 256;
     return 1;
 }
 
@@ -1810,8 +1846,8 @@ int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
     const bool v4 = mlp4_enabled() && build_shape4(p.sh4, m, n, nn, nh, 1, 0);
     int64_t ntiles = (b + TILE - 1) / TILE;
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
-    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) + (v4 ? al(ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) : 0) +
-           256;
+    return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) +
+           (v4 ? al(ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) + al(p.sh4.img_bytes) : 0) + 256;
 }
 
 static cudaEvent_t g_stage_events[8];
@@ -1825,8 +1861,8 @@ static TcDebug g_dbg;
 static int g_stage_events_n = 0;
 
 struct SideStreams {
-    cudaStream_t enc = nullptr, sc = nullptr;
-    cudaEvent_t fork, join_enc, join_sc, enc_done[MAX_CHUNKS], mlp_done[MAX_CHUNKS];
+    cudaStream_t enc = nullptr, sc = nullptr, pk = nullptr;
+    cudaEvent_t fork, join_enc, join_sc, enc_done[MAX_CHUNKS], mlp_done[MAX_CHUNKS], fork_pk, packed;
 };
 
 static SideStreams &side_streams() {
@@ -1834,6 +1870,9 @@ static SideStreams &side_streams() {
     if (ss.enc == nullptr) {
         cudaStreamCreateWithFlags(&ss.enc, cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&ss.sc, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&ss.pk, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ss.fork_pk, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ss.packed, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ss.join_enc, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ss.join_sc, cudaEventDisableTiming);
@@ -1884,6 +1923,15 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
     if (prof) cudaEventRecord(pev[0], s);
     SideStreams &ss = side_streams();
     cudaStream_t se = nc > 1 ? ss.enc : s, sc = nc > 1 ? ss.sc : s;
+    if (p.v4 && !only) {
+        // the step's packed MLP weight image (pack_w4), on a side stream beside the encode: 8 small
+        // blocks in the shadow of the encoder kernel, joined before the MLP
+        cudaEventRecord(ss.fork_pk, s);
+        cudaStreamWaitEvent(ss.pk, ss.fork_pk, 0);
+        pack_w4_kernel<<<PACK_BLOCKS, 256, 0, ss.pk>>>(params + woff, tab.n_levels * tab.n_feat, p.sh.ninp, nn, nh,
+                                                      ws + p.off_img);
+        cudaEventRecord(ss.packed, ss.pk);
+    }
     if (nc > 1) {
         cudaEventRecord(ss.fork, s);
         cudaStreamWaitEvent(ss.enc, ss.fork, 0);
@@ -1921,9 +1969,11 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         const int gm = (int)(ct < p.grid_mlp ? ct : p.grid_mlp);
         if (p.v4) {
             const int64_t h_tile = (int64_t)(nh - 1) * p.sh4.h_tile_bytes;
+            if (c == 0) cudaStreamWaitEvent(s, ss.packed, 0);  // the weight image (forked before the encode)
             mlp_tc4_kernel<<<gm, M4_THREADS, p.sh4.smem_bytes, s>>>(
                 xtc, targets + r0, nb, 1.0 / (double)b_global, dscale, p.sh4, params + woff, loss_sum, dfeat + r0, b,
-                grads + woff, ws + p.off_h + t0 * h_tile, g_dbg.pred ? g_dbg.pred + r0 : nullptr, nan_state, woff);
+                grads + woff, ws + p.off_h + t0 * h_tile, g_dbg.pred ? g_dbg.pred + r0 : nullptr, nan_state, woff,
+                ws + p.off_img);
         } else {
             mlp_tc_kernel<<<gm, PP_THREADS, p.sh.smem_bytes, s>>>(xtc, targets + r0, nb, 1.0 / (double)b_global, dscale,
                                                                   p.sh, params + woff, loss_sum, dfeat + r0, b,
@@ -1944,7 +1994,8 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
 #define LAUNCH_SC(NFV)                                                                                             \
     case NFV:                                                                                                      \
         scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, sc>>>(cc, dfeat + r0, nb, b, tab, p.n_coarse,            \
-                                                                p.coarse_floats, grads, nan_state);            \
+                                                                p.coarse_floats, grads, nan_state,             \
+                                                                (nb % 32 == 0 && b % 32 == 0) ? 1 : 0);        \
         break;
             LAUNCH_SC(1)
             LAUNCH_SC(2)
@@ -2017,7 +2068,7 @@ extern "C" int nvol_train_tc_scatter(const float *coords, const float *dfeat, in
     case NFV:                                                                                                    \
         cudaFuncSetAttribute(scatter_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);        \
         scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, s>>>(coords, dfeat, b, stride, tab, p.n_coarse,      \
-                                                               p.coarse_floats, grads, nullptr);                \
+                                                               p.coarse_floats, grads, nullptr, 0);             \
         break;
         LAUNCH_SC1(1)
         LAUNCH_SC1(2)
