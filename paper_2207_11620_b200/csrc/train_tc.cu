@@ -1648,12 +1648,18 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
                                                                 const GridTables tab, int n_coarse, int coarse_floats,
                                                                 float *__restrict__ grads,
                                                                 const int64_t *__restrict__ nan_state,
-                                                                int discard_dfeat) {
+                                                                int discard_dfeat, int rep_floats, int rep) {
     if (nan_halted(nan_state)) return;
     extern __shared__ float acc_s[];
     const uint64_t keep = l2_evict_last();
-    for (int q = threadIdx.x; q < coarse_floats; q += SC_THREADS) acc_s[q] = 0.0f;
+    // the most contended coarse levels (the first rep_floats accumulators: a 125-entry level 0
+    // takes every sample's 8 corners) are replicated rep times, lane & (rep - 1) picking the copy,
+    // which divides the collisions of the shared-memory CAS loops (fp32 shared atomics are CAS)
+    const int rep_total = rep * rep_floats;
+    const int smem_floats = rep_total + (coarse_floats - rep_floats);
+    for (int q = threadIdx.x; q < smem_floats; q += SC_THREADS) acc_s[q] = 0.0f;
     __syncthreads();
+    float *const acc_rep = acc_s + ((threadIdx.x & 31) & (rep - 1)) * rep_floats;
     // One item = one sample x SC_LG consecutive levels (level-group-major, so a
     // warp shares its level constants): the coordinates and the group's
     // dL/dfeat are loaded once up front and the group's REDs issue back to
@@ -1691,7 +1697,9 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
             const bool dense = tab.dense[l] != 0;
             const Cell32 c = cell32(px, py, pz, res);
             if (l < n_coarse) {
-                float *gs = acc_s + tab.offset[l];  // shared-typed accumulators of the dense coarse levels
+                // shared-typed accumulators of the dense coarse levels
+                const int o = (int)tab.offset[l];
+                float *gs = o < rep_floats ? acc_rep + o : acc_s + rep_total + (o - rep_floats);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const uint32_t slot = slot32(c.cx + (k & 1), c.cy + ((k >> 1) & 1), c.cz + ((k >> 2) & 1), r1, mask,
@@ -1747,15 +1755,21 @@ __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__r
     __syncthreads();
     // coarse levels: one vector RED per 16-byte-aligned float quad per CTA (the flat
     // buffer may start 4/8/12 bytes past a 16-byte boundary: scalar head and tail)
+    auto cval = [&](int q) -> float {  // the CTA's sum of coarse accumulator q (copies in a fixed order)
+        if (q >= rep_floats) return acc_s[rep_total + (q - rep_floats)];
+        float v = 0.0f;
+        for (int c = 0; c < rep; ++c) v += acc_s[c * rep_floats + q];
+        return v;
+    };
     const int head = min(coarse_floats, (int)(((16 - (reinterpret_cast<uintptr_t>(grads) & 15)) & 15) >> 2));
     const int n4 = (coarse_floats - head) >> 2;
     for (int q = threadIdx.x; q < n4; q += SC_THREADS) {
-        const float *a = acc_s + head + 4 * q;
-        const float4 v = make_float4(a[0], a[1], a[2], a[3]);
-        if (v.x != 0.0f || v.y != 0.0f || v.z != 0.0f || v.w != 0.0f) red_add4(grads + head + 4 * q, v, keep);
+        const int q0 = head + 4 * q;
+        const float4 v = make_float4(cval(q0), cval(q0 + 1), cval(q0 + 2), cval(q0 + 3));
+        if (v.x != 0.0f || v.y != 0.0f || v.z != 0.0f || v.w != 0.0f) red_add4(grads + q0, v, keep);
     }
-    for (int q = threadIdx.x; q < head; q += SC_THREADS) red_add(grads + q, acc_s[q], keep);
-    for (int q = head + 4 * n4 + threadIdx.x; q < coarse_floats; q += SC_THREADS) red_add(grads + q, acc_s[q], keep);
+    for (int q = threadIdx.x; q < head; q += SC_THREADS) red_add(grads + q, cval(q), keep);
+    for (int q = head + 4 * n4 + threadIdx.x; q < coarse_floats; q += SC_THREADS) red_add(grads + q, cval(q), keep);
 }
 
 // ============================================================================ host side
@@ -1769,7 +1783,8 @@ struct TcPlan {
     TcShape sh;
     Tc4Shape sh4;
     bool v4;  // mlp_tc4_kernel (four slots, folded split-fp16 accumulator) takes this shape
-    int grid_mlp, grid_sc, n_coarse, coarse_floats, nchunks;
+    int grid_mlp, grid_sc, n_coarse, coarse_floats, nchunks, rep_floats, rep;
+    size_t sc_smem() const { return (size_t)(rep * rep_floats + (coarse_floats - rep_floats)) * 4; }
     int64_t ntiles, chunk_tiles, off_x, off_dfeat, off_h, off_img, total;
     float lo_scale() const { return v4 ? 1.0f : tc::kLoScale; }
 };
@@ -1830,6 +1845,25 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
         if (!tab.dense[l] || end * 4 > (int64_t)COARSE_BYTES) break;
         p.n_coarse = l + 1;
         p.coarse_floats = (int)end;
+    }
+    // replicated coarse levels (NVOL_SC_REP copies of the first NVOL_SC_REP_LEVELS levels)
+    static int rep_env = -1, rep_lv = -1;
+    if (rep_env < 0) {
+        const char *e = getenv("NVOL_SC_REP");
+        const char *f = getenv("NVOL_SC_REP_LEVELS");
+        rep_env = e ? atoi(e) : 8;
+        rep_lv = f ? atoi(f) : 2;
+        if (rep_env < 1) rep_env = 1;
+        while (rep_env & (rep_env - 1)) rep_env &= rep_env - 1;  // power of two
+        if (rep_env > 32) rep_env = 32;
+    }
+    p.rep = 1;
+    p.rep_floats = 0;
+    for (int l = 0; l < p.n_coarse && l < rep_lv; ++l) {
+        const int end = (int)(tab.offset[l] + tab.entries[l] * tab.n_feat);
+        if ((size_t)(rep_env * end + (p.coarse_floats - end)) * 4 > 200 * 1024) break;
+        p.rep_floats = end;
+        p.rep = rep_env;
     }
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
     p.off_x = 0;
@@ -1905,7 +1939,7 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         cudaFuncSetAttribute(mlp_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh4.smem_bytes);
     else
         cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p.sh.smem_bytes);
-    const size_t csm = (size_t)p.coarse_floats * 4;
+    const size_t csm = p.sc_smem();
     switch (tab.n_feat) {
         case 1: cudaFuncSetAttribute(scatter_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm); break;
         case 2: cudaFuncSetAttribute(scatter_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm); break;
@@ -1995,7 +2029,8 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
     case NFV:                                                                                                      \
         scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, sc>>>(cc, dfeat + r0, nb, b, tab, p.n_coarse,            \
                                                                 p.coarse_floats, grads, nan_state,             \
-                                                                (nb % 32 == 0 && b % 32 == 0) ? 1 : 0);        \
+                                                                (nb % 32 == 0 && b % 32 == 0) ? 1 : 0,         \
+                                                                p.rep_floats, p.rep);                          \
         break;
             LAUNCH_SC(1)
             LAUNCH_SC(2)
@@ -2061,14 +2096,15 @@ extern "C" int nvol_train_tc_scatter(const float *coords, const float *dfeat, in
         set_error("grid shape not supported by the tcgen05 path");
         return NVOL_EINVAL;
     }
-    const size_t csm = (size_t)p.coarse_floats * 4;
+    const size_t csm = p.sc_smem();
     cudaStream_t s = as_stream(stream);
     switch (n_feat) {
 #define LAUNCH_SC1(NFV)                                                                                          \
     case NFV:                                                                                                    \
         cudaFuncSetAttribute(scatter_kernel<NFV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);        \
         scatter_kernel<NFV><<<p.grid_sc, SC_THREADS, csm, s>>>(coords, dfeat, b, stride, tab, p.n_coarse,      \
-                                                               p.coarse_floats, grads, nullptr, 0);             \
+                                                               p.coarse_floats, grads, nullptr, 0, p.rep_floats, \
+                                                               p.rep);                                          \
         break;
         LAUNCH_SC1(1)
         LAUNCH_SC1(2)

@@ -502,11 +502,16 @@ def test_fused_adam_encode_tail(nv, name, batch, monkeypatch):
             assert pipe.launches_per_step() == 4
             torch.cuda.synchronize()
             assert int(pipe.work.abs().sum().item()) == 0        # work words re-armed
-            before = model._ws.clone()
+            # the encoder tile buffer (hi + lo fp16 tiles) at the head of the workspace; the rest is
+            # step scratch the kernels drop from L2 once dead (indeterminate by design)
+            ninp = -(-golden_config(golden(f"encode_{name}.npz"))["encoding"]["n_levels"]
+                     * golden_config(golden(f"encode_{name}.npz"))["encoding"]["n_features_per_level"] // 16) * 16
+            tiles = 2 * 128 * ninp * 2 * -(-batch // 128)
+            before = model._ws[:tiles].clone()
             c, t = pipe.bufs[pipe.done & 1]                       # the look-ahead batch (step 10)
             model.fwd_bwd_device(c, t, pipe.acc, b_global=pipe.B, flags=TRAIN_ENCODE_ONLY)
             torch.cuda.synchronize()
-            assert torch.equal(before, model._ws)
+            assert torch.equal(before, model._ws[:tiles])
     assert losses["1"][0] == pytest.approx(losses["0"][0], rel=1e-6)
     np.testing.assert_allclose(losses["1"], losses["0"], rtol=2e-2)
 
