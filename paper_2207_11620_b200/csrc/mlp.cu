@@ -5,6 +5,7 @@
 // These kernels back the reference-shaped API (float32 and the float64
 // gradient-check builds); the training hot path uses the fused kernels in
 // train_fused.cu instead.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -406,6 +407,161 @@ __global__ void nan_scan_kernel(const float *__restrict__ g, int64_t n, const Gr
     }
 }
 
+// adam_step_kernel's update streamed by the bulk-copy (TMA) engine: each CTA walks chunks of
+// AD_CH floats of the four flat arrays through an AD_ST-deep ring of shared-memory stages --
+// one thread issues 4 bulk loads per chunk (p, m, v evict-first; g evict-last, it stays in L2
+// for the next scatter), the CTA updates the stage in place and one thread bulk-stores it back
+// (p, m, v, and g = 0).  The DMA engine keeps ~100 KB in flight per CTA without occupying
+// registers, which is what the HBM-bound update needs.  Same arithmetic, same NaN contract and
+// same step bookkeeping (ticket) as adam_step_kernel.
+constexpr int AD_CH = 2048;     // floats per array per chunk (8 KB)
+constexpr int AD_ST = 3;        // ring depth
+constexpr int AD_THREADS = 256; // 2 float4 per thread per array per chunk
+
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void *dst, const void *src, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"((uint32_t)__cvta_generic_to_shared(src)), "r"(bytes), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(AD_THREADS) adam_tma_kernel(
+    float *__restrict__ p, float *__restrict__ g, float *__restrict__ m, float *__restrict__ v, int64_t n,
+    const float *__restrict__ sched, int64_t sched_len, int64_t *__restrict__ step_counter, float b1, float omb1,
+    float b2, float omb2, float eps, float l2, int64_t *__restrict__ nan_state, double *__restrict__ loss_acc,
+    double *__restrict__ losses, int64_t t0, int64_t cap, double inv_b, uint32_t *__restrict__ ticket) {
+    extern __shared__ __align__(128) float ring[];  // [AD_ST][4][AD_CH]: p, g, m, v
+    __shared__ uint64_t full[AD_ST];
+    if (nan_halted(nan_state)) return;
+    const int tid = threadIdx.x;
+    const int64_t tc = *step_counter;
+    const int64_t t = tc >= sched_len ? sched_len - 1 : tc;
+    const float lr = sched[3 * t], c1 = sched[3 * t + 1], c2 = sched[3 * t + 2];
+    const int64_t lim = nan_limit(nan_state);
+    const int64_t head = min(n, (int64_t)(((128 - (reinterpret_cast<uintptr_t>(p) & 127)) & 127) >> 2));
+    const int64_t nbody = ((n - head) >> 2) << 2;  // float4-aligned body, whole 16-byte units
+    const int64_t nch = (nbody + AD_CH - 1) / AD_CH;
+    int64_t bad = kNanNone;
+    auto one = [&](float &P, float &G, float &M, float &V, int64_t q) {
+        if (q >= lim) return;
+        if (isnan(G)) {
+            bad = min(bad, q);
+            return;
+        }
+        adam_one<float>(P, G, M, V, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+    };
+    const uint64_t first = l2_evict_first(), keep = l2_evict_last();
+    float *arr[4] = {p + head, g + head, m + head, v + head};
+    if (tid == 0) {
+        for (int s = 0; s < AD_ST; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int s, int64_t c) {  // thread 0: chunk c -> stage s
+        const int64_t off = c * AD_CH;
+        const uint32_t bytes = (uint32_t)(min((int64_t)AD_CH, nbody - off) * 4);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[s])),
+                     "r"(4 * bytes)
+                     : "memory");
+        for (int a = 0; a < 4; ++a)
+            bulk_g2s_hint(ring + ((int64_t)s * 4 + a) * AD_CH, arr[a] + off, bytes, &full[s], a == 1 ? keep : first);
+    };
+    int64_t c = blockIdx.x;
+    if (tid == 0)
+        for (int s = 0; s < AD_ST; ++s)
+            if (c + (int64_t)s * gridDim.x < nch) issue(s, c + (int64_t)s * gridDim.x);
+    uint32_t par = 0;
+    for (int k = 0; c < nch; ++k, c += gridDim.x) {
+        const int s = k % AD_ST;
+        {
+            const uint32_t addr = (uint32_t)__cvta_generic_to_shared(&full[s]);
+            const uint32_t ph = (par >> s) & 1u;
+            asm volatile(
+                "{\n\t.reg .pred P1;\n\tW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W_%=;\n\t}\n" ::"r"(addr),
+                "r"(ph)
+                : "memory");
+            par ^= 1u << s;
+        }
+        const int64_t off = c * AD_CH;
+        const int cnt = (int)min((int64_t)AD_CH, nbody - off);
+        float4 *sp = reinterpret_cast<float4 *>(ring + ((int64_t)s * 4 + 0) * AD_CH);
+        float4 *sg = reinterpret_cast<float4 *>(ring + ((int64_t)s * 4 + 1) * AD_CH);
+        float4 *sm = reinterpret_cast<float4 *>(ring + ((int64_t)s * 4 + 2) * AD_CH);
+        float4 *sv = reinterpret_cast<float4 *>(ring + ((int64_t)s * 4 + 3) * AD_CH);
+        for (int j = tid; j < cnt / 4; j += AD_THREADS) {
+            float4 P = sp[j], G = sg[j], M = sm[j], V = sv[j];
+            const int64_t q = head + off + 4 * j;
+            if (q + 3 < lim && !(isnan(G.x) | isnan(G.y) | isnan(G.z) | isnan(G.w))) {
+                adam_one<float>(P.x, G.x, M.x, V.x, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+                adam_one<float>(P.y, G.y, M.y, V.y, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+                adam_one<float>(P.z, G.z, M.z, V.z, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+                adam_one<float>(P.w, G.w, M.w, V.w, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+            } else {
+                one(P.x, G.x, M.x, V.x, q);
+                one(P.y, G.y, M.y, V.y, q + 1);
+                one(P.z, G.z, M.z, V.z, q + 2);
+                one(P.w, G.w, M.w, V.w, q + 3);
+            }
+            sp[j] = P;
+            sg[j] = G;
+            sm[j] = M;
+            sv[j] = V;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> bulk stores
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t bytes = (uint32_t)cnt * 4u;
+            for (int a = 0; a < 4; ++a) bulk_s2g_hint(arr[a] + off, ring + ((int64_t)s * 4 + a) * AD_CH, bytes, a == 1 ? keep : first);
+            bulk_commit();
+            const int64_t nc = c + (int64_t)AD_ST * gridDim.x;
+            if (nc < nch) {
+                bulk_wait_read0();  // stage s has been read out by its stores
+                issue(s, nc);
+            }
+        }
+    }
+    if (tid == 0) bulk_wait0();  // the stores are complete before the ticket publishes the step
+    // scalar head / tail (block 0)
+    if (blockIdx.x == 0) {
+        const int64_t tail0 = head + nbody;
+        for (int64_t jj = tid; jj < head + (n - tail0); jj += AD_THREADS) {
+            const int64_t q = jj < head ? jj : tail0 + (jj - head);
+            float P = p[q], G = g[q], M = m[q], V = v[q];
+            one(P, G, M, V, q);
+            p[q] = P;
+            g[q] = G;
+            m[q] = M;
+            v[q] = V;
+        }
+    }
+    if (bad != kNanNone) nan_mark(nan_state, bad);
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+            __threadfence();
+            *ticket = 0u;
+            if (nan_limit(nan_state) != kNanNone) {
+                nan_state[1] = 1;  // halt: the step is not recorded, t does not advance
+                return;
+            }
+            const int64_t kk = tc - t0;
+            if (losses && kk >= 0 && kk < cap) losses[kk] = *reinterpret_cast<volatile double *>(loss_acc) * inv_b;
+            if (loss_acc) *loss_acc = 0.0;
+            *step_counter = tc + 1;
+        }
+    }
+}
+
 __global__ void step_advance_kernel(int64_t *counter) { *counter += 1; }
 
 __global__ void loss_record_kernel(double *acc, double *losses, const int64_t *counter, int64_t t0, int64_t cap,
@@ -500,7 +656,31 @@ int nvol_adam_train_step(float *p, float *g, float *m, float *v, int64_t n, cons
     NVOL_REQUIRE(((uintptr_t)p & 127) == ((uintptr_t)g & 127) && ((uintptr_t)p & 127) == ((uintptr_t)m & 127) &&
                      ((uintptr_t)p & 127) == ((uintptr_t)v & 127) && ((uintptr_t)p & 3) == 0,
                  "flat Adam buffers must share their alignment modulo 128 bytes");
-    adam_step_kernel<<<stream_grid((n + 3) / 4), 256, 0, as_stream(stream)>>>(
+    static int tma = -1;  // NVOL_ADAM_TMA=0: the register-streaming adam_step_kernel (A/B measurements)
+    if (tma < 0) {
+        const char *e = getenv("NVOL_ADAM_TMA");
+        tma = (e && e[0] == '0') ? 0 : 1;
+    }
+    cudaStream_t s = as_stream(stream);
+    if (tma) {
+        const size_t smem = (size_t)AD_ST * 4 * AD_CH * 4;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(adam_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, adam_tma_kernel, AD_THREADS, smem);
+        const int64_t nch = (n / AD_CH) + 1;
+        const int64_t grid = std::max((int64_t)1, std::min((int64_t)sms * std::max(per, 1), nch));
+        adam_tma_kernel<<<(unsigned)grid, AD_THREADS, smem, s>>>(p, g, m, v, n, sched, sched_len, step_counter, beta1,
+                                                                 one_minus_beta1, beta2, one_minus_beta2, eps, l2,
+                                                                 nan_state, loss_acc, losses, t0, cap, inv_b, ticket);
+        return check_launch("adam_train_step");
+    }
+    adam_step_kernel<<<stream_grid((n + 3) / 4), 256, 0, s>>>(
         p, g, m, v, n, sched, sched_len, step_counter, beta1, one_minus_beta1, beta2, one_minus_beta2, eps, l2,
         nan_state, loss_acc, losses, t0, cap, inv_b, ticket);
     return check_launch("adam_train_step");

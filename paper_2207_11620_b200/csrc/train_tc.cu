@@ -1851,7 +1851,7 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
     if (rep_env < 0) {
         const char *e = getenv("NVOL_SC_REP");
         const char *f = getenv("NVOL_SC_REP_LEVELS");
-        rep_env = e ? atoi(e) : 8;
+        rep_env = e ? atoi(e) : 4;
         rep_lv = f ? atoi(f) : 2;
         if (rep_env < 1) rep_env = 1;
         while (rep_env & (rep_env - 1)) rep_env &= rep_env - 1;  // power of two

@@ -91,6 +91,45 @@ def test_adam_bit_exact(nv):
         assert not g.any()
 
 
+@pytest.mark.parametrize("lead", [0, 1, 3])
+def test_pipeline_adam_bit_exact(nv, oracle, lead):
+    """nvol_adam_train_step (the step pipeline's Adam: bulk-copy streamed, flat buffers that
+    start 0-3 floats past a 16-byte boundary, many chunks plus scalar head and tail) is
+    bit-identical to the reference's adam_step on every element; the step is recorded and the
+    counter advances; the consumed gradient is zeroed."""
+    from paper_2207_11620_b200 import _lib
+    n = 3_000_007
+    r = np.random.default_rng(lead)
+    arrs = [r.normal(0, 0.1, n).astype(np.float32), r.normal(0, 1e-3, n).astype(np.float32),
+            r.normal(0, 1e-4, n).astype(np.float32), np.abs(r.normal(0, 1e-6, n)).astype(np.float32)]
+    arrs[1][::5] = 0.0
+    dev = []
+    for a in arrs:
+        buf = torch.zeros(n + 8, dtype=torch.float32, device="cuda")[lead:lead + n]
+        buf.copy_(torch.from_numpy(a))
+        dev.append(buf)
+    t = 2500
+    opt = oracle.AdamState(t=t)
+    sc = oracle.adam_scalars(opt)               # (lr, b1, 1-b1, b2, 1-b2, c1, c2, eps, l2) as float32
+    sched = torch.tensor([float(sc[0]), float(sc[5]), float(sc[6])], dtype=torch.float32, device="cuda")
+    counter = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ticket = torch.zeros(1, dtype=torch.int32, device="cuda")
+    acc = torch.full((1,), 3.0, dtype=torch.float64, device="cuda")
+    losses = torch.zeros(2, dtype=torch.float64, device="cuda")
+    ns = torch.tensor([(1 << 63) - 1, 0], dtype=torch.int64, device="cuda")
+    _lib.call("nvol_adam_train_step", *[_lib.ptr(x) for x in dev], n, _lib.ptr(sched), 1, _lib.ptr(counter),
+              float(sc[1]), float(sc[2]), float(sc[3]), float(sc[4]), float(sc[7]), float(sc[8]), _lib.ptr(ns),
+              _lib.ptr(acc), _lib.ptr(losses), 0, 2, 0.5, _lib.ptr(ticket), _lib.stream())
+    pw, gw, mw, vw = (x.copy() for x in arrs)
+    opt.m, opt.v = [mw], [vw]
+    oracle.adam_step(opt, [pw], [gw])
+    np.testing.assert_array_equal(dev[0].cpu().numpy(), pw)
+    np.testing.assert_array_equal(dev[2].cpu().numpy(), mw)
+    np.testing.assert_array_equal(dev[3].cpu().numpy(), vw)
+    assert not dev[1].any().item()
+    assert int(counter.item()) == 1 and float(losses[0].item()) == 1.5 and float(acc.item()) == 0.0
+
+
 def test_adam_known_answers(nv):
     from paper_2207_11620_b200.network import OptimizerState, adam_step
     opt = OptimizerState(l2_reg=0.0)
