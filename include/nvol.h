@@ -405,6 +405,19 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
 int nvol_macrocell_ranges(const float *vals, int64_t dx, int64_t dy, int64_t dz, int64_t ng,
                           int32_t clip, float *lo, float *hi, void *stream);
 
+/* rng.py RngStream.uniform / _render_kernels.py:26-49 _u01: the path tracer's counter
+ * stream (SplitMix64-style avalanche of (seed, frame, pixel, event), 24-bit float32 in
+ * [0, 1)) for n keys: out[i] = u01(seed, frame, pixel[i], event[i]).  Device arrays. */
+int nvol_rng_u01(uint64_t seed, uint64_t frame, const int64_t *pixel, const int64_t *event, int64_t n,
+                 float *out, void *stream);
+
+/* macrocell.py:159-181 dda_traverse (_render_kernels.py:153-188 dda_collect): the macro-cell
+ * cells a float64 ray [host] ray = {ox, oy, oz, dx, dy, dz} walks over [t0, t1] with cell size
+ * ng on a gx x gy x gz grid: cells (cap x 3, int64) and (s_enter, s_exit) pairs (cap x 2,
+ * float64), *count records; zero-length grazes dropped.  Device outputs. */
+int nvol_dda_collect(const double *ray, double t0, double t1, double ng, int64_t gx, int64_t gy,
+                     int64_t gz, int64_t cap, int64_t *cells, double *ts, int64_t *count, void *stream);
+
 /* macrocell.py:136-156 macrocell_set_tf: mu = max TF opacity over [lo,hi]
  * (np.interp semantics, float64) * density_scale; untouched cells -> 0.
  * op_v / op_a [host]: opacity control points. */

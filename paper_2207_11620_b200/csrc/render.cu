@@ -24,6 +24,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "field_exact.cuh"
 
@@ -772,6 +774,70 @@ __device__ __forceinline__ float u01(uint64_t seed, uint64_t frame, int64_t pixe
     return __fmul_rn((float)(h >> 40), 1.0f / 16777216.0f);
 }
 
+// The counter stream on its own (rng.py RngStream.uniform): the same u01 the path tracer draws
+__global__ void rng_u01_kernel(uint64_t seed, uint64_t frame, const int64_t *__restrict__ pixel,
+                               const int64_t *__restrict__ event, int64_t n, float *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = u01(seed, frame, pixel[i], event[i]);
+}
+
+// macrocell.py:159-181 dda_traverse / _render_kernels.py:153-188 dda_collect: every
+// (cell, s_enter, s_exit) the macro-cell DDA walks along [t0, t1] of one float64 ray,
+// zero-length grazes dropped (the segments tile the interval); the walk of cell_entry /
+// cell_advance in float64 from the caller's origin / direction.  One thread.
+__global__ void dda_collect_kernel(double ox, double oy, double oz, double dx, double dy, double dz, double t0,
+                                   double t1, double ng, int64_t gx, int64_t gy, int64_t gz, int64_t cap,
+                                   int64_t *__restrict__ cells, double *__restrict__ ts, int64_t *__restrict__ count) {
+    const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
+    const int64_t gd[3] = {gx, gy, gz};
+    int64_t c[3], st[3];
+    double tm[3], td[3];
+    for (int a = 0; a < 3; ++a) {
+        const double p = o[a] + t0 * d[a];
+        c[a] = clampl((int64_t)floor(p / ng), 0, gd[a] - 1);
+        if (d[a] > 0.0) {
+            st[a] = 1;
+            tm[a] = t0 + ((double)(c[a] + 1) * ng - p) / d[a];
+            td[a] = ng / d[a];
+        } else if (d[a] < 0.0) {
+            st[a] = -1;
+            tm[a] = t0 + ((double)c[a] * ng - p) / d[a];
+            td[a] = -ng / d[a];
+        } else {
+            st[a] = 0;
+            tm[a] = INFINITY;
+            td[a] = INFINITY;
+        }
+    }
+    double cur = t0;
+    int64_t k = 0;
+    for (;;) {
+        double se = tm[0];
+        if (tm[1] < se) se = tm[1];
+        if (tm[2] < se) se = tm[2];
+        if (se > t1) se = t1;
+        if (se > cur && k < cap) {
+            for (int a = 0; a < 3; ++a) cells[3 * k + a] = clampl(c[a], 0, gd[a] - 1);
+            ts[2 * k] = cur;
+            ts[2 * k + 1] = se;
+            ++k;
+            cur = se;
+        }
+        if (se >= t1 || k >= cap) break;
+        if (tm[0] <= tm[1] && tm[0] <= tm[2]) {
+            c[0] += st[0];
+            tm[0] += td[0];
+        } else if (tm[1] <= tm[2]) {
+            c[1] += st[1];
+            tm[1] += td[1];
+        } else {
+            c[2] += st[2];
+            tm[2] += td[2];
+        }
+    }
+    *count = k;
+}
+
 // _render_kernels.py:92-138 _dda_enter for the PT state
 __device__ void pt_dda_enter(const RmScene &S, PtState &P) {
     const double t0 = P.t, ng = S.ng;
@@ -1512,6 +1578,24 @@ int nvol_macrocell_ranges(const float *vals, int64_t dx, int64_t dy, int64_t dz,
     mc_ranges_kernel<<<(unsigned)(gx * gy * gz), 256, 0, as_stream(stream)>>>(vals, dx, dy, dz, ng, gx, gy, gz, clip,
                                                                                lo, hi);
     return check_launch("macrocell_ranges");
+}
+
+int nvol_rng_u01(uint64_t seed, uint64_t frame, const int64_t *pixel, const int64_t *event, int64_t n, float *out,
+                 void *stream) {
+    NVOL_REQUIRE(n >= 0 && (n == 0 || (pixel && event && out)), "bad arguments");
+    if (n == 0) return NVOL_OK;
+    rng_u01_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, as_stream(stream)>>>(seed, frame, pixel,
+                                                                                                      event, n, out);
+    return check_launch("rng_u01");
+}
+
+int nvol_dda_collect(const double *ray, double t0, double t1, double ng, int64_t gx, int64_t gy, int64_t gz,
+                     int64_t cap, int64_t *cells, double *ts, int64_t *count, void *stream) {
+    NVOL_REQUIRE(ray && cells && ts && count && cap >= 1 && ng > 0.0 && gx >= 1 && gy >= 1 && gz >= 1,
+                 "bad arguments");
+    dda_collect_kernel<<<1, 1, 0, as_stream(stream)>>>(ray[0], ray[1], ray[2], ray[3], ray[4], ray[5], t0, t1, ng, gx,
+                                                       gy, gz, cap, cells, ts, count);
+    return check_launch("dda_collect");
 }
 
 int nvol_macrocell_set_tf(const float *lo, const float *hi, int64_t ncell, const double *op_v, const double *op_a,

@@ -9,6 +9,7 @@ tensors shaped (gz, gy, gx).
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -119,3 +120,31 @@ def macrocell_set_tf(grid: MacroCellGrid, tf: TransferFunction) -> None:
     cv = (np.ctypeslib.as_ctypes(pv), np.ctypeslib.as_ctypes(pa))
     _lib.call("nvol_macrocell_set_tf", _lib.ptr(grid.value_lo), _lib.ptr(grid.value_hi), grid.value_lo.numel(),
               cv[0], cv[1], len(pv), float(tf.density_scale), _lib.ptr(grid.mu_max), _lib.stream())
+
+
+def dda_traverse(grid: MacroCellGrid, origin, direction, visitor) -> None:
+    """Walk the cells pierced by the ray inside the volume box, front to back (macrocell.py:159-181).
+
+    visitor(cell_xyz (3,) int64, s_enter, s_exit) -> bool; returning False stops the walk.  The
+    segments tile [t_min, t_max] of the ray / volume intersection exactly.  The walk runs on the
+    device (nvol_dda_collect), in float64 like the marcher's cell stepping."""
+    from .camera import intersect_aabb
+    dx, dy, dz = grid.vol_dims
+    hit = intersect_aabb(origin, direction, (dx, dy, dz))
+    if hit is None:
+        return
+    t0, t1 = hit
+    gx, gy, gz = grid.grid_dims
+    cap = gx + gy + gz + 4
+    dev = _lib.device()
+    cells = torch.empty((cap, 3), dtype=torch.int64, device=dev)
+    ts = torch.empty((cap, 2), dtype=torch.float64, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    ray = (ctypes.c_double * 6)(*[float(x) for x in (*origin, *direction)])
+    _lib.call("nvol_dda_collect", ray, float(t0), float(t1), float(grid.n_g), gx, gy, gz, cap, _lib.ptr(cells),
+              _lib.ptr(ts), _lib.ptr(count), _lib.stream())
+    n = int(count.item())
+    c, t = cells[:n].cpu().numpy(), ts[:n].cpu().numpy()
+    for i in range(n):
+        if visitor(c[i], float(t[i, 0]), float(t[i, 1])) is False:
+            return
