@@ -1,0 +1,3 @@
+export PYTHONUNBUFFERED=1
+python tools/psnr_engines.py --cfg cfg2 --dims 48 --batch 16384 --steps 200 --seeds 10
+python tools/psnr_engines.py --cfg cfg2 --dims 256 --batch 65536 --steps 3000 --seeds 8
