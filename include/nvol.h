@@ -405,6 +405,13 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
 int nvol_macrocell_ranges(const float *vals, int64_t dx, int64_t dy, int64_t dz, int64_t ng,
                           int32_t clip, float *lo, float *hi, void *stream);
 
+/* tracking.py adaptive_step / correct_opacity: the marcher's own device formulas over n
+ * inputs x.  which 0: adaptive step, x = majorant mu, (a, b, c) = (s1, s2, p)
+ * (_render_kernels.py:244-253); which 1: opacity correction 1 - (1 - x)^(a / b), a = s-bar,
+ * b = s1 (_render_kernels.py:364-392).  Device arrays. */
+int nvol_march_formula(int32_t which, const float *x, int64_t n, float a, float b, float c, float *out,
+                       void *stream);
+
 /* rng.py RngStream.uniform / _render_kernels.py:26-49 _u01: the path tracer's counter
  * stream (SplitMix64-style avalanche of (seed, frame, pixel, event), 24-bit float32 in
  * [0, 1)) for n keys: out[i] = u01(seed, frame, pixel[i], event[i]).  Device arrays. */

@@ -69,6 +69,7 @@ _SIGS = {
     "nvol_macrocell_ranges": [P, I64, I64, I64, I64, I32, P, P, P],
     "nvol_macrocell_set_tf": [P, P, I64, P, P, I32, F64, P, P],
     "nvol_rng_u01": [U64, U64, P, P, I64, P, P],
+    "nvol_march_formula": [I32, P, I64, F32, F32, F32, P, P],
     "nvol_dda_collect": [P, F64, F64, F64, I64, I64, I64, I64, P, P, P, P],
 }
 _RESTYPES = {"nvol_last_error": ctypes.c_char_p, "nvol_train_workspace_bytes": I64, "nvol_mlp_image_bytes": I64,

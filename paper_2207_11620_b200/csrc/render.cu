@@ -774,6 +774,16 @@ __device__ __forceinline__ float u01(uint64_t seed, uint64_t frame, int64_t pixe
     return __fmul_rn((float)(h >> 40), 1.0f / 16777216.0f);
 }
 
+// The marcher's step-size and opacity formulas on their own (tracking.py adaptive_step /
+// correct_opacity): which = 0: adaptive(x, s1 = a, s2 = b, p = c); which = 1: opacity x
+// resampled from step s1 = b to step sbar = a, 1 - (1 - x)^(sbar / s1) -- the device functions
+// the ray marcher evaluates (_render_kernels.py:244-253, 364-392).
+__global__ void march_formula_kernel(int which, const float *__restrict__ x, int64_t n, float a, float b, float c,
+                                     float *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = which == 0 ? adaptive(x[i], a, b, c) : 1.0f - powd(1.0f - x[i], a / b);
+}
+
 // The counter stream on its own (rng.py RngStream.uniform): the same u01 the path tracer draws
 __global__ void rng_u01_kernel(uint64_t seed, uint64_t frame, const int64_t *__restrict__ pixel,
                                const int64_t *__restrict__ event, int64_t n, float *__restrict__ out) {
@@ -1578,6 +1588,14 @@ int nvol_macrocell_ranges(const float *vals, int64_t dx, int64_t dy, int64_t dz,
     mc_ranges_kernel<<<(unsigned)(gx * gy * gz), 256, 0, as_stream(stream)>>>(vals, dx, dy, dz, ng, gx, gy, gz, clip,
                                                                                lo, hi);
     return check_launch("macrocell_ranges");
+}
+
+int nvol_march_formula(int32_t which, const float *x, int64_t n, float a, float b, float c, float *out, void *stream) {
+    NVOL_REQUIRE((which == 0 || which == 1) && n >= 0 && (n == 0 || (x && out)), "bad arguments");
+    if (n == 0) return NVOL_OK;
+    march_formula_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, as_stream(stream)>>>(which, x, n, a,
+                                                                                                            b, c, out);
+    return check_launch("march_formula");
 }
 
 int nvol_rng_u01(uint64_t seed, uint64_t frame, const int64_t *pixel, const int64_t *event, int64_t n, float *out,

@@ -486,11 +486,13 @@ def test_tcgen05_step_shape_sweep(nv, nn, nh, levels, feat):
         assert rel_l2(a, b) < 2e-2, i
 
 
+@pytest.mark.timeout(600)
 def test_tcgen05_training_converges(nv):
-    """cfg2-encoder training with the tcgen05 engine tracks the fp32 engine.
-    Single trajectories are chaotic under float-atomic summation order
-    (the reference itself spreads by dB between seeds), so the bar
-    is on the mean PSNR over three sampler seeds per engine."""
+    """cfg2-encoder training with the tcgen05 engine tracks the fp32 engine.  Single
+    trajectories are chaotic under float-atomic summation order (the reference
+    itself spreads by dB between seeds; measured here 0.6-1.0 dB std over ten 200-step runs
+    for either engine), so the bar is on the mean PSNR over eight sampler seeds per engine:
+    the two means agree within max(0.5 dB, 2 standard errors of their difference)."""
     from paper_2207_11620_b200 import fields, trainer
     from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
     from paper_2207_11620_b200.sampler import InCoreSampler
@@ -500,17 +502,16 @@ def test_tcgen05_training_converges(nv):
     res = {}
     for mode in (0, MODE_TCGEN05):
         runs = []
-        for seed in (1, 2, 3):
+        for seed in range(1, 9):
             m = build_model(cfg, dims=(48, 48, 48), seed=0)
             m.train_mode = mode
             trainer.train(m, InCoreSampler(fld, seed=seed), steps=200)
             runs.append(psnr(fld, trainer.decode(m, dims=(48, 48, 48))))
-        res[mode] = float(np.mean(runs))
-    assert res[MODE_TCGEN05] > 20.0
-    # one-sided: half-precision operands must not cost more than 1.5 dB against the fp32
-    # engine (three 200-step runs are chaotic to ~1.5 dB either way; the 0.1 dB parity bar
-    # is test_psnr_ensemble_within_0p1_db's, on the SURVEY protocol)
-    assert res[MODE_TCGEN05] > res[0] - 1.5, res
+        res[mode] = np.asarray(runs)
+    a, b = res[MODE_TCGEN05], res[0]
+    assert a.mean() > 20.0
+    se = float(np.sqrt(a.var(ddof=1) / a.size + b.var(ddof=1) / b.size))
+    assert abs(a.mean() - b.mean()) <= max(0.5, 2 * se), (a.mean(), b.mean(), se)
 
 
 @pytest.mark.parametrize("name,batch", [("cfg2", 8192), ("odd", 4000), ("cfg1", 1000)])

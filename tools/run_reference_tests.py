@@ -63,7 +63,7 @@ def run(tag: str):
     res = {"tag": tag, "totals": totals, "tests": rows,
            "how": "reference test files run unmodified; `neuralvol` -> tools/refshim (aliases onto "
                   "paper_2207_11620_b200 + the numba FFI over the C ABI); adapter (tools/refshim/refshim_adapter.py): "
-                  "numpy reads CUDA tensors, numpy/list values assign into CUDA tensors, Tensor.copy = clone"}
+                  "numpy reads CUDA tensors, numpy/list values assign into CUDA tensors, Tensor.copy = clone, Tensor.astype -> numpy"}
     (out / f"reference_tests_{tag}.json").write_text(json.dumps(res, indent=1))
     lines = [f"# Reference test files against paper_2207_11620_b200 ({tag})", "",
              f"Totals: {totals}", "", "| file | test | outcome | detail |", "|---|---|---|---|"]
