@@ -54,6 +54,7 @@ def member(seed: int, steps: int, cfg_name: str = "cfg2") -> None:
     PART.mkdir(exist_ok=True)
     (PART / f"{cfg_name}_seed{seed}.json").write_text(json.dumps(
         {"seed": seed, "steps": steps, "psnr": val, "final_loss": float(hist.losses[-1]),
+         "losses": [float(x) for x in hist.losses],
          "train_s": t1 - t0, "decode_s": time.time() - t1,
          "openblas_num_threads": os.environ.get("OPENBLAS_NUM_THREADS", "unset")}))
     print("seed", seed, "psnr", val, flush=True)
