@@ -284,14 +284,18 @@ def run_ours(args):
         exchange = {"ms": float(t.item()), "bytes_per_rank": 4 * model.flat_size * (2 if pipe.sharded else 1),
                     "kind": "NCCL reduce-scatter + all-gather (sharded optimizer)" if pipe.sharded
                     else "NCCL all-reduce", "share_of_step": float(t.item()) / ms_per_step}
+    # the kernels the step launches (nvol_train_fwd_bwd / nvol_adam_train_step pick them; the
+    # NVOL_MLP4 / NVOL_ADAM_TMA switches select the previous designs for A/B runs)
+    K_ADAM = "adam_step_kernel" if os.environ.get("NVOL_ADAM_TMA", "1") == "0" else "adam_tma_kernel"
+    K_MLP = "mlp_tc_kernel" if os.environ.get("NVOL_MLP4", "1") == "0" else "mlp_tc4_kernel"
     t_sample = float(_event_ms(torch, sample_fn)[0])
     t_adam = float(_event_ms(torch, adam_fn)[0])
-    kernels = {"sample_incore_kernel": t_sample, "adam_step_kernel": t_adam}
+    kernels = {"sample_incore_kernel": t_sample, K_ADAM: t_adam}
     if pipe.fused:
         kernels["adam_encode_kernel"] = float(_event_ms(torch, fused_fn)[0])
     if args.mode == 1:
         st = _event_ms(torch, stages_fn, nev=5)
-        kernels.update({"encode_tiles_kernel": float(st[0]), "mlp_tc_kernel": float(st[1] - st[0]),
+        kernels.update({"encode_tiles_kernel": float(st[0]), K_MLP: float(st[1] - st[0]),
                         "scatter_kernel": float(st[2] - st[1])})
     n_flat = model.flat_size
     adam_bytes = 32 * n_flat
@@ -299,7 +303,7 @@ def run_ours(args):
     mlp_flops = 3 * 2 * B * (32 * 64 + 3 * 64 * 64 + 64)
     # roofline of the dominant single kernel
     dom = max(kernels, key=kernels.get)
-    per_unit = {"adam_step_kernel": (adam_bytes, "hbm", "32 B/param x 12,181,396 flat params"),
+    per_unit = {K_ADAM: (adam_bytes, "hbm", "32 B/param x 12,181,396 flat params"),
                 "scatter_kernel": (2 * gather_bytes, "hbm", "16 levels x 8 corners x 2 feat x 4 B x 2 (RMW) per sample"),
                 "encode_tiles_kernel": (gather_bytes + B * 12 + B * 64 * 2, "hbm",
                                         "1,024 B gathered + 12 B coords + 128 B fp16 tiles per sample"),
@@ -332,7 +336,7 @@ def run_ours(args):
     roof["step_frac_of_hbm"] = step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm
     roof["kernel_ms"] = kernels
     if args.mode == 1:
-        roof["mlp_tc_tflops"] = mlp_flops / (kernels["mlp_tc_kernel"] * 1e-3) / 1e12
+        roof["mlp_tc_tflops"] = mlp_flops / (kernels[K_MLP] * 1e-3) / 1e12
     # every step kernel against the peak that bounds it; the L2 denominators are
     # measured live (nvol_l2_probe: random 8-byte gathers / float2 REDs into a
     # 48 MB L2-resident region), the HBM and tensor ones are MEASURED_PEAKS.json
@@ -350,14 +354,13 @@ def run_ours(args):
         rl["scatter_kernel"] = {"bound": "l2 RED rate", "achieved_gops": sc_ops / (kernels["scatter_kernel"] * 1e-3) / 1e9,
                                 "peak_gops": l2_red, "basis": "B x 13 global levels x 8 corner updates"}
         rl["scatter_kernel"]["frac"] = rl["scatter_kernel"]["achieved_gops"] / l2_red
-        rl["mlp_tc_kernel"] = {"bound": "tensor", "achieved_tflops": roof["mlp_tc_tflops"], "peak_tflops": tc_sus,
+        rl[K_MLP] = {"bound": "tensor", "achieved_tflops": roof["mlp_tc_tflops"], "peak_tflops": tc_sus,
                                "frac": roof["mlp_tc_tflops"] / tc_sus,
                                "note": "M=128 x N=64 tcgen05 MMAs issue at <= 2725 MAC/clk/SM (67% of the 4096 peak, "
                                        "tools/micro/mma_bench.cu); the chain of 8 dependent layer phases per tile is "
                                        "latency-bound"}
-    rl["adam_step_kernel"] = {"bound": "hbm", "achieved_gbs": adam_bytes / (kernels["adam_step_kernel"] * 1e-3) / 1e9,
-                              "peak_gbs": hbm}
-    rl["adam_step_kernel"]["frac"] = rl["adam_step_kernel"]["achieved_gbs"] / hbm
+    rl[K_ADAM] = {"bound": "hbm", "achieved_gbs": adam_bytes / (kernels[K_ADAM] * 1e-3) / 1e9, "peak_gbs": hbm}
+    rl[K_ADAM]["frac"] = rl[K_ADAM]["achieved_gbs"] / hbm
     if "adam_encode_kernel" in kernels:
         t_ae = kernels["adam_encode_kernel"]
         rl["adam_encode_kernel"] = {"bound": "hbm (Adam stream) + l2 gathers (encode), overlapped",

@@ -1069,11 +1069,21 @@ constexpr int M4_THREADS = M4_WARPS * 32;
 
 struct Tc4Shape {
     int nin, ninp, nn, nh, accw, slots, relu_out, loss_kind;
+    int split;  // 1: split-fp16 forward (hi*W_hi + lo*W_hi + hi*W_lo); 0: plain fp16 forward (hi*W_hi)
     uint32_t o_w[MAX_NH], o_wl[MAX_NH], o_wout, o_dwout, o_p[M4_SLOTS], o_q[M4_SLOTS], smem_bytes, half_bytes;
     uint32_t xhalf, t_acc[M4_SLOTS], t_dw[MAX_NH], t_alloc;
     uint32_t img_bytes;              // the packed weight image [0, img_bytes) of shared memory (pack_w4)
     int64_t w_floats, h_tile_bytes;  // per tile, per stored activation h_1..h_{nh-1} in the scratch
 };
+
+static bool mlp_split_enabled() {
+    static int on = -1;  // NVOL_MLP_SPLIT=0: plain fp16 training forward (A/B measurements)
+    if (on < 0) {
+        const char *e = getenv("NVOL_MLP_SPLIT");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
 
 static int build_shape4(Tc4Shape &s, int m, int n, int nn, int nh, int relu_out, int loss_kind) {
     s.nin = m * n;
@@ -1082,6 +1092,7 @@ static int build_shape4(Tc4Shape &s, int m, int n, int nn, int nh, int relu_out,
     s.nh = nh;
     s.relu_out = relu_out;
     s.loss_kind = loss_kind;
+    s.split = mlp_split_enabled() ? 1 : 0;
     if (nh < 1 || nh > MAX_NH || !(nn == 16 || nn == 32 || nn == 64)) return 0;
     if (s.ninp > 2 * nn || s.ninp > 128) return 0;
     s.accw = max(nn, s.ninp);
@@ -1272,11 +1283,11 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     __syncthreads();  // (the weight staging area is dead from here: the X loads below overwrite it)
     tc::fence_after();
     const uint32_t tmem = tmem_base_sh;
-    auto load_x = [&](int t, int64_t tile) {  // X hi -> P[t], X lo -> Q[t]
+    auto load_x = [&](int t, int64_t tile) {  // X hi -> P[t], X lo -> Q[t] (split forward only)
         const uint8_t *src = xtiles + tile * xtile_bytes;
-        tc::mbar_arrive_expect_tx(&bar_x[t], 2 * sh.xhalf);
+        tc::mbar_arrive_expect_tx(&bar_x[t], (sh.split ? 2 : 1) * sh.xhalf);
         tc::bulk_g2s(smem + sh.o_p[t], src, sh.xhalf, &bar_x[t]);
-        tc::bulk_g2s(smem + sh.o_q[t], src + sh.xhalf, sh.xhalf, &bar_x[t]);
+        if (sh.split) tc::bulk_g2s(smem + sh.o_q[t], src + sh.xhalf, sh.xhalf, &bar_x[t]);
     };
     // h_j (j >= 1: the scratch written by the forward epilogue; j = 0: the X hi tile) -> Q[t]
     auto load_h = [&](int t, int64_t tile, int j) {
@@ -1348,8 +1359,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                         for (int k = 0; k < win / 16; ++k) {
                             const uint64_t dk = (uint64_t)(k * 16);
                             tc::mma_f16(acc, ah + dk, bh + dk, idesc_f, k > 0);
-                            tc::mma_f16(acc, al + dk, bh + dk, idesc_f, 1);
-                            tc::mma_f16(acc, ah + dk, bl + dk, idesc_f, 1);
+                            if (sh.split) {
+                                tc::mma_f16(acc, al + dk, bh + dk, idesc_f, 1);
+                                tc::mma_f16(acc, ah + dk, bl + dk, idesc_f, 1);
+                            }
                         }
                         tc::mma_commit(&bar_acc[t]);
                     }
@@ -1454,8 +1467,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                     const uint32_t o0 = tc::tile_off(s, c, NN), o1 = tc::tile_off(s, c + 8, NN);
                     *reinterpret_cast<uint4 *>(pbuf + o0) = h0;
                     *reinterpret_cast<uint4 *>(pbuf + o1) = h1;
-                    *reinterpret_cast<uint4 *>(qbuf + o0) = l0;
-                    *reinterpret_cast<uint4 *>(qbuf + o1) = l1;
+                    if (sh.split) {
+                        *reinterpret_cast<uint4 *>(qbuf + o0) = l0;
+                        *reinterpret_cast<uint4 *>(qbuf + o1) = l1;
+                    }
                     uint8_t *g = hs + (int64_t)i * sh.h_tile_bytes;
                     st_global_v4(g + o0, h0);
                     st_global_v4(g + o1, h1);

@@ -284,13 +284,15 @@ class StepPipeline:
             return 1 + 5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 + 1
         if self.fused:
             return 4    # sample (next step's), MLP, scatter, Adam + next encode
-        # sample (next step's, overlapped), nchunks x (encode, MLP, scatter), Adam step
+        # sample (next step's, overlapped), the MLP weight image (pack_w4, side stream; four-slot
+        # MLP kernel), nchunks x (encode, MLP, scatter), Adam step
         # (chunk plan of train_tc.cu make_plan: NVOL_TRAIN_CHUNKS, default 1)
         ntiles = (self.b + 127) // 128
         nc = max(1, min(int(os.environ.get("NVOL_TRAIN_CHUNKS", "1")), 4, ntiles))
         ct = (ntiles + nc - 1) // nc
         nc = (ntiles + ct - 1) // ct
-        return 1 + 3 * nc + 1
+        pack = 0 if os.environ.get("NVOL_MLP4", "1") == "0" else 1
+        return 1 + pack + 3 * nc + 1
 
     def step(self, n: int = 1) -> None:
         """Enqueue n steps (no host synchronisation)."""
