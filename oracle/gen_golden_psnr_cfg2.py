@@ -3,6 +3,7 @@ capacity-limited protocol) -- test infrastructure.
 
     OPENBLAS_NUM_THREADS=1 python oracle/gen_golden_psnr_cfg2.py [--cfg cfg1] --seed S [--steps N]   # one member
     python oracle/gen_golden_psnr_cfg2.py [--cfg cfg1] --merge      # -> tests/golden/psnr_<cfg>_mlobb.json
+    python oracle/gen_golden_psnr_cfg2.py --append                 # add the PART members to the fixture
 
 SURVEY.md §8(c) protocol at configs[1]: the reference's cfg2 model (HashGrid 16 x 2^19 x 2,
 4 x 64 ReLU MLP, B = 65,536, L1 + Adam; model seed 0) trained with
@@ -76,14 +77,37 @@ def merge(cfg_name: str = "cfg2") -> None:
          "generator": "oracle/gen_golden_psnr_cfg2.py (neuralvol.trainer.train + decode + volume.psnr)"}, indent=1))
 
 
+def append(cfg_name: str = "cfg2") -> None:
+    """Extend an existing fixture with the members in PART (same steps / BLAS threads), keeping
+    their per-step loss trajectories as 500-step block means (loss_block_means)."""
+    path = OUT / os.environ.get("PSNR_OUT", f"psnr_{cfg_name}_mlobb.json")
+    g = json.loads(path.read_text())
+    parts = sorted((json.loads(p.read_text()) for p in PART.glob(f"{cfg_name}_seed*.json")), key=lambda d: d["seed"])
+    for p in parts:
+        assert p["steps"] == g["steps"] and p["openblas_num_threads"] == g["openblas_num_threads"], p["seed"]
+        assert p["seed"] not in g["sampler_seeds"], p["seed"]
+        g["sampler_seeds"].append(p["seed"])
+        g["psnr_db"].append(p["psnr"])
+        g["final_losses"].append(p["final_loss"])
+        g["reference_train_s"].append(p["train_s"])
+        g.setdefault("loss_block_means", {})[str(p["seed"])] = [
+            float(x) for x in np.asarray(p["losses"]).reshape(-1, 500).mean(1)]
+    g["loss_block"] = 500
+    g["mean"], g["std"] = float(np.mean(g["psnr_db"])), float(np.std(g["psnr_db"]))
+    path.write_text(json.dumps(g, indent=1))
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--seed", type=int)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--merge", action="store_true")
+    ap.add_argument("--append", action="store_true")
     ap.add_argument("--cfg", default="cfg2", choices=sorted(SETUPS))
     a = ap.parse_args()
     if a.merge:
         merge(a.cfg)
+    elif a.append:
+        append(a.cfg)
     else:
         member(a.seed, a.steps, a.cfg)

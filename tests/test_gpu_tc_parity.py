@@ -267,16 +267,22 @@ def test_tc_gradients_per_element(cfg2_case):
 
 @pytest.mark.timeout(900)
 def test_psnr_ensemble_cfg2(nv):
-    """PSNR at the bench config: the cfg2 model trained by the benchmarked tcgen05 engine for the
-    fixture's 3000 steps on mlobb 256^3 against the reference's own ensemble
-    (tests/golden/psnr_cfg2_mlobb.json, oracle/gen_golden_psnr_cfg2.py, OPENBLAS_NUM_THREADS=1).
+    """PSNR and loss trajectory at the bench config: the cfg2 model trained by the benchmarked
+    tcgen05 engine for the fixture's 3000 steps on mlobb 256^3 against the reference's own
+    ensemble (tests/golden/psnr_cfg2_mlobb.json, oracle/gen_golden_psnr_cfg2.py,
+    OPENBLAS_NUM_THREADS=1: 13 reference runs, ~50 CPU-minutes each).
 
     The north-star bar is 0.1 dB on the ensemble mean.  At this configuration the reference is
-    itself chaotic: its six seeds spread over ~4 dB (std ~1.3 dB, a bimodal plateau), so a 0.1 dB
-    difference of means is not resolvable from six reference runs.  The bar applied is therefore
-    max(0.1 dB, 2 standard errors of the difference of the two ensemble means) -- the 0.1 dB bar
-    wherever the reference's spread can resolve it (cfg1: test_psnr_ensemble_within_0p1_db) --
-    with the device ensemble over the reference's seeds plus 26 more (32 runs, ~0.5 s each)."""
+    itself chaotic (Adam with epsilon 1e-15 at lr 5e-3): single runs decorrelate after ~50 steps,
+    visit a low-loss basin and leave it again, and end 40.7-45.8 dB apart (std 1.24 dB over 13
+    seeds; its first six seeds alone averaged 43.1 dB, the next seven 41.7 dB), so a 0.1 dB
+    difference of means is not resolvable from the reference's runs.  The PSNR bar applied is
+    therefore max(0.1 dB, 2 standard errors of the difference of the two ensemble means) -- the
+    0.1 dB bar wherever the reference's spread resolves it (cfg1: test_psnr_ensemble_within_0p1_db)
+    -- with the device ensemble over the reference's seeds plus more (32 runs, ~0.5 s each).
+    The training trajectory is compared the same way, block by block: the ensemble mean of the
+    mean loss over each 500-step block against the reference runs that recorded their losses
+    (fixture loss_block_means), within max(1% of the reference, 2 standard errors)."""
     _need_tc()
     from paper_2207_11620_b200 import fields, trainer
     from paper_2207_11620_b200.model import MODE_TCGEN05, build_model
@@ -289,17 +295,24 @@ def test_psnr_ensemble_cfg2(nv):
     dims = tuple(g["dims"])
     fld = fields.rasterize(g["field"], dims, host=True)
     seeds = list(g["sampler_seeds"]) + [100 + k for k in range(32 - len(g["sampler_seeds"]))]
-    res = []
+    res, blocks = [], []
     for seed in seeds:
         m = build_model(g["config"], dims=dims, seed=g["model_seed"])
         m.train_mode = MODE_TCGEN05
-        trainer.train(m, InCoreSampler(fld, seed=seed), steps=g["steps"])
+        h = trainer.train(m, InCoreSampler(fld, seed=seed), steps=g["steps"])
+        blocks.append(np.asarray(h.losses).reshape(-1, g["loss_block"]).mean(1))
         res.append(psnr(fld, trainer.decode(m, dims=dims)))
     ref = np.asarray(g["psnr_db"])
     gpu = np.asarray(res)
     se = float(np.sqrt(ref.var(ddof=1) / ref.size + gpu.var(ddof=1) / gpu.size))
     d = float(gpu.mean() - ref.mean())
+    rb = np.asarray(list(g["loss_block_means"].values()))
+    gb = np.asarray(blocks)
+    bse = np.sqrt(rb.var(0, ddof=1) / rb.shape[0] + gb.var(0, ddof=1) / gb.shape[0])
+    bd = gb.mean(0) - rb.mean(0)
     print({"gpu_mean": float(gpu.mean()), "gpu_std": float(gpu.std(ddof=1)), "ref_mean": float(ref.mean()),
            "ref_std": float(ref.std(ddof=1)), "delta_db": d, "two_se_db": 2 * se,
-           "gpu_on_ref_seeds": [float(x) for x in gpu[:ref.size]]})
+           "gpu_on_ref_seeds": [float(x) for x in gpu[:ref.size]],
+           "loss_blocks_gpu": gb.mean(0).tolist(), "loss_blocks_ref": rb.mean(0).tolist(), "two_se": (2 * bse).tolist()})
     assert abs(d) <= max(0.1, 2 * se), (d, se, list(gpu), list(ref))
+    assert np.all(np.abs(bd) <= np.maximum(0.01 * rb.mean(0), 2 * bse)), (bd, bse)
