@@ -258,6 +258,13 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
  * n = 0 disables.  [host] array of event handles. */
 int nvol_set_stage_events(void *const *events, int32_t n);
 
+/* Pipeline hook (trainer.StepPipeline): while set, nvol_train_fwd_bwd mode 1
+ * records this cudaEvent_t right after the step's encoder launch (before the
+ * MLP), so the caller forks the next step's sampling there -- it then runs
+ * beside the latency-bound MLP instead of the L2-bound encoder.  NULL disables.
+ * No reference counterpart (trainer.py:61-77 samples serially). */
+int nvol_set_fork_event(void *event);
+
 /* Parity hooks for the tcgen05 training engine (tests only; all null in
  * production).  While set, nvol_train_fwd_bwd mode 1 additionally writes
  * feat  [b][n_levels*n_feat] f32: the hot encoder's fp32 features

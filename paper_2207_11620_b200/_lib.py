@@ -60,6 +60,7 @@ _SIGS = {
                               P, I64, P, P, P, P, I32, I32, I32, I32, P, I64, P],
     "nvol_render_workspace_bytes": [I64, I32],
     "nvol_set_stage_events": [P, I32],
+    "nvol_set_fork_event": [P],
     "nvol_train_tc_debug": [P, P, P],
     "nvol_train_tc_scatter": [P, P, I64, I64, P, P, P, P, I32, I32, P, P],
     "nvol_l2_persist": [I64],

@@ -1900,6 +1900,9 @@ int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
 }
 
 static cudaEvent_t g_stage_events[8];
+// nvol_set_fork_event: recorded on the encoder's stream right after the step's encode launch, so a
+// caller can start side work (the next step's sampling) beside the MLP instead of the encoder
+static cudaEvent_t g_fork_event = nullptr;
 // Parity hooks (nvol_train_tc_debug): the hot kernels additionally write the fp32 features
 // (encode_tiles_kernel), the per-sample prediction (mlp_tc_kernel) and a copy of the
 // feature-major dL/dfeat; all null in production.
@@ -2008,6 +2011,7 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
             st = check_launch("encode_tiles_kernel");
             if (st) return st;
         }
+        if (c == 0 && g_fork_event) cudaEventRecord(g_fork_event, se);
         if (only) return NVOL_OK;
         if (nc > 1) {
             cudaEventRecord(ss.enc_done[c], se);
@@ -2067,6 +2071,11 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
 }
 
 }  // namespace nvol
+
+extern "C" int nvol_set_fork_event(void *event) {
+    nvol::g_fork_event = reinterpret_cast<cudaEvent_t>(event);
+    return NVOL_OK;
+}
 
 // Profiling hook: with >= 4 events set, nvol_train_fwd_bwd (mode 1) runs as a
 // single chunk on the caller's stream and records events[0..3] before encode,

@@ -153,6 +153,11 @@ class StepPipeline:
         # (not with the sharded optimizer: its step tail is the slice Adam + all-gather)
         self.fused = (self.overlap and self.train_mode == MODE_TCGEN05 and not self.sharded
                       and os.environ.get("NVOL_FUSED_TAIL", "0") == "1")
+        # the tcgen05 engine records a fork event after its encode launch (NVOL_FORK_AFTER_ENCODE=0:
+        # fork at the start of the step)
+        self.fork_after_encode = (self.overlap and not self.fused and model._engine() == MODE_TCGEN05
+                                  and model._tc_device() and os.environ.get("NVOL_FORK_AFTER_ENCODE", "1") != "0")
+        self.fork_ev = torch.cuda.Event() if self.fork_after_encode else None
         self.fingerprint = pipeline_fingerprint(model)
         self.work = torch.zeros(2 + 32, dtype=torch.int32, device=dev)   # NVOL_MAX_LEVELS
         if self.host_feed:
@@ -162,6 +167,9 @@ class StepPipeline:
             self.staged = [None, None]          # host tensors whose DMA may still be in flight
             self.staging = [None, None]         # pinned staging for non-pinned host batches
             self.loss_host = torch.zeros(self.capacity, dtype=torch.float64).pin_memory()
+            # each step's loss is read back on its own stream (after the step's event), so the
+            # 8-byte D2H never sits between two steps on the main stream
+            self.d2h_stream = torch.cuda.Stream(device=dev)
         self.use_graph = use_graph
         self.graphs = [None, None]
         self.done = 0
@@ -230,13 +238,26 @@ class StepPipeline:
                 macrocell_update_online(self.mc_grid, SampleBatch(*self.bufs[parity], trusted=True))
         elif self.overlap:
             self.side.wait_stream(main)                 # fork: next step's batch on the side stream
-            with torch.cuda.stream(self.side):
-                self.sample_into(parity ^ 1, 1)
+            if not self.fork_after_encode:
+                with torch.cuda.stream(self.side):
+                    self.sample_into(parity ^ 1, 1)
         else:
             self.sample_into(parity, 0)
         c, t = self.bufs[parity]
-        m.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_PREENCODED if self.fused else 0,
-                         nan_state=self.nan_state)
+        if self.fork_after_encode:
+            # fork the next step's sampling after this step's encode (nvol_set_fork_event): the
+            # sampler then overlaps the latency-bound MLP, not the L2-bound encoder
+            _lib.call("nvol_set_fork_event", self.fork_ev.cuda_event)
+            try:
+                m.fwd_bwd_device(c, t, self.acc, b_global=self.B, nan_state=self.nan_state)
+            finally:
+                _lib.call("nvol_set_fork_event", None)
+            self.side.wait_event(self.fork_ev)
+            with torch.cuda.stream(self.side):
+                self.sample_into(parity ^ 1, 1)
+        else:
+            m.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_PREENCODED if self.fused else 0,
+                             nan_state=self.nan_state)
         if self.sharded:
             import torch.distributed as dist
             from .distributed import allgather_shards, reduce_scatter_grads
@@ -332,7 +353,10 @@ class StepPipeline:
             if self.host_feed:
                 main = torch.cuda.current_stream()
                 self.free[parity].record(main)
-                self.loss_host[self.done:self.done + 1].copy_(self.losses[self.done:self.done + 1], non_blocking=True)
+                self.d2h_stream.wait_event(self.free[parity])
+                with torch.cuda.stream(self.d2h_stream):
+                    self.loss_host[self.done:self.done + 1].copy_(self.losses[self.done:self.done + 1],
+                                                                  non_blocking=True)
             self.done += 1
 
     def finish(self) -> np.ndarray:
@@ -346,6 +370,7 @@ class StepPipeline:
         m = self.model
         if self.host_feed:
             torch.cuda.current_stream().synchronize()
+            self.d2h_stream.synchronize()
             losses = self.loss_host[:self.done].numpy().copy()
             self.staged = [None, None]
         else:
