@@ -622,7 +622,7 @@ def render_bench(torch, args, rank=0, world=1):
     from paper_2207_11620_b200.distributed import render_tile
     import torch.distributed as dist
     res["sharding"] = f"image row tiles over {world} GPU(s), frame time = max over ranks"
-    for arch, mode in (("wavefront", "tensor"), ("wavefront", "exact"), ("reference", "exact")):
+    for arch, mode in (("wavefront", "tensor"), ("reference", "tensor"), ("wavefront", "exact"), ("reference", "exact")):
         render_tile(m, tf, cam, cfg, grid, rank, world, arch, mode)       # warm-up
         torch.cuda.synchronize()
         ts = []

@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "field_exact.cuh"
+#include "infer_tile.cuh"
 
 namespace nvol {
 
@@ -465,6 +466,86 @@ __global__ void __launch_bounds__(FE_THREADS) rm_mega_kernel(RayState *__restric
         }
     }
     atomicAdd(evals, ev);
+}
+
+// render_reference / rm_reference with the tcgen05 evaluator: the in-shader marcher on the tensor
+// cores.  Persistent CTAs (two per SM); each CTA keeps 256 rays in flight, one per thread, and pulls
+// new hit rays from a global queue as its rays finish.  A round: every ray marches to its next
+// sample (rm_next / coord_at, ending and replacing rays as the reference's loop does), the CTA
+// evaluates the 256 samples as two tensor-core tiles (infer_tile: the encode and split-fp16 MLP of
+// the batched evaluator, bit-identical values), and every ray composites its own value
+// (rm_consume) -- the reference's per-ray sequence sample -> Phi -> consume, so images equal the
+// wavefront's bit for bit, with no ray records, staging or compaction in global memory.
+template <int NF>
+__global__ void __launch_bounds__(IT_THREADS, 2) rm_tc_kernel(const int32_t *__restrict__ hitpix, int64_t n,
+                                                              int32_t *__restrict__ queue, const CamParams cam,
+                                                              const RmScene S, const float *__restrict__ mu,
+                                                              const float *__restrict__ params, const GridTables tab,
+                                                              const InferShape sh, const uint8_t *__restrict__ wimg,
+                                                              float *__restrict__ img,
+                                                              unsigned long long *__restrict__ evals) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ float s_xyz[3 * IT_THREADS], s_val[IT_THREADS];
+    __shared__ uint8_t s_ok[IT_THREADS];
+    infer_prologue(smem, sh, wimg, &mbar, &tmem_base_sh);
+    const int tid = threadIdx.x, s = tid & (IT_TILE - 1), h = tid >> 7;
+    const uint32_t tmem = tmem_base_sh;
+    uint32_t phase = 0;
+    RayState R;
+    bool have = false, drained = false;
+    float ts = 0.0f;
+    unsigned long long ev = 0;
+    for (;;) {
+        bool staged = false;
+        float x = 0.5f, y = 0.5f, z = 0.5f;
+        while (!drained) {
+            if (!have) {
+                const int32_t q = atomicAdd(queue, 1);
+                if (q >= n) {
+                    drained = true;
+                    break;
+                }
+                make_ray(cam, S, hitpix[q], R);  // a hit ray (ray_hits_kernel + selection)
+                have = true;
+            }
+            const float t = rm_next(S, mu, R);
+            if (t < 0.0f) {
+                if (rm_phase_end(S, R)) {
+                    rm_final(S, R, img);
+                    have = false;
+                }
+                continue;
+            }
+            ts = t;
+            coord_at(S, R, t, x, y, z);
+            staged = true;
+            break;
+        }
+        s_xyz[3 * tid] = x;
+        s_xyz[3 * tid + 1] = y;
+        s_xyz[3 * tid + 2] = z;
+        s_ok[tid] = staged ? 1 : 0;
+        if (!__syncthreads_or(staged ? 1 : 0)) break;  // (also publishes s_xyz / s_ok)
+        for (int half = 0; half < 2; ++half) {         // the rays of threads [128 half, 128 half + 128)
+            const int r = half * IT_TILE + s;
+            const float v = infer_tile<NF, true>(smem, sh, tab, params, s_xyz[3 * r], s_xyz[3 * r + 1],
+                                                 s_xyz[3 * r + 2], s_ok[r] != 0, tmem, &mbar, phase);
+            if (h == 0) s_val[r] = v;
+        }
+        __syncthreads();
+        if (staged) {
+            ++ev;
+            if (rm_consume(S, R, s_val[tid], ts, R.sbar) && rm_phase_end(S, R)) {
+                rm_final(S, R, img);
+                have = false;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) ev += __shfl_down_sync(0xffffffffu, ev, o);
+    if ((tid & 31) == 0 && ev) atomicAdd(evals, ev);
+    infer_teardown(tmem, sh);
 }
 
 // ----------------------------------------------------------------------------- wavefront stages
@@ -1393,7 +1474,20 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
     cudaStreamSynchronize(s);
     // ray records up front for the path tracer and the in-shader marcher; the wavefront
     // ray march generates each ray inside its first rm_step (no record write + read)
-    if (n > 0 && (S.pathtrace || architecture == 1)) {
+    // the in-shader marcher on the tensor cores (architecture 1, tcgen05 evaluator): rays are
+    // generated inside rm_tc_kernel, so no ray records
+    InferShape ish{};
+    const bool tc_inshader = architecture == 1 && eval_mode == 1 && !use_grid && !S.pathtrace && n_layers >= 2 &&
+                             widths[n_layers] == 1 && widths[0] == n_levels * n_feat &&
+                             build_infer_shape(ish, n_levels, n_feat, widths[1], n_layers - 1, relu_out) &&
+                             [&] {
+                                 for (int i = 1; i < n_layers; ++i)
+                                     if (widths[i] != widths[1]) return false;
+                                 for (int l = 0; l < n_levels; ++l)
+                                     if (level_entries[l] >= (1ll << 31)) return false;
+                                 return true;
+                             }();
+    if (n > 0 && (S.pathtrace || (architecture == 1 && !tc_inshader))) {
         raygen_kernel<<<(unsigned)((n + RG_THREADS - 1) / RG_THREADS), RG_THREADS, 0, s>>>(C, S, w.ids[1], n, w.rays);
         st = check_launch("raygen");
         if (st) return st;
@@ -1416,7 +1510,35 @@ int nvol_render(const double *cam_params, const double *render_params, const flo
         stats_out[2] = (int64_t)vi;
         return check_launch("render (pathtrace)");
     }
-    if (architecture == 1) {
+    if (tc_inshader) {
+        if (n > 0) {
+            NVOL_REQUIRE(mlp_image, "the tcgen05 evaluator needs an mlp_image scratch buffer (nvol_mlp_image_bytes)");
+            st = pack_mlp_image(weights, ish.nin, ish.ninp, widths[1], n_layers - 1, ish.o_w, ish.o_wout,
+                                (uint8_t *)mlp_image, s, ish.o_wlo);
+            if (st) return st;
+            cudaMemsetAsync(w.coord_rays, 0, 4, s);  // the ray queue
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int64_t ctas = (n + IT_THREADS - 1) / IT_THREADS;
+            const int grid = (int)(ctas < 2 * sms ? ctas : 2 * sms);
+            auto go = [&](auto kern) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ish.smem_bytes);
+                kern<<<grid, IT_THREADS, ish.smem_bytes, s>>>(w.ids[1], n, w.coord_rays, C, S, mu, params, tab, ish,
+                                                              (const uint8_t *)mlp_image, img, w.evals);
+            };
+            switch (n_feat) {
+                case 1: go(rm_tc_kernel<1>); break;
+                case 2: go(rm_tc_kernel<2>); break;
+                case 4: go(rm_tc_kernel<4>); break;
+                default: go(rm_tc_kernel<8>); break;
+            }
+            st = check_launch("rm_tc_kernel");
+            if (st) return st;
+        }
+        if (max_hist > 0) alive_hist[0] = (int32_t)n;
+        iters = 1;
+    } else if (architecture == 1) {
         // in-shader: one thread per ray to completion
         if (n > 0) {
             int wtot = 0;

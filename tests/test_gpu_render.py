@@ -92,6 +92,32 @@ def test_in_shader_equals_wavefront_and_reference(scene):
     assert img_psnr(a, z["img_megakernel"]) >= 50.0
 
 
+@pytest.mark.parametrize("mode", ["raymarch", "raymarch_shadow"])
+def test_tensor_in_shader_equals_tensor_wavefront(scene, mode):
+    """The in-shader marcher on the tensor cores (rm_tc_kernel: rays march in place, each round's
+    128 samples of a CTA evaluated as one tcgen05 tile) runs the reference's per-ray sequence
+    sample -> Phi -> consume with the batched evaluator's values: the image equals the tensor
+    wavefront's bit for bit, and it evaluates exactly the samples the rays consume (no samples
+    staged past termination), i.e. no more than the wavefront and no fewer than K = 1."""
+    from paper_2207_11620_b200.camera import default_camera
+    from paper_2207_11620_b200.render import RenderConfig, render
+    z, dims, model, grid, tf, cam = scene
+    cam = default_camera(dims, 320, 180)
+    model.infer_mode = "tensor"
+    try:
+        out = {}
+        for arch, k in (("reference", 8), ("wavefront", 8), ("wavefront", 1)):
+            st = []
+            img = render(model, tf, cam, RenderConfig(mode=mode, use_macrocells=True, k_batch=k), arch, grid=grid,
+                         stats_out=st)
+            out[(arch, k)] = (img, st[0].evals)
+    finally:
+        model.infer_mode = "exact"
+    np.testing.assert_array_equal(out[("reference", 8)][0], out[("wavefront", 8)][0])
+    assert out[("reference", 8)][1] == out[("wavefront", 1)][1]
+    assert out[("reference", 8)][1] <= out[("wavefront", 8)][1]
+
+
 def test_k_batching_is_scheduling_only(scene):
     # test_render.py:116-128
     from paper_2207_11620_b200.render import RenderConfig, render
