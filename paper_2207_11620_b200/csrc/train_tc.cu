@@ -1902,7 +1902,7 @@ int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
 static cudaEvent_t g_stage_events[8];
 // nvol_set_fork_event: recorded on the encoder's stream right after the step's encode launch, so a
 // caller can start side work (the next step's sampling) beside the MLP instead of the encoder
-static cudaEvent_t g_fork_event = nullptr;
+static thread_local cudaEvent_t g_fork_event = nullptr;
 // Parity hooks (nvol_train_tc_debug): the hot kernels additionally write the fp32 features
 // (encode_tiles_kernel), the per-sample prediction (mlp_tc_kernel) and a copy of the
 // feature-major dL/dfeat; all null in production.
