@@ -34,15 +34,18 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
         for (int c = 0; c < 4; ++c) acc[a][c] = (T)0;
     for (int64_t k0 = kbeg; k0 < kend; k0 += 16) {
         for (int q = threadIdx.x; q < 16 * 64; q += 256) {
-            int kk = q / 64, mm = q % 64;
-            int64_t gm = m0 + mm, gk = k0 + kk;
+            // consecutive threads walk the operand's contiguous dimension (k for a row-major A /
+            // transposed B, m / n otherwise), so every warp load is a few full sectors
+            const int ka = TA ? q / 64 : q % 16, ma = TA ? q % 64 : q / 16;
+            const int64_t gm = m0 + ma, gka = k0 + ka;
             T va = (T)0;
-            if (gm < M && gk < kend) va = TA ? A[gk * lda + gm] : A[gm * lda + gk];
-            As[kk][mm] = va;
-            int64_t gn = n0 + mm;
+            if (gm < M && gka < kend) va = TA ? A[gka * lda + gm] : A[gm * lda + gka];
+            As[ka][ma] = va;
+            const int kb = TB ? q % 16 : q / 64, nb = TB ? q / 16 : q % 64;
+            const int64_t gn = n0 + nb, gkb = k0 + kb;
             T vb = (T)0;
-            if (gn < N && gk < kend) vb = TB ? B[gn * ldb + gk] : B[gk * ldb + gn];
-            Bs[kk][mm] = vb;
+            if (gn < N && gkb < kend) vb = TB ? B[gn * ldb + gkb] : B[gkb * ldb + gn];
+            Bs[kb][nb] = vb;
         }
         __syncthreads();
 #pragma unroll
@@ -82,15 +85,26 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
     }
 }
 
+// C += sum_z part[z] in a fixed order (deterministic): block (32 x 8) -- 32 consecutive outputs
+// (coalesced rows of the partials) x 8 interleaved z-subsequences, folded in z-subsequence order
 template <typename T>
-__global__ void splitk_reduce_kernel(const T *__restrict__ part, int nz, int64_t M, int64_t N, T *__restrict__ C,
-                                     int64_t ldc) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M * N) return;
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const T *__restrict__ part, int nz, int64_t M, int64_t N,
+                                                            T *__restrict__ C, int64_t ldc) {
+    __shared__ T sums[8][32];
+    const int64_t i = (int64_t)blockIdx.x * 32 + threadIdx.x;
+    const int64_t mn = M * N;
     T acc = (T)0;
-    for (int z = 0; z < nz; ++z) acc += part[(int64_t)z * M * N + i];
-    const int64_t r = i / N, c = i - r * N;
-    C[r * ldc + c] += acc;
+    if (i < mn)
+        for (int z = threadIdx.y; z < nz; z += 8) acc += part[(int64_t)z * mn + i];
+    sums[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y == 0 && i < mn) {
+        T t = sums[0][threadIdx.x];
+#pragma unroll
+        for (int y = 1; y < 8; ++y) t += sums[y][threadIdx.x];
+        const int64_t r = i / N, c = i - r * N;
+        C[r * ldc + c] += t;
+    }
 }
 
 template <typename T, bool TA, bool TB>
@@ -99,17 +113,19 @@ static int gemm(int64_t M, int64_t N, int64_t K, const T *A, int64_t lda, const 
     dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), 1);
     int64_t tiles = (int64_t)grid.x * grid.y;
     if (accumulate && !relu && tiles < 296 && K > 4096) {
-        int64_t split = min((int64_t)1024, max((int64_t)1, (296 * 4) / tiles));
-        split = min(split, (K + 1023) / 1024);
+        // the weight-gradient reductions over the batch (M, N <= a few tiles, K = B): split K into
+        // chunks of ~128 rows so the whole GPU works on them (B = 65,536: 512 CTAs), each chunk's
+        // partial summed afterwards in chunk order -- one pass, no atomics, deterministic
+        const int64_t split = min((int64_t)2048, max((int64_t)1, (K + 127) / 128));
         grid.z = (unsigned)split;
     }
-    if (grid.z > 1 && g_deterministic) {
+    if (grid.z > 1) {
         // ordered split-K: partials [split][M][N], then C += sum_z in z order
         T *part = nullptr;
         if (cudaMallocAsync((void **)&part, sizeof(T) * grid.z * M * N, s) != cudaSuccess)
             return check_launch("gemm partials alloc");
         gemm_kernel<T, TA, TB><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, accumulate, relu, part);
-        splitk_reduce_kernel<T><<<grid_for(M * N, 256), 256, 0, s>>>(part, (int)grid.z, M, N, C, ldc);
+        splitk_reduce_kernel<T><<<(unsigned)((M * N + 31) / 32), dim3(32, 8), 0, s>>>(part, (int)grid.z, M, N, C, ldc);
         cudaFreeAsync(part, s);
         return check_launch("gemm (ordered split-K)");
     }

@@ -42,6 +42,24 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
                     cudaStream_t s);
 int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh);
 
+// [b][w] -> [w][b] (the hot scatter reads dL/dfeat feature-major)
+__global__ void transpose_kernel(const float *__restrict__ in, float *__restrict__ out, int64_t b, int w) {
+    __shared__ float t[32][33];
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
+    const int c0 = blockIdx.y * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t r = r0 + k;
+        const int c = c0 + threadIdx.x;
+        t[k][threadIdx.x] = (r < b && c < w) ? in[r * w + c] : 0.0f;
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int c = c0 + k;
+        const int64_t r = r0 + threadIdx.x;
+        if (c < w && r < b) out[(int64_t)c * b + r] = t[threadIdx.x][k];
+    }
+}
+
 }  // namespace nvol
 
 using namespace nvol;
@@ -54,6 +72,8 @@ int nvol_mlp_forward(int64_t, int32_t, const int32_t *, const void *const *, voi
 int nvol_mlp_backward(int64_t, int32_t, const int32_t *, const void *const *, const void *const *, const void *,
                       void *const *, void *, void *, void *, int32_t, int32_t, void *);
 int nvol_nan_scan(const float *, int64_t, const int64_t *, int32_t, int64_t *, void *);
+int nvol_train_tc_scatter(const float *, const float *, int64_t, int64_t, const int64_t *, const int64_t *,
+                          const int64_t *, const uint8_t *, int32_t, int32_t, float *, void *);
 
 int64_t nvol_train_workspace_bytes(int64_t b, int32_t n_levels, int32_t n_feat, int32_t n_neurons, int32_t n_hidden,
                                    int32_t mode) {
@@ -125,8 +145,18 @@ int nvol_train_fwd_bwd(const float *coords, const float *targets, int64_t b, int
     st = nvol_mlp_backward(b, nl, widths, wptr, (const void *const *)acts, dpred, gptr, dfeat, s0, s1, relu_out, 4,
                            stream);
     if (st) return st;
-    st = nvol_grid_encode_bwd_coords(coords, dfeat, b, level_off, level_res, level_entries, level_dense, m, n,
-                                     grads, 4, g_deterministic, stream);
+    st = NVOL_EINVAL;
+    if (!g_deterministic) {
+        // float-atomic mode: the training engine's scatter (shared-memory coarse levels, merged
+        // corner pairs) on the transposed dL/dfeat; shapes it does not take fall through
+        transpose_kernel<<<dim3((unsigned)((b + 31) / 32), (unsigned)((m * n + 31) / 32)), dim3(32, 8), 0, s>>>(
+            dfeat, s0, b, m * n);
+        st = nvol_train_tc_scatter(coords, s0, b, b, level_off, level_res, level_entries, level_dense, m, n, grads,
+                                   stream);
+    }
+    if (st != NVOL_OK)  // ordered mode: the sort-based fold, bit-identical to the reference's serial scatter
+        st = nvol_grid_encode_bwd_coords(coords, dfeat, b, level_off, level_res, level_entries, level_dense, m, n,
+                                         grads, 4, g_deterministic, stream);
     if (st == NVOL_OK && nan_state) st = nvol_nan_scan(grads, off, starts, nl + 1 < 16 ? nl + 1 : 16, nan_state, stream);
     (void)s;
     return st;
