@@ -1070,6 +1070,7 @@ constexpr int M4_THREADS = M4_WARPS * 32;
 struct Tc4Shape {
     int nin, ninp, nn, nh, accw, slots, relu_out, loss_kind;
     int split;  // 1: split-fp16 forward (hi*W_hi + lo*W_hi + hi*W_lo); 0: plain fp16 forward (hi*W_hi)
+    int rr;     // 1: the MMA warp serves the slots in round-robin order, blocking on each (no polling)
     uint32_t o_w[MAX_NH], o_wl[MAX_NH], o_wout, o_dwout, o_p[M4_SLOTS], o_q[M4_SLOTS], smem_bytes, half_bytes;
     uint32_t xhalf, t_acc[M4_SLOTS], t_dw[MAX_NH], t_alloc;
     uint32_t img_bytes;              // the packed weight image [0, img_bytes) of shared memory (pack_w4)
@@ -1093,6 +1094,14 @@ static int build_shape4(Tc4Shape &s, int m, int n, int nn, int nh, int relu_out,
     s.relu_out = relu_out;
     s.loss_kind = loss_kind;
     s.split = mlp_split_enabled() ? 1 : 0;
+    {
+        static int rr = -1;  // NVOL_MMA_RR=0: the polling MMA issuer (A/B measurements)
+        if (rr < 0) {
+            const char *e = getenv("NVOL_MMA_RR");
+            rr = (e && e[0] == '0') ? 0 : 1;
+        }
+        s.rr = rr;
+    }
     if (nh < 1 || nh > MAX_NH || !(nn == 16 || nn == 32 || nn == 64)) return 0;
     if (s.ninp > 2 * nn || s.ninp > 128) return 0;
     s.accw = max(nn, s.ninp);
@@ -1333,9 +1342,15 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                 if ((done >> t) & 1u) continue;
                 const int p = ph[t];
                 bool ok = true;
-                if ((started >> t) & 1u) ok = mbar_test(&bar_op[t], (par_op >> t) & 1u);
-                if (ok && p == 0) ok = mbar_test(&bar_x[t], (par_x >> t) & 1u);
-                if (ok && p >= NH) ok = mbar_test(&bar_h[t], (par_h >> t) & 1u);
+                if (sh.rr) {  // slots progress in lockstep: wait for this one instead of polling all
+                    if ((started >> t) & 1u) tc::mbar_wait(&bar_op[t], (par_op >> t) & 1u);
+                    if (p == 0) tc::mbar_wait(&bar_x[t], (par_x >> t) & 1u);
+                    if (p >= NH) tc::mbar_wait(&bar_h[t], (par_h >> t) & 1u);
+                } else {
+                    if ((started >> t) & 1u) ok = mbar_test(&bar_op[t], (par_op >> t) & 1u);
+                    if (ok && p == 0) ok = mbar_test(&bar_x[t], (par_x >> t) & 1u);
+                    if (ok && p >= NH) ok = mbar_test(&bar_h[t], (par_h >> t) & 1u);
+                }
                 if (!__all_sync(0xffffffffu, ok)) continue;
                 if ((started >> t) & 1u) par_op ^= 1u << t;
                 if (p == 0) par_x ^= 1u << t;
