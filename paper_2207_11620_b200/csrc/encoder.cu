@@ -171,34 +171,86 @@ __global__ void det_keys_kernel(const float *__restrict__ coords, int64_t b, con
     }
 }
 
+// the contribution w_k * dL/dfeat of every sorted (i, l, c) corner, in sorted order (parallel;
+// the same xmul the serial scatter does)
 template <int N>
-__global__ void det_fold_kernel(const float *__restrict__ coords, const float *__restrict__ dl,
-                                int64_t total, const GridTables tab,
-                                const uint32_t *__restrict__ keys, const uint32_t *__restrict__ ids,
-                                float *__restrict__ grad) {
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= total) return;
-    uint32_t key = keys[p];
-    if (p > 0 && keys[p - 1] == key) return;  // not the head of a run
+__global__ void det_values_kernel(const float *__restrict__ coords, const float *__restrict__ dl, int64_t total,
+                                  const GridTables tab, const uint32_t *__restrict__ ids, float *__restrict__ vals) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= total) return;
     const int m = tab.n_levels;
+    const uint32_t id = ids[q];
+    const int k = id & 7;
+    const int64_t il = id >> 3;
+    const int64_t i = il / m;
+    const int l = (int)(il - i * m);
+    const Cell<float> c = cell_of<float>(coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], tab.res[l]);
+    const float w = corner_weight<float>(c, k);
+    const float *d = dl + i * (int64_t)m * N + (int64_t)l * N;
+#pragma unroll
+    for (int f = 0; f < N; ++f) vals[q * N + f] = xmul(w, d[f]);
+}
+
+constexpr int DET_LONG = 32;  // runs longer than this are folded by a warp (det_fold_long_kernel)
+
+// one thread per run head: fold the run's contributions in order into its row (short runs);
+// long runs go to a list for det_fold_long_kernel
+template <int N>
+__global__ void det_fold_kernel(int64_t total, const uint32_t *__restrict__ keys, const float *__restrict__ vals,
+                                float *__restrict__ grad, uint32_t *__restrict__ long_heads,
+                                uint32_t *__restrict__ n_long) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= total) return;
+    const uint32_t key = keys[p];
+    if (p > 0 && keys[p - 1] == key) return;  // not the head of a run
+    if (p + DET_LONG < total && keys[p + DET_LONG] == key) {
+        long_heads[atomicAdd(n_long, 1u)] = (uint32_t)p;
+        return;
+    }
     float acc[N];
     float *g = grad + (int64_t)key * N;
 #pragma unroll
     for (int f = 0; f < N; ++f) acc[f] = g[f];
-    for (int64_t q = p; q < total && keys[q] == key; ++q) {
-        uint32_t id = ids[q];
-        int k = id & 7;
-        int64_t il = id >> 3;
-        int64_t i = il / m;
-        int l = (int)(il - i * m);
-        Cell<float> c = cell_of<float>(coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], tab.res[l]);
-        float w = corner_weight<float>(c, k);
-        const float *d = dl + i * (int64_t)m * N + (int64_t)l * N;
+    for (int64_t q = p; q < total && keys[q] == key; ++q)
 #pragma unroll
-        for (int f = 0; f < N; ++f) acc[f] = xadd(acc[f], xmul(w, d[f]));
-    }
+        for (int f = 0; f < N; ++f) acc[f] = xadd(acc[f], vals[q * N + f]);
 #pragma unroll
     for (int f = 0; f < N; ++f) g[f] = acc[f];
+}
+
+// one warp per long run: the lanes load 32 contributions at a time (coalesced) and lane 0 folds
+// them in order through shuffles -- the same sequence of xadds as the serial scatter
+template <int N>
+__global__ void det_fold_long_kernel(int64_t total, const uint32_t *__restrict__ keys, const float *__restrict__ vals,
+                                     float *__restrict__ grad, const uint32_t *__restrict__ long_heads,
+                                     const uint32_t *__restrict__ n_long) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const uint32_t cnt = *n_long;
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < cnt; w += nw) {
+        const int64_t p = long_heads[w];
+        const uint32_t key = keys[p];
+        float acc[N];
+        float *g = grad + (int64_t)key * N;
+#pragma unroll
+        for (int f = 0; f < N; ++f) acc[f] = g[f];
+        for (int64_t q0 = p;; q0 += 32) {
+            const int64_t q = q0 + lane;
+            const bool in = q < total && keys[q] == key;
+            float v[N];
+#pragma unroll
+            for (int f = 0; f < N; ++f) v[f] = in ? vals[q * N + f] : 0.0f;
+            const unsigned ballot = __ballot_sync(0xffffffffu, in);
+            const int nin = __popc(ballot);  // the run's positions are a prefix of the chunk
+            for (int j = 0; j < nin; ++j)
+#pragma unroll
+                for (int f = 0; f < N; ++f) acc[f] = xadd(acc[f], __shfl_sync(0xffffffffu, v[f], j));
+            if (nin < 32) break;
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int f = 0; f < N; ++f) g[f] = acc[f];
+    }
 }
 
 static int launch_bwd_serial(const float *coords, const float *dl, int64_t b, const GridTables &tab,
@@ -212,18 +264,33 @@ static int launch_bwd_serial(const float *coords, const float *dl, int64_t b, co
     size_t temp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr, (int)total, 0, key_bits, s);
-    size_t bytes = 4 * (size_t)total * 4 + temp_bytes;
+    const int nf = tab.n_feat;
+    size_t bytes = (5 + (size_t)nf) * (size_t)total * 4 + 256 + temp_bytes;
     if (cudaMallocAsync((void **)&buf, bytes, s) != cudaSuccess) return check_launch("det scatter alloc");
     uint32_t *k0 = buf, *v0 = buf + total, *k1 = buf + 2 * total, *v1 = buf + 3 * total;
-    void *temp = buf + 4 * total;
+    uint32_t *heads = buf + 4 * total;
+    float *vals = reinterpret_cast<float *>(buf + 5 * total);
+    uint32_t *n_long = buf + (5 + nf) * total;
+    void *temp = n_long + 64;
+    cudaMemsetAsync(n_long, 0, 4, s);
     det_keys_kernel<<<grid_for(b * tab.n_levels, 256), 256, 0, s>>>(coords, b, tab, k0, v0);
     cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k0, k1, v0, v1, (int)total, 0, key_bits, s);
     unsigned grid = grid_for(total, 256);
-    switch (tab.n_feat) {
-        case 1: det_fold_kernel<1><<<grid, 256, 0, s>>>(coords, dl, total, tab, k1, v1, grad); break;
-        case 2: det_fold_kernel<2><<<grid, 256, 0, s>>>(coords, dl, total, tab, k1, v1, grad); break;
-        case 4: det_fold_kernel<4><<<grid, 256, 0, s>>>(coords, dl, total, tab, k1, v1, grad); break;
-        default: det_fold_kernel<8><<<grid, 256, 0, s>>>(coords, dl, total, tab, k1, v1, grad); break;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    switch (nf) {
+#define DET_FOLD(NFV)                                                                                         \
+    case NFV:                                                                                                 \
+        det_values_kernel<NFV><<<grid, 256, 0, s>>>(coords, dl, total, tab, v1, vals);                       \
+        det_fold_kernel<NFV><<<grid, 256, 0, s>>>(total, k1, vals, grad, heads, n_long);                      \
+        det_fold_long_kernel<NFV><<<(unsigned)(sms * 8), 256, 0, s>>>(total, k1, vals, grad, heads, n_long);  \
+        break;
+        DET_FOLD(1)
+        DET_FOLD(2)
+        DET_FOLD(4)
+        default: DET_FOLD(8)
+#undef DET_FOLD
     }
     cudaFreeAsync(buf, s);
     return check_launch("grid_encode_bwd_deterministic");
