@@ -234,18 +234,28 @@ __global__ void det_fold_long_kernel(int64_t total, const uint32_t *__restrict__
         float *g = grad + (int64_t)key * N;
 #pragma unroll
         for (int f = 0; f < N; ++f) acc[f] = g[f];
-        for (int64_t q0 = p;; q0 += 32) {
-            const int64_t q = q0 + lane;
-            const bool in = q < total && keys[q] == key;
-            float v[N];
+        // 8 chunks of 32 contributions per round trip: the loads of a round are all in flight at once
+        constexpr int CH = 8;
+        bool more = true;
+        for (int64_t q0 = p; more; q0 += 32 * CH) {
+            bool in[CH];
+            float v[CH][N];
 #pragma unroll
-            for (int f = 0; f < N; ++f) v[f] = in ? vals[q * N + f] : 0.0f;
-            const unsigned ballot = __ballot_sync(0xffffffffu, in);
-            const int nin = __popc(ballot);  // the run's positions are a prefix of the chunk
-            for (int j = 0; j < nin; ++j)
+            for (int c = 0; c < CH; ++c) {
+                const int64_t q = q0 + c * 32 + lane;
+                in[c] = q < total && keys[q] == key;
 #pragma unroll
-                for (int f = 0; f < N; ++f) acc[f] = xadd(acc[f], __shfl_sync(0xffffffffu, v[f], j));
-            if (nin < 32) break;
+                for (int f = 0; f < N; ++f) v[c][f] = in[c] ? vals[q * N + f] : 0.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                if (!more) break;
+                const int nin = __popc(__ballot_sync(0xffffffffu, in[c]));  // a prefix of the chunk
+                for (int j = 0; j < nin; ++j)
+#pragma unroll
+                    for (int f = 0; f < N; ++f) acc[f] = xadd(acc[f], __shfl_sync(0xffffffffu, v[c][f], j));
+                if (nin < 32) more = false;
+            }
         }
         if (lane == 0)
 #pragma unroll
