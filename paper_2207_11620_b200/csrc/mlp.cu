@@ -20,8 +20,9 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
                                                    int64_t lda, const T *__restrict__ B, int64_t ldb,
                                                    T *__restrict__ C, int64_t ldc, int accumulate, int relu,
                                                    T *__restrict__ partials) {
-    __shared__ T As[16][64 + 1];
-    __shared__ T Bs[16][64 + 1];
+    // rows padded to 68 elements: 16-byte aligned vector reads of a thread's 4 consecutive m / n
+    __shared__ __align__(16) T As[16][64 + 4];
+    __shared__ __align__(16) T Bs[16][64 + 4];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
     const int64_t kchunk = (K + gridDim.z - 1) / gridDim.z;
@@ -51,10 +52,17 @@ __global__ void __launch_bounds__(256) gemm_kernel(int64_t M, int64_t N, int64_t
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) {
             T a[4], b[4];
+            if constexpr (sizeof(T) == 4) {
+                const float4 av = *reinterpret_cast<const float4 *>(&As[kk][ty * 4]);
+                const float4 bv = *reinterpret_cast<const float4 *>(&Bs[kk][tx * 4]);
+                a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
+                b[0] = bv.x; b[1] = bv.y; b[2] = bv.z; b[3] = bv.w;
+            } else {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) a[r] = As[kk][ty * 4 + r];
+                for (int r = 0; r < 4; ++r) a[r] = As[kk][ty * 4 + r];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) b[r] = Bs[kk][tx * 4 + r];
+                for (int r = 0; r < 4; ++r) b[r] = Bs[kk][tx * 4 + r];
+            }
 #pragma unroll
             for (int r = 0; r < 4; ++r)
 #pragma unroll
