@@ -76,9 +76,25 @@ def macrocell_build(fld, n_g: int = DEFAULT_CELL_SIZE) -> MacroCellGrid:
 
 
 def macrocell_from_model(model, n_g: int = DEFAULT_CELL_SIZE, chunk: int = 0) -> MacroCellGrid:
-    """Ranges from the model decoded at voxel centres (macrocell.py:84-98)."""
+    """Ranges from the model decoded at voxel centres (macrocell.py:84-98).
+
+    A NeuralModel is decoded on the device; any other object with the reference's
+    `dims` + `eval_fused(coords)` protocol is evaluated through that method, in chunks of
+    `chunk` voxel centres computed exactly as the reference does, and the ranges are
+    taken on the device."""
+    from .model import NeuralModel
     from .trainer import decode_brick
     dx, dy, dz = model.dims
+    if not isinstance(model, NeuralModel):
+        step = int(chunk) if chunk else 262144
+        zz, yy, xx = np.meshgrid(np.arange(dz), np.arange(dy), np.arange(dx), indexing="ij")
+        coords = np.stack([(xx.ravel() + 0.5) / dx, (yy.ravel() + 0.5) / dy, (zz.ravel() + 0.5) / dz],
+                          axis=1).astype(np.float32)
+        vals = np.empty(dx * dy * dz, dtype=np.float32)
+        for s in range(0, coords.shape[0], step):
+            v = model.eval_fused(coords[s:s + step])
+            vals[s:s + step] = v.cpu().numpy() if isinstance(v, torch.Tensor) else np.asarray(v, np.float32)
+        return _ranges(torch.from_numpy(vals.reshape(dz, dy, dx)).to(_lib.device()), (dx, dy, dz), n_g, clip=True)
     vals = torch.empty((dz, dy, dx), dtype=torch.float32, device=model.flat_params.device)
     decode_brick(model, (dx, dy, dz), 0, dz, vals, mode="centres64")
     return _ranges(vals, (dx, dy, dz), n_g, clip=True)

@@ -341,3 +341,21 @@ def test_pathtrace_wavefront_equals_megakernel(scene):
         np.testing.assert_array_equal(a, b)
         assert s1[0].evals == s2[0].evals
         assert s1[0].violations == s2[0].violations
+
+
+def test_macrocell_from_model_duck_typed(nv):
+    """macrocell_from_model accepts any object with the reference's dims + eval_fused protocol
+    (macrocell.py:84-98; the reference's test_macrocell.py::test_from_model_axis_order)."""
+    from paper_2207_11620_b200.macrocell import macrocell_from_model
+
+    class Stub:
+        dims = (6, 4, 5)
+
+        def eval_fused(self, coords):
+            return coords[:, 0].astype(np.float32)  # value = x coordinate
+
+    g = macrocell_from_model(Stub(), n_g=2, chunk=17)
+    lo, hi = g.value_lo.cpu().numpy(), g.value_hi.cpu().numpy()
+    for cx in range(3):
+        assert np.allclose(lo[:, :, cx], np.float32((max(2 * cx - 1, 0) + 0.5) / 6))
+        assert np.allclose(hi[:, :, cx], np.float32((min(2 * cx + 2, 5) + 0.5) / 6))
