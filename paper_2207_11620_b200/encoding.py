@@ -13,6 +13,8 @@ outside the B200 hot path: make_encoder raises ConfigError for them.
 """
 from __future__ import annotations
 
+from contextlib import contextmanager
+
 import math
 from dataclasses import dataclass
 
@@ -44,6 +46,17 @@ def set_deterministic(flag: bool) -> None:
 
 def deterministic() -> bool:
     return _deterministic
+
+
+@contextmanager
+def deterministic_mode(flag: bool = True):
+    """set_deterministic(flag) for the duration of a block, then the previous mode."""
+    prev = _deterministic
+    set_deterministic(flag)
+    try:
+        yield
+    finally:
+        set_deterministic(prev)
 
 
 @dataclass(frozen=True)
