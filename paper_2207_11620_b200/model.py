@@ -354,12 +354,20 @@ class NeuralModel:
         if not self._use_kernels():
             return self._train_step_generic(coords, targets)
         c, t = self._stage_batch(coords, targets)
-        loss_sum = torch.zeros(1, dtype=torch.float64, device=c.device)
+        if getattr(self, "_ts_bufs", None) is None:
+            # the step's loss accumulator and one pinned read-back slot for [loss bits, NaN state]
+            self._ts_bufs = (torch.zeros(1, dtype=torch.float64, device=c.device),
+                             torch.zeros(3, dtype=torch.int64).pin_memory())
+        loss_sum, back = self._ts_bufs
+        loss_sum.zero_()
         ns = self._nan_state()
         self.fwd_bwd_device(c, t, loss_sum, nan_state=ns)
         self.adam_device(ns)
-        loss = float(loss_sum.item()) / c.shape[0]
-        lim = int(ns[0].item())
+        back[0:1].copy_(loss_sum.view(torch.int64), non_blocking=True)   # one D2H + one sync per call
+        back[1:3].copy_(ns, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        loss = float(back[0:1].view(torch.float64).item()) / c.shape[0]
+        lim = int(back[1])
         if lim != NAN_NONE:
             ns.copy_(torch.tensor([NAN_NONE, 0], dtype=torch.int64))
             raise self.nan_error(lim)
