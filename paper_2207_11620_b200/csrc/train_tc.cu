@@ -587,7 +587,11 @@ int pack_mlp_image(const float *wflat, int nin, int ninp, int nn, int nh, const 
 __device__ unsigned long long g_tl[4096];
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
+#ifdef NVOL_TIMELINE_CLOCK  // SM cycle counter (cheaper to read; stamps of CTA 0 share one SM)
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+#else
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+#endif
     return t;
 }
 #define TL(slot, val)                                              \
@@ -1064,7 +1068,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
 // CUDA cores (warp transpose-reduce + shared atomics).  The MMA warp polls the
 // slots' barriers without blocking and serves whichever slot is ready.
 constexpr int M4_SLOTS = 4;
-constexpr int M4_WARPS = 4 * M4_SLOTS + 1;  // 4 epilogue warps per slot (one per TMEM lane quarter) + MMA
+constexpr int M4_MMA_WARPS = 2;  // up to this many MMA issuers (launch: NVOL_MMA_WARPS, default 2); warp m
+                                  // serves the slots t with t % (issuers) == m
+constexpr int M4_WARPS = 4 * M4_SLOTS + M4_MMA_WARPS;  // 4 epilogue warps per slot (one per TMEM lane quarter) + MMA
 constexpr int M4_THREADS = M4_WARPS * 32;
 
 struct Tc4Shape {
@@ -1283,7 +1289,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
         tc::mbar_arrive_expect_tx(&bar_w, sh.img_bytes);
         tc::bulk_g2s(smem, wimg, sh.img_bytes, &bar_w);
     }
-    for (int q = tid; q < 4 * M4_SLOTS * NN; q += M4_THREADS) reinterpret_cast<float *>(smem + sh.o_dwout)[q] = 0.0f;
+    for (int q = tid; q < 4 * M4_SLOTS * NN; q += blockDim.x) reinterpret_cast<float *>(smem + sh.o_dwout)[q] = 0.0f;
     __syncthreads();
     tc::mbar_wait(&bar_w, 0);
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, sh.t_alloc);
@@ -1292,6 +1298,22 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     __syncthreads();  // (the weight staging area is dead from here: the X loads below overwrite it)
     tc::fence_after();
     const uint32_t tmem = tmem_base_sh;
+    // zero the dW accumulators (every dW MMA then accumulates, so the issuer warps' chains into
+    // one dW_j may interleave: the tensor pipe serialises their read-modify-writes,
+    // tools/micro/mma_shared_acc.cu) -- the 16 epilogue warps, lane quarter x column group
+    if (warp < 4 * M4_SLOTS) {
+        const int q = warp & 3, grp = warp >> 2;
+        const uint32_t dw0 = (uint32_t)S * sh.accw, ncol = (uint32_t)(NINP + (NH - 1) * NN);
+        const uint32_t z = 0;
+        for (uint32_t c = (uint32_t)grp * 8; c < ncol; c += 8 * M4_SLOTS)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                             tmem + ((uint32_t)(q * 32) << 16) + dw0 + c), "r"(z)
+                         : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
     auto load_x = [&](int t, int64_t tile) {  // X hi -> P[t], X lo -> Q[t] (split forward only)
         const uint8_t *src = xtiles + tile * xtile_bytes;
         tc::mbar_arrive_expect_tx(&bar_x[t], (sh.split ? 2 : 1) * sh.xhalf);
@@ -1311,7 +1333,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     }
     const int nph = 2 * NH;
 
-    if (warp == 4 * M4_SLOTS) {
+    if (warp >= 4 * M4_SLOTS) {
         // ================================================================ MMA issuer (polls, never blocks on one slot)
         // The whole warp runs the loop converged, every decision is a warp vote and every
         // operand address is computed arithmetically from kernel parameters, so the state and
@@ -1321,14 +1343,15 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
         const uint32_t sbase = tc::smem_u32(smem);
         const uint32_t w1 = 4u * NN * NINP, wst = 4u * NN * NN, wlo1 = 2u * NN * NN;  // o_w / o_wl by layer
         const uint32_t dw0 = (uint32_t)S * sh.accw;
-        uint32_t par_x = 0, par_h = 0, par_op = 0, started = 0, done = 0, dw_started = 0;
+        const int mw = warp - 4 * M4_SLOTS, nmw = (int)(blockDim.x >> 5) - 4 * M4_SLOTS;  // issuer mw of nmw
+        uint32_t par_x = 0, par_h = 0, par_op = 0, started = 0, done = 0;
         int64_t kt[M4_SLOTS];
         int ph[M4_SLOTS];
 #pragma unroll
         for (int t = 0; t < M4_SLOTS; ++t) {
             kt[t] = 0;
             ph[t] = 0;
-            if (t >= S || tile_of(t, 0) >= ntiles) done |= 1u << t;
+            if (t >= S || t % nmw != mw || tile_of(t, 0) >= ntiles) done |= 1u << t;
         }
         const uint32_t idesc_f = tc::make_idesc(128, NN, 0, 0);
 #ifdef NVOL_TIMELINE
@@ -1342,10 +1365,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                 if ((done >> t) & 1u) continue;
                 const int p = ph[t];
                 bool ok = true;
-                if (sh.rr) {  // slots progress in lockstep: wait for this one instead of polling all
-                    if ((started >> t) & 1u) tc::mbar_wait(&bar_op[t], (par_op >> t) & 1u);
-                    if (p == 0) tc::mbar_wait(&bar_x[t], (par_x >> t) & 1u);
-                    if (p >= NH) tc::mbar_wait(&bar_h[t], (par_h >> t) & 1u);
+                if (sh.rr) {  // slots progress in lockstep: wait (suspended) for this one instead of polling all
+                    if ((started >> t) & 1u) tc::mbar_wait_sleep(&bar_op[t], (par_op >> t) & 1u);
+                    if (p == 0) tc::mbar_wait_sleep(&bar_x[t], (par_x >> t) & 1u);
+                    if (p >= NH) tc::mbar_wait_sleep(&bar_h[t], (par_h >> t) & 1u);
                 } else {
                     if ((started >> t) & 1u) ok = mbar_test(&bar_op[t], (par_op >> t) & 1u);
                     if (ok && p == 0) ok = mbar_test(&bar_x[t], (par_x >> t) & 1u);
@@ -1358,7 +1381,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                 started |= 1u << t;
                 tc::fence_after();
 #ifdef NVOL_TIMELINE
-                if (lane == 0) TL(2 * (mma_n & 511), gtime());
+                if (lane == 0) TL(2 * ((2 * mma_n + mw) & 511), gtime());
 #endif
                 const uint32_t acc = tmem_u + (uint32_t)t * sh.accw;
                 const uint32_t pb = sbase + sh.o_p[0] + 2u * (uint32_t)t * sh.half_bytes, qb = pb + sh.half_bytes;
@@ -1391,22 +1414,19 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                     const uint64_t bd1 = tc::make_desc(qb, (win / 8) * 128, 128);
                     const uint64_t ad2 = tc::make_desc(pb, 128, (NN / 8) * 128);
                     const uint64_t bd2 = tc::make_desc(sbase + ow, (win / 8) * 128, 128);
-                    const uint32_t first = ((dw_started >> j) & 1u) ? 1u : 0u;
                     if (elect_one()) {
-                        for (int k = 0; k < TILE / 16; ++k)
-                            tc::mma_f16(tdw, ad1 + (uint64_t)(k * 2 * (NN / 8) * 8), bd1 + (uint64_t)(k * 2 * (win / 8) * 8), id1,
-                                        (first || k > 0) ? 1 : 0);
+                        for (int k = 0; k < TILE / 16; ++k)  // dW_j was zeroed in the prologue: always accumulate
+                            tc::mma_f16(tdw, ad1 + (uint64_t)(k * 2 * (NN / 8) * 8), bd1 + (uint64_t)(k * 2 * (win / 8) * 8), id1, 1);
                         for (int k = 0; k < NN / 16; ++k)
                             tc::mma_f16(acc, ad2 + (uint64_t)(k * 16), bd2 + (uint64_t)(k * 2 * (win / 8) * 8), id2, k > 0);
                         tc::mma_commit(&bar_acc[t]);
                     }
-                    dw_started |= 1u << j;
                 }
                 __syncwarp();
                 issued = true;
 #ifdef NVOL_TIMELINE
                 if (lane == 0)
-                    TL(2 * (mma_n & 511) + 1, ((unsigned long long)t << 60) | ((unsigned long long)p << 52) | (gtime() & ((1ull << 52) - 1)));
+                    TL(2 * ((2 * mma_n + mw) & 511) + 1, ((unsigned long long)t << 60) | ((unsigned long long)p << 52) | (gtime() & ((1ull << 52) - 1)));
                 ++mma_n;
 #endif
                 if (p + 1 == nph) {
@@ -2038,7 +2058,13 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         if (p.v4) {
             const int64_t h_tile = (int64_t)(nh - 1) * p.sh4.h_tile_bytes;
             if (c == 0) cudaStreamWaitEvent(s, ss.packed, 0);  // the weight image (forked before the encode)
-            mlp_tc4_kernel<<<gm, M4_THREADS, p.sh4.smem_bytes, s>>>(
+            static int nmw = -1;  // MMA-issuing warps (NVOL_MMA_WARPS=1: one issuer for all slots)
+            if (nmw < 0) {
+                const char *e = getenv("NVOL_MMA_WARPS");
+                nmw = e ? atoi(e) : M4_MMA_WARPS;
+                nmw = nmw < 1 ? 1 : (nmw > M4_MMA_WARPS ? M4_MMA_WARPS : nmw);
+            }
+            mlp_tc4_kernel<<<gm, (4 * M4_SLOTS + nmw) * 32, p.sh4.smem_bytes, s>>>(
                 xtc, targets + r0, nb, 1.0 / (double)b_global, dscale, p.sh4, params + woff, loss_sum, dfeat + r0, b,
                 grads + woff, ws + p.off_h + t0 * h_tile, g_dbg.pred ? g_dbg.pred + r0 : nullptr, nan_state, woff,
                 ws + p.off_img);
