@@ -477,6 +477,15 @@ def run_ours(args):
     rend = None
     if not args.no_render:
         rend = render_bench(torch, args, rank, world)
+        wt = rend.get("wavefront_tensor") if rend else None
+        if wt:
+            # the frame against the L2 random-gather ceiling of its field evaluations: every
+            # evaluation at an arbitrary position gathers 16 levels x 8 corners (whole frame,
+            # marching and compaction included; the evaluator kernel alone is in DESIGN.md)
+            g = wt["evals_per_s"] * 16 * 8 / 1e9
+            rend["roofline"] = {"bound": "l2 gather rate (field evaluations)", "gathers_per_eval": 128,
+                                "achieved_gather_gops": g, "peak_gather_gops": l2_gather, "frac": g / l2_gather,
+                                "basis": "wavefront_tensor frame: evaluations/s x 128 corner gathers, whole frame"}
     c5 = None
     if not args.no_cfg5:
         c5 = cfg5_bench(torch, args, rank, world)
