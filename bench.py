@@ -274,7 +274,10 @@ def run_ours(args):
         ev[1].record(stream)
 
     exchange = None
-    if world > 1:
+    if world > 1 and getattr(pipe, "peer", None) is not None:
+        exchange = {"kind": "peer-memory fused reduce-scatter + Adam + all-gather (csrc/dp_peer.cu, NVOL_DP_PEER=1)",
+                    "ms": None, "note": "inside the step (one kernel per rank); ms_per_step includes it"}
+    elif world > 1:
         snap = model.flat_params.clone()
         t_x = float(_event_ms(torch, exchange_fn)[0])
         model.flat_params.copy_(snap)

@@ -265,6 +265,26 @@ int nvol_set_stage_events(void *const *events, int32_t n);
  * No reference counterpart (trainer.py:61-77 samples serially). */
 int nvol_set_fork_event(void *event);
 
+/* Data-parallel exchange over peer memory (distributed.PeerExchange; NVOL_DP_PEER=1): the sharded
+ * optimizer's reduce-scatter -> Adam on this rank's slice -> all-gather as ONE kernel per rank that
+ * reads / writes the other ranks' flat buffers through their CUDA-IPC (NVLink P2P) mappings.
+ * Replaces dist.reduce_scatter + adam_step (network.py:160-183) + dist.all_gather of the NCCL
+ * path; the step's loss is the rank-ordered sum of the ranks' loss sums and the NaN limit their
+ * minimum.  Arrays of `world` device addresses (host int64): flat gradients, flat parameters,
+ * loss sums (double), NaN states (int64[2]) and step flags (int64[2]: ready, done) of every rank;
+ * [lo, hi) is this rank's slice of the flat buffer, m / v its own moment buffers.
+ *   nvol_dp_signal: own ready flag = step + 1 (after this rank's scatter);
+ *   nvol_dp_wait:   before a step, every rank's done flag >= step; zeroes the own loss sum. */
+int nvol_dp_signal(int64_t *own_flags, const int64_t *step_counter, const int64_t *nan_state, void *stream);
+int nvol_dp_wait(int32_t world, const int64_t *flags, const int64_t *step_counter, double *own_loss_acc,
+                 const int64_t *nan_state, void *stream);
+int nvol_dp_fused_adam(int32_t world, int32_t rank, const int64_t *grads, const int64_t *params,
+                       const int64_t *loss_accs, const int64_t *nan_states, const int64_t *flags, int64_t lo,
+                       int64_t hi, float *m, float *v, const float *sched, int64_t sched_len,
+                       int64_t *step_counter, float beta1, float one_minus_beta1, float beta2,
+                       float one_minus_beta2, float eps, float l2, int64_t *nan_state, double *losses,
+                       int64_t t0, int64_t cap, double inv_b, uint32_t *ticket, void *stream);
+
 /* Parity hooks for the tcgen05 training engine (tests only; all null in
  * production).  While set, nvol_train_fwd_bwd mode 1 additionally writes
  * feat  [b][n_levels*n_feat] f32: the hot encoder's fp32 features

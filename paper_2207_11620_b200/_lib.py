@@ -61,6 +61,10 @@ _SIGS = {
     "nvol_render_workspace_bytes": [I64, I32],
     "nvol_set_stage_events": [P, I32],
     "nvol_set_fork_event": [P],
+    "nvol_dp_signal": [P, P, P, P],
+    "nvol_dp_wait": [I32, P, P, P, P, P],
+    "nvol_dp_fused_adam": [I32, I32, P, P, P, P, P, I64, I64, P, P, P, I64, P, F32, F32, F32, F32, F32, F32, P, P,
+                           I64, I64, F64, P, P],
     "nvol_train_tc_debug": [P, P, P],
     "nvol_train_tc_scatter": [P, P, I64, I64, P, P, P, P, I32, I32, P, P],
     "nvol_l2_persist": [I64],

@@ -159,3 +159,67 @@ class DataParallelTrainer:
 
     def finish(self):
         return self.pipeline.finish()
+
+
+class PeerExchange:
+    """The sharded optimizer's exchange over peer memory (NVOL_DP_PEER=1; csrc/dp_peer.cu).
+
+    Instead of NCCL reduce-scatter -> Adam on the slice -> NCCL all-gather, every rank maps the
+    other ranks' flat gradient / parameter buffers, loss sums, NaN states and step flags (CUDA IPC
+    handles exchanged once through the process group; NVLink P2P between the GPUs of a node) and
+    one kernel per rank (nvol_dp_fused_adam) sums its slice of all the gradients in rank order,
+    updates it and writes it into every rank's parameters.  Step flags in peer memory order the
+    ranks (nvol_dp_signal after the scatter, nvol_dp_wait before the next step), so the whole
+    exchange lives inside the captured step graph with no collective launch.
+
+    host_sync (NVOL_DP_PEER_HOSTSYNC=1, tests): synchronise the device and barrier the ranks
+    before the fused kernel and before each step, so the flags are already set when the kernels
+    read them (several ranks time-sharing ONE GPU must not spin on each other)."""
+
+    def __init__(self, model, pipe, rank: int, world: int, group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+        if world > 8:
+            raise ConfigError("the peer exchange supports up to 8 ranks")
+        dev = model.flat_params.device
+        self.rank, self.world, self.group = rank, world, group
+        self.flags = torch.full((2,), int(pipe.t0), dtype=torch.int64, device=dev)
+        mine = [model.flat_grads_padded, model.flat_params_padded, pipe.acc, pipe.nan_state, self.flags]
+        handles = [reduce_tensor(t) for t in mine]
+        everyone = [None] * world
+        torch.cuda.synchronize()
+        dist.all_gather_object(everyone, handles, group=group)
+        self.peers = []                       # keeps the peer mappings alive
+        cols = [[0] * world for _ in range(len(mine))]
+        for j in range(world):
+            ts = mine if j == rank else [fn(*args) for fn, args in everyone[j]]
+            self.peers.append(ts)
+            for a, t in enumerate(ts):
+                cols[a][j] = t.data_ptr()
+        from . import _lib
+        self.grads, self.params, self.accs, self.nans, self.flag_ptrs = (_lib.host_i64(c) for c in cols)
+        self.host_sync = os.environ.get("NVOL_DP_PEER_HOSTSYNC", "0") == "1"
+        dist.barrier(group=group)
+
+    def _sync(self) -> None:
+        if self.host_sync:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
+
+    def before_step(self, pipe) -> None:
+        """Every rank's slices of the previous step are written; the loss sum is free."""
+        from . import _lib
+        self._sync()
+        _lib.call("nvol_dp_wait", self.world, self.flag_ptrs, _lib.ptr(pipe.counter), _lib.ptr(pipe.acc),
+                  _lib.ptr(pipe.nan_state), _lib.stream())
+
+    def exchange_and_update(self, model, pipe) -> None:
+        """After this rank's scatter: signal, then the fused reduce-scatter + Adam + all-gather."""
+        from . import _lib
+        _lib.call("nvol_dp_signal", _lib.ptr(self.flags), _lib.ptr(pipe.counter), _lib.ptr(pipe.nan_state),
+                  _lib.stream())
+        self._sync()
+        _lib.call("nvol_dp_fused_adam", self.world, self.rank, self.grads, self.params, self.accs, self.nans,
+                  self.flag_ptrs, pipe.slo, pipe.shi, _lib.ptr(model.flat_m), _lib.ptr(model.flat_v),
+                  _lib.ptr(pipe.sched), pipe.sched.numel() // 3, _lib.ptr(pipe.counter), *pipe.adam_consts,
+                  _lib.ptr(pipe.nan_state), _lib.ptr(pipe.losses), pipe.t0, pipe.capacity, 1.0 / pipe.B,
+                  _lib.ptr(pipe.ticket), _lib.stream())

@@ -159,6 +159,11 @@ class StepPipeline:
                                   and model._tc_device() and os.environ.get("NVOL_FORK_AFTER_ENCODE", "1") != "0")
         self.fork_ev = torch.cuda.Event() if self.fork_after_encode else None
         self.fingerprint = pipeline_fingerprint(model)
+        # the sharded exchange over peer memory instead of NCCL (NVOL_DP_PEER=1, distributed.PeerExchange)
+        self.peer = None
+        if self.sharded and os.environ.get("NVOL_DP_PEER", "0") == "1":
+            from .distributed import PeerExchange
+            self.peer = PeerExchange(model, self, rank, world, group)
         self.work = torch.zeros(2 + 32, dtype=torch.int32, device=dev)   # NVOL_MAX_LEVELS
         if self.host_feed:
             self.copy_stream = torch.cuda.Stream(device=dev)
@@ -231,6 +236,8 @@ class StepPipeline:
     def _body(self, parity: int) -> None:
         m = self.model
         main = torch.cuda.current_stream()
+        if self.peer is not None:
+            self.peer.before_step(self)
         if self.host_feed:
             if self.mc_grid is not None:
                 from .macrocell import macrocell_update_online
@@ -258,6 +265,11 @@ class StepPipeline:
         else:
             m.fwd_bwd_device(c, t, self.acc, b_global=self.B, flags=TRAIN_PREENCODED if self.fused else 0,
                              nan_state=self.nan_state)
+        if self.peer is not None:
+            if self.overlap:
+                main.wait_stream(self.side)
+            self.peer.exchange_and_update(m, self)
+            return
         if self.sharded:
             import torch.distributed as dist
             from .distributed import allgather_shards, reduce_scatter_grads

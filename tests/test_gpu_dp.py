@@ -29,9 +29,10 @@ def _free_port():
     return p
 
 
-def _dp_worker(rank, world, port, sharded, out, steps=STEPS):
+def _dp_worker(rank, world, port, sharded, out, steps=STEPS, peer="0"):
     # NVOL_FUSED_TAIL=1 must not engage with the sharded optimizer (its step tail is the slice Adam)
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NVOL_DP_SHARDED=sharded, NVOL_FUSED_TAIL="1")
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), NVOL_DP_SHARDED=sharded, NVOL_FUSED_TAIL="1",
+                      NVOL_DP_PEER=peer, NVOL_DP_PEER_HOSTSYNC=peer)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     from paper_2207_11620_b200 import fields
@@ -43,16 +44,17 @@ def _dp_worker(rank, world, port, sharded, out, steps=STEPS):
     tr = DataParallelTrainer(model, InCoreSampler(fld, seed=1), capacity=steps, use_graph=False)
     assert tr.pipeline.sharded == (sharded == "1")
     assert not (tr.pipeline.sharded and tr.pipeline.fused)
+    assert (tr.pipeline.peer is not None) == (peer == "1")
     tr.step(steps)
     losses = tr.finish()
     out[rank] = (losses, model.flat_params.cpu().numpy(), model.flat_m.cpu().numpy(), model.opt.t)
     dist.destroy_process_group()
 
 
-def _run(sharded, steps=STEPS):
+def _run(sharded, steps=STEPS, peer="0"):
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
-    mp.spawn(_dp_worker, args=(2, _free_port(), sharded, out, steps), nprocs=2, join=True)
+    mp.spawn(_dp_worker, args=(2, _free_port(), sharded, out, steps, peer), nprocs=2, join=True)
     return dict(out)
 
 
@@ -91,3 +93,36 @@ def test_dp_two_ranks_match_single_process(nv):
         np.testing.assert_allclose(l0, h.losses, rtol=2e-2)
         np.testing.assert_allclose(p0, ref_p, rtol=0, atol=2e-3)
         np.testing.assert_allclose(m0, ref_m, rtol=0, atol=5e-4)
+
+
+@pytest.mark.timeout(600)
+def test_dp_peer_exchange_matches_single_process(nv):
+    """The exchange over peer memory (NVOL_DP_PEER=1, csrc/dp_peer.cu: one kernel per rank reads its
+    slice of both ranks' gradients through CUDA-IPC mappings, sums them in rank order, applies Adam
+    and writes the slice into both ranks' parameters; step flags in peer memory order the ranks).
+    Two ranks sharing this GPU (host-synchronised flags: NVOL_DP_PEER_HOSTSYNC=1): identical
+    parameters, moments and losses on both ranks, the single-process trajectory of the same global
+    batch (step 0 to 1e-6, one step's Adam update to the summation-order bound), and the same
+    result as the NCCL-path sharded optimizer up to gradient summation order."""
+    from paper_2207_11620_b200 import fields, trainer
+    from paper_2207_11620_b200.model import build_model
+    from paper_2207_11620_b200.sampler import InCoreSampler
+    model = build_model(CFG, dims=(32, 32, 32), seed=0)
+    fld = fields.rasterize("mlobb", (32, 32, 32))
+    h1 = trainer.train(model, InCoreSampler(fld, seed=1), steps=1)
+    one_p = model.flat_params.cpu().numpy()
+    model = build_model(CFG, dims=(32, 32, 32), seed=0)
+    h = trainer.train(model, InCoreSampler(fld, seed=1), steps=STEPS)
+    (l0, p0, m0, t0), (l1, p1, m1, t1) = (lambda o: (o[0], o[1]))(_run("1", steps=1, peer="1"))
+    np.testing.assert_array_equal(p0, p1)
+    assert l0[0] == pytest.approx(h1.losses[0], rel=1e-6)
+    d = np.abs(p0 - one_p)
+    assert (d <= 1e-6).mean() > 0.9999 and d.max() <= 2 * 0.005 + 1e-6, (d.max(), (d > 1e-6).sum())
+    out = _run("1", peer="1")
+    (l0, p0, m0, t0), (l1, p1, m1, t1) = out[0], out[1]
+    np.testing.assert_array_equal(p0, p1)
+    np.testing.assert_array_equal(m0, m1)
+    np.testing.assert_array_equal(l0, l1)
+    assert t0 == t1 == STEPS
+    assert l0[0] == pytest.approx(h.losses[0], rel=1e-6)
+    np.testing.assert_allclose(l0, h.losses, rtol=2e-2)
