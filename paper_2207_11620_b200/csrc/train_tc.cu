@@ -40,7 +40,10 @@ constexpr int MAX_NH = 8;
 // MMA-issuer warp that round-robins the slots' layer phases.
 constexpr int PP_EPI_WARPS = 16;
 constexpr int PP_THREADS = (PP_EPI_WARPS + 1) * 32;
-constexpr int SC_THREADS = 1024;
+#ifndef NVOL_SC_THREADS
+#define NVOL_SC_THREADS 1024
+#endif
+constexpr int SC_THREADS = NVOL_SC_THREADS;
 constexpr int SC_LG = 4;  // levels per scatter item
 constexpr uint32_t COARSE_BYTES = 48 * 1024;
 
