@@ -1645,16 +1645,8 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
         const int q = warp & 3, grp = warp >> 2;
         const int o = q * 32 + lane;
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-#ifdef NVOL_FLUSH_ROT
-        // every CTA flushes at once: each starts at a different layer, so the REDs of
-        // concurrent CTAs land on different gradient lines
-        for (int jj = 0; jj < NH; ++jj) {
-            const int j = (jj + (int)blockIdx.x) % NH;
-            const int64_t base = j == 0 ? 0 : (int64_t)NN * NIN + (int64_t)(j - 1) * NN * NN;
-#else
         int64_t base = 0;
         for (int j = 0; j < NH; ++j) {
-#endif
             const int win = (j == 0) ? NIN : NN;
             const int wacc = (j == 0) ? NINP : NN;
             int c0, nc;
@@ -1683,13 +1675,8 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                     }
                 }
             }
-#ifndef NVOL_FLUSH_ROT
             base += (int64_t)NN * win;
-#endif
         }
-#ifdef NVOL_FLUSH_ROT
-        const int64_t base = (int64_t)NN * NIN + (int64_t)(NH - 1) * NN * NN;
-#endif
         if (tid < NN) {
             float v = 0.0f;
             for (int w = 0; w < 4 * M4_SLOTS; ++w) v += reinterpret_cast<const float *>(smem + sh.o_dwout)[w * NN + tid];
