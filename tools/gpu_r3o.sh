@@ -1,4 +1,5 @@
 # A/B (same box): mlp_tc4 dW flush starting at a per-CTA layer (-DNVOL_FLUSH_ROT)
+# (the compile-time knob was removed after this measurement: DESIGN.md "dW flush order")
 export PYTHONUNBUFFERED=1
 for ex in "" "-DNVOL_FLUSH_ROT" "" "-DNVOL_FLUSH_ROT"; do
 touch paper_2207_11620_b200/csrc/train_tc.cu; make -s -C paper_2207_11620_b200/csrc EXTRA="$ex" 2>&1 | grep error

@@ -1,4 +1,5 @@
 # A/B (same box): mlp_tc4 dW flush as plain stores (timing bound only, wrong sums) (-DNVOL_FLUSH_STORE_EXPT)
+# (the compile-time knob was removed after this measurement: DESIGN.md "dW flush order")
 export PYTHONUNBUFFERED=1
 for ex in "" "-DNVOL_FLUSH_STORE_EXPT" "" "-DNVOL_FLUSH_STORE_EXPT"; do
 touch paper_2207_11620_b200/csrc/train_tc.cu; make -s -C paper_2207_11620_b200/csrc EXTRA="$ex" 2>&1 | grep error
