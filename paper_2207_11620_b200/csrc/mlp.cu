@@ -438,8 +438,14 @@ __global__ void nan_scan_kernel(const float *__restrict__ g, int64_t n, const Gr
 // (p, m, v, and g = 0).  The DMA engine keeps ~100 KB in flight per CTA without occupying
 // registers, which is what the HBM-bound update needs.  Same arithmetic, same NaN contract and
 // same step bookkeeping (ticket) as adam_step_kernel.
-constexpr int AD_CH = 2048;     // floats per array per chunk (8 KB)
-constexpr int AD_ST = 3;        // ring depth
+#ifndef NVOL_AD_CH
+#define NVOL_AD_CH 2048
+#endif
+#ifndef NVOL_AD_ST
+#define NVOL_AD_ST 3
+#endif
+constexpr int AD_CH = NVOL_AD_CH;  // floats per array per chunk (8 KB)
+constexpr int AD_ST = NVOL_AD_ST;  // ring depth
 constexpr int AD_THREADS = 256; // 2 float4 per thread per array per chunk
 
 __device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
