@@ -496,6 +496,18 @@ __global__ void __launch_bounds__(AD_THREADS) adam_tma_kernel(
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+#if defined(NVOL_ADAM_LAYOUT_EXPT)
+    // timing experiment only (tools/adam_layout.py): m / v (1) or p / m / v (2) interleaved in
+    // AD_CH-float blocks, so the chunk's optimizer state is one contiguous DRAM region
+    auto at = [&](int a, int64_t off) -> float * {
+        const int64_t blk = off / AD_CH;
+        if (NVOL_ADAM_LAYOUT_EXPT == 1 && a >= 2) return m + blk * 2 * AD_CH + (a == 3 ? AD_CH : 0);
+        if (NVOL_ADAM_LAYOUT_EXPT == 2 && a != 1) return p + blk * 3 * AD_CH + (a == 0 ? 0 : (a == 2 ? AD_CH : 2 * AD_CH));
+        return arr[a] + off;
+    };
+#else
+    auto at = [&](int a, int64_t off) -> float * { return arr[a] + off; };
+#endif
     auto issue = [&](int s, int64_t c) {  // thread 0: chunk c -> stage s
         const int64_t off = c * AD_CH;
         const uint32_t bytes = (uint32_t)(min((int64_t)AD_CH, nbody - off) * 4);
@@ -503,7 +515,7 @@ __global__ void __launch_bounds__(AD_THREADS) adam_tma_kernel(
                      "r"(4 * bytes)
                      : "memory");
         for (int a = 0; a < 4; ++a)
-            bulk_g2s_hint(ring + ((int64_t)s * 4 + a) * AD_CH, arr[a] + off, bytes, &full[s], a == 1 ? keep : first);
+            bulk_g2s_hint(ring + ((int64_t)s * 4 + a) * AD_CH, at(a, off), bytes, &full[s], a == 1 ? keep : first);
     };
     int64_t c = blockIdx.x;
     if (tid == 0)
@@ -550,7 +562,7 @@ __global__ void __launch_bounds__(AD_THREADS) adam_tma_kernel(
         __syncthreads();
         if (tid == 0) {
             const uint32_t bytes = (uint32_t)cnt * 4u;
-            for (int a = 0; a < 4; ++a) bulk_s2g_hint(arr[a] + off, ring + ((int64_t)s * 4 + a) * AD_CH, bytes, a == 1 ? keep : first);
+            for (int a = 0; a < 4; ++a) bulk_s2g_hint(at(a, off), ring + ((int64_t)s * 4 + a) * AD_CH, bytes, a == 1 ? keep : first);
             bulk_commit();
             const int64_t nc = c + (int64_t)AD_ST * gridDim.x;
             if (nc < nch) {
