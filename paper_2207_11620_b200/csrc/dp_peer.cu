@@ -95,9 +95,9 @@ __global__ void __launch_bounds__(256) dp_fused_adam_kernel(
         }
         for (int j = 0; j < G; ++j) __stcg(P.g[j] + q, 0.0f);
     }
+    __threadfence_system();  // every thread's peer stores, before the block's ticket / done flag
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
         if (atomicAdd(ticket, 1u) == gridDim.x - 1) {  // the last block: every block's writes are out
             __threadfence_system();
             *ticket = 0u;
