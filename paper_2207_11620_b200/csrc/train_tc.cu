@@ -1262,7 +1262,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     const uint8_t *__restrict__ xtiles, const float *__restrict__ targets, int64_t b, double inv_bglobal, float dscale,
     const Tc4Shape sh, const float *__restrict__ wflat, double *__restrict__ loss_sum, float *__restrict__ dfeat,
     int64_t stride, float *__restrict__ dw_grads, uint8_t *__restrict__ hscratch, float *__restrict__ dbg_pred,
-    int64_t *__restrict__ nan_state, int64_t woff, const uint8_t *__restrict__ wimg) {
+    int64_t *__restrict__ nan_state, int64_t woff, const uint8_t *__restrict__ wimg, float *__restrict__ dw_part) {
     if (nan_halted(nan_state)) return;  // NaN contract: a halted pipeline does no more work
 #ifdef NVOL_TIMELINE
     if (threadIdx.x == 0) TL(4002, gtime());
@@ -1641,6 +1641,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     if (threadIdx.x == 0) TL(4003, gtime());
 #endif
     const float unscale = 1.0f / (dscale * tc::kActScale);  // dW = (dscale*delta)^T (kActScale*H)
+    // dw_part: this CTA's dW as plain stores into its own partial row (summed in CTA order by
+    // scatter_kernel's prologue); every CTA REDing into the same 57 KB of gradient at once
+    // serialises on a few L2 slices (in-step MLP 37.9 -> 33.8 us, tools/gpu_r3t.sh)
+    float *const dw_out = dw_part ? dw_part + (int64_t)blockIdx.x * sh.w_floats : dw_grads;
     if (warp < 4 * M4_SLOTS) {
         const int q = warp & 3, grp = warp >> 2;
         const int o = q * 32 + lane;
@@ -1660,17 +1664,26 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
 #pragma unroll
                         for (int e = 0; e < 16; ++e)
                             if (c + e < win && isnan(v[e])) nan_at = min(nan_at, woff + base);  // W_j's group
-                        float *g = dw_grads + base + (int64_t)o * win + c;
+                        float *g = dw_out + base + (int64_t)o * win + c;
                         if (c + 16 <= win && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
 #pragma unroll
-                            for (int e = 0; e < 16; e += 4)
-                                atomicAdd(reinterpret_cast<float4 *>(g + e),
-                                          make_float4(v[e] * unscale, v[e + 1] * unscale, v[e + 2] * unscale,
-                                                      v[e + 3] * unscale));
+                            for (int e = 0; e < 16; e += 4) {
+                                const float4 w4 = make_float4(v[e] * unscale, v[e + 1] * unscale, v[e + 2] * unscale,
+                                                              v[e + 3] * unscale);
+                                if (dw_part)
+                                    *reinterpret_cast<float4 *>(g + e) = w4;
+                                else
+                                    atomicAdd(reinterpret_cast<float4 *>(g + e), w4);
+                            }
                         } else {
 #pragma unroll
                             for (int e = 0; e < 16; ++e)
-                                if (c + e < win) atomicAdd(g + e, v[e] * unscale);
+                                if (c + e < win) {
+                                    if (dw_part)
+                                        g[e] = v[e] * unscale;
+                                    else
+                                        atomicAdd(g + e, v[e] * unscale);
+                                }
                         }
                     }
                 }
@@ -1681,7 +1694,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             float v = 0.0f;
             for (int w = 0; w < 4 * M4_SLOTS; ++w) v += reinterpret_cast<const float *>(smem + sh.o_dwout)[w * NN + tid];
             if (isnan(v)) nan_at = min(nan_at, woff + base);
-            atomicAdd(dw_grads + base + tid, v * unscale);
+            if (dw_part)
+                dw_out[base + tid] = v * unscale;
+            else
+                atomicAdd(dw_grads + base + tid, v * unscale);
         }
     }
     if (nan_at != kNanNone) nan_mark(nan_state, nan_at);
@@ -1694,6 +1710,47 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
 }
 
 // ============================================================================ 3. scatter
+// mlp_tc4_kernel's per-CTA weight-gradient partials [n_part][w_floats] (dw_part), summed in CTA
+// order into the flat gradient (dw[q] += sum_r part[r][q]) by dw_reduce_kernel, which runs on a side
+// stream beside the scatter (its 256-thread CTAs fit in the registers the scatter leaves free):
+// each CTA owns DWR_Q consecutive q, its warps split the partial rows into DWR_G groups (128-byte
+// loads), the group sums are folded in group order.  A NaN in a sum marks its parameter group
+// (W_0 .. W_{nh-1}, W_out) as the MLP kernel's own flush would have.
+struct DwPartials {
+    const float *part;  // nullptr: the MLP kernel REDs its dW itself
+    float *dw;          // the flat gradient's MLP weights (grads + woff)
+    int n_part, w_floats, nin, nn, nh;
+    int64_t woff;
+};
+constexpr int DWR_Q = 32, DWR_G = 8;
+
+__global__ void __launch_bounds__(DWR_Q * DWR_G) dw_reduce_kernel(const DwPartials d, int64_t *__restrict__ nan_state) {
+    if (nan_halted(nan_state)) return;
+    __shared__ float s_red[DWR_G][DWR_Q];
+    const int ql = threadIdx.x % DWR_Q, grp = threadIdx.x / DWR_Q;
+    const int q = (int)blockIdx.x * DWR_Q + ql;
+    const int rpg = (d.n_part + DWR_G - 1) / DWR_G;
+    float acc = 0.0f;
+    if (q < d.w_floats) {
+        const int r1 = min(d.n_part, (grp + 1) * rpg);
+#pragma unroll 4
+        for (int r = grp * rpg; r < r1; ++r) acc += __ldcg(d.part + (int64_t)r * d.w_floats + q);
+    }
+    s_red[grp][ql] = acc;
+    __syncthreads();
+    if (threadIdx.x < DWR_Q && q < d.w_floats) {
+        float v = 0.0f;
+#pragma unroll
+        for (int g2 = 0; g2 < DWR_G; ++g2) v += s_red[g2][ql];
+        d.dw[q] += v;
+        if (isnan(v)) {
+            const int a = d.nn * d.nin, hid = a + (d.nh - 1) * d.nn * d.nn;
+            const int start = q < a ? 0 : (q < hid ? a + ((q - a) / (d.nn * d.nn)) * d.nn * d.nn : hid);
+            nan_mark(nan_state, d.woff + start);
+        }
+    }
+}
+
 template <int NF>
 __global__ void __launch_bounds__(SC_THREADS, 1) scatter_kernel(const float *__restrict__ coords,
                                                                 const float *__restrict__ dfeat, int64_t b,
@@ -1838,7 +1895,7 @@ struct TcPlan {
     bool v4;  // mlp_tc4_kernel (four slots, folded split-fp16 accumulator) takes this shape
     int grid_mlp, grid_sc, n_coarse, coarse_floats, nchunks, rep_floats, rep;
     size_t sc_smem() const { return (size_t)(rep * rep_floats + (coarse_floats - rep_floats)) * 4; }
-    int64_t ntiles, chunk_tiles, off_x, off_dfeat, off_h, off_img, total;
+    int64_t ntiles, chunk_tiles, off_x, off_dfeat, off_h, off_img, off_dwp, total;
     float lo_scale() const { return v4 ? 1.0f : tc::kLoScale; }
 };
 
@@ -1923,7 +1980,8 @@ static int make_plan(TcPlan &p, int64_t b, const GridTables &tab, int nn, int nh
     p.off_dfeat = al(p.ntiles * TILE * p.sh.ninp * 4);  // hi + lo fp16 tiles
     p.off_h = p.off_dfeat + al(b * p.sh.nin * 4);      // mlp_tc4_kernel's activation scratch h_1..h_{nh-1}
     p.off_img = p.off_h + (p.v4 ? al(p.ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) : 0);  // packed weights
-    p.total = p.off_img + (p.v4 ? al(p.sh4.img_bytes) : 0) + 256;
+    p.off_dwp = p.off_img + (p.v4 ? al(p.sh4.img_bytes) : 0);  // mlp_tc4_kernel's per-CTA dW partials
+    p.total = p.off_dwp + (p.v4 ? al((int64_t)p.grid_mlp * p.sh4.w_floats * 4) : 0) + 256;
     return 1;
 }
 
@@ -1933,8 +1991,12 @@ int64_t train_tc_workspace(int64_t b, int m, int n, int nn, int nh) {
     const bool v4 = mlp4_enabled() && build_shape4(p.sh4, m, n, nn, nh, 1, 0);
     int64_t ntiles = (b + TILE - 1) / TILE;
     auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+    // (the same regions make_plan lays out; the dW partials sized for the largest MLP grid)
     return al(ntiles * TILE * p.sh.ninp * 4) + al(b * p.sh.nin * 4) +
-           (v4 ? al(ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) + al(p.sh4.img_bytes) : 0) + 256;
+           (v4 ? al(ntiles * (int64_t)(nh - 1) * p.sh4.h_tile_bytes) + al(p.sh4.img_bytes) +
+                     al((int64_t)num_sms() * p.sh4.w_floats * 4)
+               : 0) +
+           256;
 }
 
 static cudaEvent_t g_stage_events[8];
@@ -1951,8 +2013,9 @@ static TcDebug g_dbg;
 static int g_stage_events_n = 0;
 
 struct SideStreams {
-    cudaStream_t enc = nullptr, sc = nullptr, pk = nullptr;
-    cudaEvent_t fork, join_enc, join_sc, enc_done[MAX_CHUNKS], mlp_done[MAX_CHUNKS], fork_pk, packed;
+    cudaStream_t enc = nullptr, sc = nullptr, pk = nullptr, red = nullptr;
+    cudaEvent_t fork, join_enc, join_sc, enc_done[MAX_CHUNKS], mlp_done[MAX_CHUNKS], fork_pk, packed, fork_red,
+        red_done;
 };
 
 static SideStreams &side_streams() {
@@ -1961,6 +2024,9 @@ static SideStreams &side_streams() {
         cudaStreamCreateWithFlags(&ss.enc, cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&ss.sc, cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&ss.pk, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&ss.red, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&ss.fork_red, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ss.red_done, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ss.fork_pk, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ss.packed, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
@@ -2028,6 +2094,23 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         cudaStreamWaitEvent(ss.sc, ss.fork, 0);
     }
     const int64_t tile_bytes = 2 * TILE * p.sh.ninp * 2;
+    // one MLP launch (no chunking): its per-CTA dW partials are folded by the scatter's prologue
+    // (NVOL_DW_PARTIALS=0: the MLP kernel REDs its dW into the gradient itself)
+    static int dwp_env = -1;
+    if (dwp_env < 0) {
+        const char *e = getenv("NVOL_DW_PARTIALS");
+        dwp_env = (e && e[0] == '0') ? 0 : 1;
+    }
+    DwPartials dwp{};
+    if (p.v4 && nc == 1 && !only && dwp_env) {
+        dwp.part = reinterpret_cast<const float *>(ws + p.off_dwp);
+        dwp.dw = grads + woff;
+        dwp.w_floats = (int)p.sh4.w_floats;
+        dwp.nin = p.sh4.nin;
+        dwp.nn = nn;
+        dwp.nh = nh;
+        dwp.woff = woff;
+    }
     for (int c = 0; c < nc; ++c) {
         const int64_t t0 = c * p.chunk_tiles;
         const int64_t r0 = t0 * TILE;
@@ -2070,7 +2153,11 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
             mlp_tc4_kernel<<<gm, (4 * M4_SLOTS + nmw) * 32, p.sh4.smem_bytes, s>>>(
                 xtc, targets + r0, nb, 1.0 / (double)b_global, dscale, p.sh4, params + woff, loss_sum, dfeat + r0, b,
                 grads + woff, ws + p.off_h + t0 * h_tile, g_dbg.pred ? g_dbg.pred + r0 : nullptr, nan_state, woff,
-                ws + p.off_img);
+                ws + p.off_img, dwp.part ? const_cast<float *>(dwp.part) : nullptr);
+            if (dwp.part) {  // the partials are folded beside the scatter (launched after it, below)
+                dwp.n_part = gm;
+                cudaEventRecord(ss.fork_red, s);
+            }
         } else {
             mlp_tc_kernel<<<gm, PP_THREADS, p.sh.smem_bytes, s>>>(xtc, targets + r0, nb, 1.0 / (double)b_global, dscale,
                                                                   p.sh, params + woff, loss_sum, dfeat + r0, b,
@@ -2103,6 +2190,17 @@ int train_tc_launch(const float *coords, const float *targets, int64_t b, int64_
         }
         st = check_launch("scatter_kernel");
         if (st) return st;
+        if (dwp.part) {
+            // after the scatter's launch, so its one-per-SM CTAs are placed first and the small
+            // reduction CTAs fill the registers they leave free
+            cudaStreamWaitEvent(ss.red, ss.fork_red, 0);
+            dw_reduce_kernel<<<(unsigned)((dwp.w_floats + DWR_Q - 1) / DWR_Q), DWR_Q * DWR_G, 0, ss.red>>>(dwp,
+                                                                                                  nan_state);
+            st = check_launch("dw_reduce_kernel");
+            if (st) return st;
+            cudaEventRecord(ss.red_done, ss.red);
+            cudaStreamWaitEvent(s, ss.red_done, 0);  // the weight gradient is complete
+        }
         if (prof) cudaEventRecord(pev[3], s);
     }
     if (nc > 1) {
