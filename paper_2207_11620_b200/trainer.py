@@ -318,14 +318,16 @@ class StepPipeline:
         if self.fused:
             return 4    # sample (next step's), MLP, scatter, Adam + next encode
         # sample (next step's, overlapped), the MLP weight image (pack_w4, side stream; four-slot
-        # MLP kernel), nchunks x (encode, MLP, scatter), Adam step
+        # MLP kernel), nchunks x (encode, MLP, scatter), the dW fold, Adam step
         # (chunk plan of train_tc.cu make_plan: NVOL_TRAIN_CHUNKS, default 1)
         ntiles = (self.b + 127) // 128
         nc = max(1, min(int(os.environ.get("NVOL_TRAIN_CHUNKS", "1")), 4, ntiles))
         ct = (ntiles + nc - 1) // nc
         nc = (ntiles + ct - 1) // ct
         pack = 0 if os.environ.get("NVOL_MLP4", "1") == "0" else 1
-        return 1 + pack + 3 * nc + 1
+        # the MLP's dW partials folded beside the scatter (dw_reduce_kernel; one MLP launch only)
+        fold = 1 if (pack and nc == 1 and os.environ.get("NVOL_DW_PARTIALS", "1") != "0") else 0
+        return 1 + pack + 3 * nc + fold + 1
 
     def step(self, n: int = 1) -> None:
         """Enqueue n steps (no host synchronisation)."""
