@@ -1522,8 +1522,14 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             // the slot's 4 warps wrote h_1..h_{NH-1} to the scratch (generic stores): proxy fence, then
             // order them before the bulk copies that stream them back (bar.sync: CTA memory barrier).
             // Done once per tile, phases after the stores, so the fence finds them retired.
+#ifdef NVOL_TIMELINE
+            if (leader && k == 0) TL(3000 + t * 8 + 0, gtime());
+#endif
             fence_proxy_async_global();
             named_sync(1 + t, 128);
+#ifdef NVOL_TIMELINE
+            if (leader && k == 0) TL(3000 + t * 8 + 1, gtime());
+#endif
             if (leader) load_h(t, tile, NH - 1);  // Q (h_{NH-1} lo) is free: stream h_{NH-1} back for dW_{NH-1}
             float outp = 0.0f;
             for (int c = 0; c < NN; c += 16) {
@@ -1533,6 +1539,9 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
 #pragma unroll
                 for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * relu_nan(v[e]);
             }
+#ifdef NVOL_TIMELINE
+            if (leader && k == 0) TL(3000 + t * 8 + 2, gtime());
+#endif
             const float o = outp * (1.0f / tc::kActScale);
             const float pred = sh.relu_out ? relu_nan(o) : o;
             if (dbg_pred && valid) dbg_pred[row] = pred;  // parity hook (nvol_train_tc_debug)
@@ -1553,6 +1562,9 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             }
             lsum += sl;
             const float gd = gf * dscale;
+#ifdef NVOL_TIMELINE
+            if (leader && k == 0) TL(3000 + t * 8 + 3, gtime());
+#endif
             for (int c = 0; c < NN; c += 16) {
                 float v[16], dv[16];
                 tc::tmem_ld16(tacc + c, v);

@@ -42,3 +42,8 @@ for t in range(4):
         if w == 0:
             break
         print(f"slot {t} epi {k:2d}: acc-ready {(w - t0) / 1e3:7.2f}  release {(r - t0) / 1e3 if r else -1:7.2f}")
+for t in range(4):
+    m = [int(a[3000 + t * 8 + i]) for i in range(4)]
+    if m[0]:
+        print(f"slot {t} last fwd epilogue: start {(m[0] - t0) / 1e3:7.2f}  fence+sync {(m[1] - m[0]) / 1e3:5.2f}  "
+              f"output dot {(m[2] - m[1]) / 1e3:5.2f}  loss {(m[3] - m[2]) / 1e3:5.2f}")
