@@ -1279,6 +1279,12 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     int64_t nan_at = kNanNone;
     auto tile_of = [&](int t, int64_t k) -> int64_t { return (int64_t)blockIdx.x + ((int64_t)t + (int64_t)S * k) * gridDim.x; };
 
+    auto load_x = [&](int t, int64_t tile) {  // X hi -> P[t], X lo -> Q[t] (split forward only)
+        const uint8_t *src = xtiles + tile * xtile_bytes;
+        tc::mbar_arrive_expect_tx(&bar_x[t], (sh.split ? 2 : 1) * sh.xhalf);
+        tc::bulk_g2s(smem + sh.o_p[t], src, sh.xhalf, &bar_x[t]);
+        if (sh.split) tc::bulk_g2s(smem + sh.o_q[t], src + sh.xhalf, sh.xhalf, &bar_x[t]);
+    };
     // ---- prologue: the packed weight image (pack_w4) by one bulk copy
     if (tid == 0) {
         for (int t = 0; t < M4_SLOTS; ++t) {
@@ -1291,6 +1297,10 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
         tc::fence_mbar_init();
         tc::mbar_arrive_expect_tx(&bar_w, sh.img_bytes);
         tc::bulk_g2s(smem, wimg, sh.img_bytes, &bar_w);
+        // the slots' first X tiles right behind it (the slot buffers lie past the image): their
+        // latency overlaps the TMEM allocation and the dW zeroing below
+        for (int t = 0; t < S; ++t)
+            if (tile_of(t, 0) < ntiles) load_x(t, tile_of(t, 0));
     }
     for (int q = tid; q < 4 * M4_SLOTS * NN; q += blockDim.x) reinterpret_cast<float *>(smem + sh.o_dwout)[q] = 0.0f;
     __syncthreads();
@@ -1298,7 +1308,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     if (warp == 0) tc::tmem_alloc(&tmem_base_sh, sh.t_alloc);
     tc::fence_proxy_async();
     tc::fence_before();
-    __syncthreads();  // (the weight staging area is dead from here: the X loads below overwrite it)
+    __syncthreads();
     tc::fence_after();
     const uint32_t tmem = tmem_base_sh;
     // zero the dW accumulators (every dW MMA then accumulates, so the issuer warps' chains into
@@ -1317,12 +1327,6 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    auto load_x = [&](int t, int64_t tile) {  // X hi -> P[t], X lo -> Q[t] (split forward only)
-        const uint8_t *src = xtiles + tile * xtile_bytes;
-        tc::mbar_arrive_expect_tx(&bar_x[t], (sh.split ? 2 : 1) * sh.xhalf);
-        tc::bulk_g2s(smem + sh.o_p[t], src, sh.xhalf, &bar_x[t]);
-        if (sh.split) tc::bulk_g2s(smem + sh.o_q[t], src + sh.xhalf, sh.xhalf, &bar_x[t]);
-    };
     // h_j (j >= 1: the scratch written by the forward epilogue; j = 0: the X hi tile) -> Q[t]
     auto load_h = [&](int t, int64_t tile, int j) {
         const uint8_t *src = j == 0 ? xtiles + tile * xtile_bytes : hscratch + tile * hs_tile + (int64_t)(j - 1) * sh.h_tile_bytes;
@@ -1330,10 +1334,6 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
         tc::mbar_arrive_expect_tx(&bar_h[t], bytes);
         tc::bulk_g2s(smem + sh.o_q[t], src, bytes, &bar_h[t]);
     };
-    if (tid == 0) {
-        for (int t = 0; t < S; ++t)
-            if (tile_of(t, 0) < ntiles) load_x(t, tile_of(t, 0));
-    }
     const int nph = 2 * NH;
 
     if (warp >= 4 * M4_SLOTS) {
