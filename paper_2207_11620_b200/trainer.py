@@ -315,8 +315,11 @@ class StepPipeline:
         """Kernels of one step from this library (for the bench's gpu_launches)."""
         if self.train_mode == 0:
             return 1 + 5 + 3 * (self.model.mlp.config.n_hidden_layers + 1) + 1 + 1
+        pack = 0 if os.environ.get("NVOL_MLP4", "1") == "0" else 1
         if self.fused:
-            return 4    # sample (next step's), MLP, scatter, Adam + next encode
+            # sample (next step's), the weight image, MLP, the dW fold, scatter, Adam + next encode
+            fold = 1 if (pack and os.environ.get("NVOL_DW_PARTIALS", "1") != "0") else 0
+            return 1 + pack + 2 + fold + 1
         # sample (next step's, overlapped), the MLP weight image (pack_w4, side stream; four-slot
         # MLP kernel), nchunks x (encode, MLP, scatter), the dW fold, Adam step
         # (chunk plan of train_tc.cu make_plan: NVOL_TRAIN_CHUNKS, default 1)
@@ -324,7 +327,6 @@ class StepPipeline:
         nc = max(1, min(int(os.environ.get("NVOL_TRAIN_CHUNKS", "1")), 4, ntiles))
         ct = (ntiles + nc - 1) // nc
         nc = (ntiles + ct - 1) // ct
-        pack = 0 if os.environ.get("NVOL_MLP4", "1") == "0" else 1
         # the MLP's dW partials folded beside the scatter (dw_reduce_kernel; one MLP launch only)
         fold = 1 if (pack and nc == 1 and os.environ.get("NVOL_DW_PARTIALS", "1") != "0") else 0
         return 1 + pack + 3 * nc + fold + 1

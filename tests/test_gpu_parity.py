@@ -539,7 +539,7 @@ def test_fused_adam_encode_tail(nv, name, batch, monkeypatch):
         pipe = model._pipeline
         assert pipe.fused == (fused == "1") and pipe.done == 10 and model.opt.t == 10
         if fused == "1":
-            assert pipe.launches_per_step() == 4
+            assert pipe.launches_per_step() == 6   # sample, pack_w4, MLP, dW fold, scatter, Adam + encode
             torch.cuda.synchronize()
             assert int(pipe.work.abs().sum().item()) == 0        # work words re-armed
             # the encoder tile buffer (hi + lo fp16 tiles) at the head of the workspace; the rest is
