@@ -77,22 +77,54 @@ __global__ void __launch_bounds__(256) dp_fused_adam_kernel(
     const int64_t lim = s_lim;
     const int64_t t = tc >= sched_len ? sched_len - 1 : tc;
     const float lr = sched[3 * t], c1 = sched[3 * t + 1], c2 = sched[3 * t + 2];
-    for (int64_t q = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += (int64_t)gridDim.x * blockDim.x) {
-        float g = 0.0f;
-        for (int j = 0; j < G; ++j) g = xadd(g, __ldcv(P.g[j] + q));  // the ranks' contributions in rank order
-        if (q < lim && isnan(g)) {
+    // one element: the ranks' contributions summed in rank order, the update written to every rank
+    auto one = [&](int64_t q, float g, float &pp) -> bool {
+        if (q >= lim) return false;
+        if (isnan(g)) {
             // a NaN that only the sum produces (inf + -inf across ranks): every rank's limit drops,
             // so all of them halt at their next step
             for (int j = 0; j < G; ++j) atomicMin(reinterpret_cast<unsigned long long *>(const_cast<int64_t *>(P.nan[j])),
                                                   (unsigned long long)q);
-        } else if (q < lim) {
-            float pp = __ldcv(P.p[0] + q);  // this rank's own current value (P.p[0] is this rank)
-            float mm = m[q], vv = v[q];
-            adam_one<float>(pp, g, mm, vv, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
-            m[q] = mm;
-            v[q] = vv;
-            for (int j = 0; j < G; ++j) __stcg(P.p[j] + q, pp);
+            return false;
         }
+        float mm = m[q], vv = v[q];
+        adam_one<float>(pp, g, mm, vv, lr, b1, omb1, b2, omb2, c1, c2, eps, l2);
+        m[q] = mm;
+        v[q] = vv;
+        return true;
+    };
+    // 16-byte body over NVLink (the slice bounds are 128-byte aligned except the last rank's end;
+    // every rank's flat buffers share their alignment), scalar tail
+    const int64_t body_end = lo + ((hi - lo) & ~(int64_t)3);
+    const bool vec = ((reinterpret_cast<uintptr_t>(P.g[0] + lo) | reinterpret_cast<uintptr_t>(P.p[0] + lo)) & 15) == 0;
+    const int64_t vend = vec ? body_end : lo;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = lo + 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); q < vend; q += 4 * stride) {
+        float4 g4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        for (int j = 0; j < G; ++j) {
+            const float4 c = __ldcv(reinterpret_cast<const float4 *>(P.g[j] + q));
+            g4 = make_float4(xadd(g4.x, c.x), xadd(g4.y, c.y), xadd(g4.z, c.z), xadd(g4.w, c.w));
+        }
+        float4 p4 = __ldcv(reinterpret_cast<const float4 *>(P.p[0] + q));  // this rank's own current value
+        const bool u0 = one(q, g4.x, p4.x), u1 = one(q + 1, g4.y, p4.y), u2 = one(q + 2, g4.z, p4.z),
+                   u3 = one(q + 3, g4.w, p4.w);
+        if (u0 & u1 & u2 & u3) {
+            for (int j = 0; j < G; ++j) __stcg(reinterpret_cast<float4 *>(P.p[j] + q), p4);
+        } else {
+            const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+            const bool uv[4] = {u0, u1, u2, u3};
+            for (int e = 0; e < 4; ++e)
+                if (uv[e])
+                    for (int j = 0; j < G; ++j) __stcg(P.p[j] + q + e, pv[e]);
+        }
+        for (int j = 0; j < G; ++j) __stcg(reinterpret_cast<float4 *>(P.g[j] + q), make_float4(0.0f, 0.0f, 0.0f, 0.0f));
+    }
+    for (int64_t q = vend + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += stride) {
+        float g = 0.0f;
+        for (int j = 0; j < G; ++j) g = xadd(g, __ldcv(P.g[j] + q));
+        float pp = __ldcv(P.p[0] + q);
+        if (one(q, g, pp))
+            for (int j = 0; j < G; ++j) __stcg(P.p[j] + q, pp);
         for (int j = 0; j < G; ++j) __stcg(P.g[j] + q, 0.0f);
     }
     __threadfence_system();  // every thread's peer stores, before the block's ticket / done flag
@@ -169,7 +201,7 @@ int nvol_dp_fused_adam(int32_t world, int32_t rank, const int64_t *grads, const 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t n = hi - lo;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, (int64_t)sms * 8));
     dp_fused_adam_kernel<<<grid, 256, 0, as_stream(stream)>>>(P, world, lo, hi, m, v, sched, sched_len, step_counter,
                                                               beta1, one_minus_beta1, beta2, one_minus_beta2, eps, l2,
                                                               nan_state, losses, t0, cap, inv_b, ticket,
