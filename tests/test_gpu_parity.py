@@ -559,7 +559,12 @@ def test_fused_adam_encode_tail(nv, name, batch, monkeypatch):
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "odd"])
 def test_tensor_inference_matches_exact(nv, name):
     """tcgen05 Phi evaluator / decode vs the bit-exact evaluator on a trained-ish
-    model: half-precision bar (1e-2 relative, floor 1e-2 * max)."""
+    model, at the SURVEY §8(c) half-precision bar: |tc - ex| <= 1e-2 * max(|ex|, 1e-3)
+    (measured ~1e-4: most outputs are ReLU zeros, so the absolute floor matters)."""
+    def bar(got, want):
+        got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+        return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-3)))
+
     from paper_2207_11620_b200 import trainer
     from paper_2207_11620_b200.model import build_model
     z = golden(f"encode_{name}.npz")
@@ -569,12 +574,12 @@ def test_tensor_inference_matches_exact(nv, name):
     c = r.random((5000, 3)).astype(np.float32)
     ex = model.eval_fused(c)
     tc = model.eval_device(torch.from_numpy(c).cuda(), "tensor").cpu().numpy()
-    assert rel_err(tc, ex, floor=1e-2) < 1e-2
+    assert bar(tc, ex) < 1e-2
     model.infer_mode = "tensor"
     d1 = trainer.decode(model, dims=(20, 16, 12)).data.cpu().numpy()
     model.infer_mode = "exact"
     d0 = trainer.decode(model, dims=(20, 16, 12)).data.cpu().numpy()
-    assert rel_err(d1, d0, floor=1e-2) < 1e-2
+    assert bar(d1, d0) < 1e-2
 
 
 def test_deterministic_training_is_bitwise_repeatable(nv):
