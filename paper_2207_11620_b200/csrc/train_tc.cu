@@ -1465,6 +1465,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             __syncwarp();
 #ifdef NVOL_TIMELINE
             if (leader) TL(1024 + t * 256 + 2 * (epi_n & 127) + 1, gtime());
+            if (lane == 0 && t < 2 && epi_n < 8) TL(3200 + t * 64 + epi_n * 4 + q, gtime());  // per-warp release
             ++epi_n;
 #endif
             if (lane == 0) mbar_arrive(&bar_op[t]);

@@ -47,3 +47,8 @@ for t in range(4):
     if m[0]:
         print(f"slot {t} last fwd epilogue: start {(m[0] - t0) / 1e3:7.2f}  fence+sync {(m[1] - m[0]) / 1e3:5.2f}  "
               f"output dot {(m[2] - m[1]) / 1e3:5.2f}  loss {(m[3] - m[2]) / 1e3:5.2f}")
+for t in range(2):
+    for e in range(8):
+        w = [int(a[3200 + t * 64 + e * 4 + q]) for q in range(4)]
+        if w[0]:
+            print(f"slot {t} epi {e}: warp releases " + " ".join(f"{(x - t0) / 1e3:7.2f}" for x in w))
