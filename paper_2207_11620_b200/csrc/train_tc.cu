@@ -1068,8 +1068,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1) mlp_tc_kernel(
 // and Q = the activation h_j the dW_j MMA needs, streamed back by a bulk copy from a
 // global scratch the forward epilogue wrote it to (L2-resident, 48 KB per tile);
 // (3) ReLU masks live in registers (bits), and dW_out = sum g*h_NH is reduced on
-// CUDA cores (warp transpose-reduce + shared atomics).  The MMA warp polls the
-// slots' barriers without blocking and serves whichever slot is ready.
+// CUDA cores (warp transpose-reduce + shared atomics).  Two MMA warps each serve
+// half of the slots in round-robin order, blocking on each slot's barriers
+// (Tc4Shape::rr; NVOL_MMA_RR=0: poll all slots and serve whichever is ready).
 constexpr int M4_SLOTS = 4;
 constexpr int M4_MMA_WARPS = 2;  // up to this many MMA issuers (launch: NVOL_MMA_WARPS, default 2); warp m
                                   // serves the slots t with t % (issuers) == m
@@ -1337,7 +1338,7 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
     const int nph = 2 * NH;
 
     if (warp >= 4 * M4_SLOTS) {
-        // ================================================================ MMA issuer (polls, never blocks on one slot)
+        // ================================================================ MMA issuers (round-robin over their slots)
         // The whole warp runs the loop converged, every decision is a warp vote and every
         // operand address is computed arithmetically from kernel parameters, so the state and
         // the descriptors stay warp-uniform (uniform registers): one elected lane issues each
