@@ -15,6 +15,7 @@
 // the NaN limit the minimum of the ranks' NaN states (nvol.h "NaN contract"), so every rank
 // records the same loss, applies the same prefix and halts together.
 #include <algorithm>
+#include <cstdio>
 #include <utility>
 
 #include "common.cuh"
@@ -40,6 +41,26 @@ __device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
     asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// wait until *flag >= want (system-scope acquire); a peer that never gets there (a rank that died)
+// traps the kernel after kPeerTimeoutNs instead of hanging the GPU
+constexpr uint64_t kPeerTimeoutNs = 60ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void wait_flag(const int64_t *flag, int64_t want, unsigned sleep_ns) {
+    if (ld_acquire_sys(flag) >= want) return;
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_sys(flag) < want) {
+        __nanosleep(sleep_ns);
+        if (global_ns() - t0 > kPeerTimeoutNs) {
+            printf("nvol dp_peer: a peer's step flag stayed below %lld for 60 s\n", (long long)want);
+            __trap();
+        }
+    }
+}
+
 // own ready flag = step + 1, after this rank's gradient (scatter + MLP flush) is complete
 __global__ void dp_signal_kernel(int64_t *flags, const int64_t *counter, const int64_t *nan_state) {
     __threadfence_system();
@@ -52,8 +73,7 @@ __global__ void dp_wait_kernel(PeerSet P, int G, const int64_t *counter, double 
                                const int64_t *nan_state) {
     if (nan_halted(nan_state)) return;
     const int64_t k = *counter;
-    for (int j = 0; j < G; ++j)
-        while (ld_acquire_sys(P.ready[j] + 1) < k) __nanosleep(256);
+    for (int j = 0; j < G; ++j) wait_flag(P.ready[j] + 1, k, 256);
     *acc_own = 0.0;
 }
 
@@ -68,7 +88,7 @@ __global__ void __launch_bounds__(256) dp_fused_adam_kernel(
     if (threadIdx.x == 0) {
         int64_t lim = kNanNone;
         for (int j = 0; j < G; ++j) {
-            while (ld_acquire_sys(P.ready[j]) < tc + 1) __nanosleep(128);  // rank j's gradient of this step
+            wait_flag(P.ready[j], tc + 1, 128);  // rank j's gradient of this step
             lim = min(lim, ld_acquire_sys(P.nan[j]));
         }
         s_lim = lim;
