@@ -1539,7 +1539,13 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
                 tc::tmem_ld16(tacc + c, v);
                 tc::tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 16; ++e) outp += s_wout[c + e] * relu_nan(v[e]);
+                for (int e = 0; e < 16; e += 4) {  // (16-byte shared loads: s_wout is 128-byte aligned)
+                    const float4 w4 = *reinterpret_cast<const float4 *>(s_wout + c + e);
+                    outp += w4.x * relu_nan(v[e]);
+                    outp += w4.y * relu_nan(v[e + 1]);
+                    outp += w4.z * relu_nan(v[e + 2]);
+                    outp += w4.w * relu_nan(v[e + 3]);
+                }
             }
 #ifdef NVOL_TIMELINE
             if (leader && k == 0) TL(3000 + t * 8 + 2, gtime());
@@ -1568,13 +1574,21 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             if (leader && k == 0) TL(3000 + t * 8 + 3, gtime());
 #endif
             for (int c = 0; c < NN; c += 16) {
-                float v[16], dv[16];
+                float v[16], dv[16], wv[16];
+#pragma unroll
+                for (int e = 0; e < 16; e += 4) {  // (issued ahead of the TMEM load's latency)
+                    const float4 w4 = *reinterpret_cast<const float4 *>(s_wout + c + e);
+                    wv[e] = w4.x;
+                    wv[e + 1] = w4.y;
+                    wv[e + 2] = w4.z;
+                    wv[e + 3] = w4.w;
+                }
                 tc::tmem_ld16(tacc + c, v);
                 tc::tmem_wait_ld();
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
                     v[e] = relu_nan(v[e]);
-                    const float x = gd * s_wout[c + e];
+                    const float x = gd * wv[e];
                     dv[e] = v[e] > 0.0f ? x : x * 0.0f;
                 }
                 store_row_f16(pbuf, s, c, NN, dv, false);
