@@ -1718,6 +1718,9 @@ __global__ void __launch_bounds__(M4_THREADS, 1) mlp_tc4_kernel(
             }
             base += (int64_t)NN * win;
         }
+#ifdef NVOL_TIMELINE
+        if (lane == 0) TL(3600 + warp, gtime());  // per warp: dW rows out of TMEM and stored
+#endif
         if (tid < NN) {
             float v = 0.0f;
             for (int w = 0; w < 4 * M4_SLOTS; ++w) v += reinterpret_cast<const float *>(smem + sh.o_dwout)[w * NN + tid];

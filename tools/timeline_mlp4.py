@@ -52,3 +52,8 @@ for t in range(2):
         w = [int(a[3200 + t * 64 + e * 4 + q]) for q in range(4)]
         if w[0]:
             print(f"slot {t} epi {e}: warp releases " + " ".join(f"{(x - t0) / 1e3:7.2f}" for x in w))
+fl0 = int(a[4003])
+if fl0:
+    w1 = [int(a[3600 + w]) for w in range(18)]
+    print("flush, per warp (us after the flush start): dW out " +
+          " ".join(f"{(x - fl0) / 1e3:.2f}" if x else "-" for x in w1))
